@@ -1,0 +1,277 @@
+"""Generate golden vectors by RUNNING THE REFERENCE (development container only).
+
+    PYTHONPATH=/root/reference/pkg/src python tools/gen_golden.py [--only NAME ...]
+
+Writes tests/golden/*.npz.  The reference (bilevel-drive 0.1.0, pure numpy/scipy)
+is imported from /root/reference/pkg/src; it does not exist on the GPU box, so the
+vectors are committed and the tests read only the .npz files.
+
+Cases:
+  basis            W/Wd/Wdd, stage-1 + aug KKTs for the BASELINE basis (pkg/basis.py, pkg/batch_qp.py,
+                   pkg/projection.py:189-214)
+  lower_*          LowerLevelSolver.solve outputs (pkg/bilevel.py:217-225) on synthetic highway scenes
+  cem_c2           teacher-forced config-2 CEM trace (B=1000, N=4, n=150, q=100) via trace_hook
+                   (pkg/bilevel.py:269-270)
+  cem_small        free-running solve_bilevel with default_rng(3) (B=200, N=3) for the drop-in API
+"""
+
+from __future__ import annotations
+
+import argparse
+import math
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, "/root/reference/pkg/src")
+
+from bilevel_drive import batch_qp  # noqa: E402
+from bilevel_drive.basis import build_basis  # noqa: E402
+from bilevel_drive.batch_qp import TrackingWeights  # noqa: E402
+from bilevel_drive.behavior import ParamLayout  # noqa: E402
+from bilevel_drive.bench import bilevel_config_for, canonical_scene  # noqa: E402
+from bilevel_drive.bilevel import (  # noqa: E402
+    BiLevelConfig, LowerLevelSolver, SamplingDistribution, rank_samples, solve_bilevel,
+    update_distribution, upper_cost_batch,
+)
+from bilevel_drive.constraints import ConstraintSpec, PlanningScene  # noqa: E402
+from bilevel_drive.highway import RoadSpec, ScenarioConfig, spawn_world  # noqa: E402
+from bilevel_drive.planners import PlannerEnvConfig, build_scene  # noqa: E402
+from bilevel_drive.projection import ProjectionConfig  # noqa: E402
+
+OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden")
+
+
+def env_for(n_obs=10, m=100, T=5.0, iters=100, obstacle_range=120.0):
+    return PlannerEnvConfig(horizon=T, num_samples=m, max_obstacles=n_obs, proj_iters=iters,
+                            obstacle_range=obstacle_range)
+
+
+def highway_scene(env, basis, lanes, density, vehicles, seed):
+    world = spawn_world(ScenarioConfig(RoadSpec(lane_count=lanes), density=density, vehicle_count=vehicles,
+                                       seed=seed))
+    return build_scene(world, env, basis.times)
+
+
+def scene_arrays(scene):
+    sp = scene.spec
+    d = dict(
+        ox=sp.obstacles_x, oy=sp.obstacles_y, b0=scene.initial_state, lane_centers=scene.lane_centers,
+        limits=np.array([sp.ellipse_a, sp.ellipse_b, sp.v_min, sp.v_max, sp.a_max, sp.kappa_max, sp.c_max,
+                         sp.y_lb, sp.y_ub]),
+    )
+    if sp.road_curvature is not None:
+        d["curv_x"] = np.asarray(sp.road_curvature[0], float)
+        d["curv_k"] = np.asarray(sp.road_curvature[1], float)
+    return d
+
+
+def sample_params(env, scene, B, seed):
+    cfg_mean = np.concatenate([np.full(env.m_seg, scene.initial_state[1]),
+                               np.full(env.m_seg, np.hypot(scene.initial_state[2], scene.initial_state[3]))])
+    cfg_cov = np.diag(np.concatenate([np.full(env.m_seg, env.sigma_offset ** 2),
+                                      np.full(env.m_seg, env.sigma_speed ** 2)]))
+    return SamplingDistribution(cfg_mean, cfg_cov).sample(B, np.random.default_rng(seed))
+
+
+def run_lower(name, scene, params, *, n_obs, m=100, T=5.0, iters=100, tol=1e-3, rho=1.0, with_goal=False,
+              weights=None):
+    basis = build_basis(10, m, T, "bernstein")
+    layout = ParamLayout(4, with_goal=with_goal)
+    weights = weights or TrackingWeights()
+    solver = LowerLevelSolver(basis, weights, layout, ProjectionConfig(rho, iters, tol), n_obs)
+    t0 = time.time()
+    sol, proj = solver.solve(params, scene)
+    dt = time.time() - t0
+    xd, yd = solver.velocities(proj.xi)
+    costs = upper_cost_batch(xd, yd, scene.spec.v_max)
+    out = dict(
+        params=params, xi_bar=sol.xi, mu=sol.mu, xi=proj.xi, residuals=proj.residuals,
+        history=proj.residual_history, iterations_used=proj.iterations_used, clip_conflicts=proj.clip_conflicts,
+        costs=costs, rho=rho, max_iters=iters, tol=tol, m=m, T=T, with_goal=with_goal,
+        weights=np.array([weights.k_p, weights.k_v, weights.w_smooth, weights.w_offset, weights.w_speed]),
+        ref_seconds=dt, **scene_arrays(scene),
+    )
+    np.savez_compressed(os.path.join(OUT, f"lower_{name}.npz"), **out)
+    print(f"lower_{name}: B={params.shape[0]} obs={n_obs} iters_used={proj.iterations_used} "
+          f"conf={proj.clip_conflicts} rmax={proj.residuals.max():.3g} rmin={proj.residuals.min():.3g} {dt:.1f}s")
+
+
+def gen_basis():
+    d = {}
+    for tag, (order, m, T, fam) in {"b100": (10, 100, 5.0, "bernstein"), "b50": (10, 50, 10.0, "bernstein"),
+                                    "mono": (10, 100, 5.0, "monomial")}.items():
+        bs = build_basis(order, m, T, fam)
+        d[f"{tag}_W"], d[f"{tag}_Wd"], d[f"{tag}_Wdd"], d[f"{tag}_t"] = bs.W, bs.Wdot, bs.Wddot, bs.times
+    bs = build_basis(10, 100, 5.0, "bernstein")
+    for goal in (False, True):
+        qp = batch_qp.build_qp_structure(bs, TrackingWeights(), ParamLayout(4, with_goal=goal))
+        g = "goal_" if goal else ""
+        d[g + "Q"], d[g + "A_eq"], d[g + "kkt"] = qp.Q, qp.A_eq, qp.kkt
+        d[g + "qmx"], d[g + "qmy"] = qp.q_map_x, qp.q_map_y
+    from bilevel_drive.projection import ProjectionOperator
+    qp = batch_qp.build_qp_structure(bs, TrackingWeights(), ParamLayout(4))
+    for n_obs in (0, 10, 50):
+        op = ProjectionOperator(bs, qp, n_obs, ProjectionConfig())
+        d[f"aug{n_obs}_kkt"] = op.aug.kkt
+    np.savez_compressed(os.path.join(OUT, "basis.npz"), **d)
+    print("basis written")
+
+
+def gen_lower():
+    env = env_for()
+    basis = build_basis(10, 100, 5.0, "bernstein")
+    sc = highway_scene(env, basis, 4, 2.0, 24, 0)
+    run_lower("c1_s0", sc, sample_params(env, sc, 100, 0), n_obs=10)
+    sc = highway_scene(env, basis, 2, 1.0, 12, 1)
+    run_lower("c1_s1", sc, sample_params(env, sc, 100, 1), n_obs=10)
+    # canonical: 3 parked vehicles + 7 sentinels at 1e4 m (pkg/bench.py:208-242)
+    sc = canonical_scene(env)
+    run_lower("canon", sc, sample_params(env, sc, 100, 2), n_obs=10)
+    # dense 50-obstacle scene (config 4 scene recipe, smaller batch)
+    env50 = env_for(n_obs=50, obstacle_range=250.0)
+    sc = highway_scene(env50, basis, 4, 3.0, 80, 0)
+    run_lower("dense50", sc, sample_params(env50, sc, 48, 3), n_obs=50)
+    # B = 1
+    sc = highway_scene(env, basis, 4, 2.0, 24, 5)
+    run_lower("b1", sc, sample_params(env, sc, 1, 5), n_obs=10, iters=30)
+    # early exit: sentinel-only scene, feasible set-points
+    sc0 = highway_scene(env, basis, 2, 0.5, 2, 7)
+    spec = sc0.spec
+    far = ConstraintSpec(obstacles_x=spec.obstacles_x * 0 + 1e4 + 100.0 * np.arange(10)[:, None],
+                         obstacles_y=np.zeros_like(spec.obstacles_y), ellipse_a=spec.ellipse_a,
+                         ellipse_b=spec.ellipse_b, v_max=spec.v_max, a_max=spec.a_max, kappa_max=spec.kappa_max,
+                         c_max=spec.c_max, y_lb=spec.y_lb, y_ub=spec.y_ub, v_min=spec.v_min)
+    sc = PlanningScene(initial_state=sc0.initial_state, spec=far, lane_centers=sc0.lane_centers)
+    for tag, scale in (("early4", 0.5), ("early39", 1.0)):
+        rng = np.random.default_rng(11)
+        p = np.concatenate([scale * 0.3 * rng.standard_normal((16, 4)), 10.0 + scale * rng.standard_normal((16, 4))],
+                           axis=1)
+        run_lower(tag, sc, p, n_obs=10, iters=80)
+    # curved road (tabulated kappa, np.interp semantics incl. both clamps)
+    curved = ConstraintSpec(obstacles_x=spec.obstacles_x, obstacles_y=spec.obstacles_y, ellipse_a=spec.ellipse_a,
+                            ellipse_b=spec.ellipse_b, v_max=spec.v_max, a_max=spec.a_max,
+                            kappa_max=spec.kappa_max, c_max=spec.c_max, y_lb=spec.y_lb, y_ub=spec.y_ub,
+                            v_min=3.0,
+                            road_curvature=(np.array([5.0, 20.0, 40.0, 60.0]), np.array([0.01, -0.3, 0.05, 0.15])))
+    sc = PlanningScene(initial_state=sc0.initial_state, spec=curved, lane_centers=sc0.lane_centers)
+    run_lower("curve", sc, sample_params(env, sc, 32, 8), n_obs=10, iters=40)
+    # zero obstacles
+    none = ConstraintSpec(obstacles_x=np.zeros((0, 100)), obstacles_y=np.zeros((0, 100)), ellipse_a=spec.ellipse_a,
+                          ellipse_b=spec.ellipse_b, v_max=spec.v_max, a_max=spec.a_max, kappa_max=spec.kappa_max,
+                          c_max=spec.c_max, y_lb=spec.y_lb, y_ub=spec.y_ub, v_min=spec.v_min)
+    sc = PlanningScene(initial_state=np.array([0.0, 4.0, 15.0, 0.5, 1.0, -0.2]), spec=none,
+                       lane_centers=sc0.lane_centers)
+    run_lower("nobs0", sc, sample_params(env, sc, 24, 9), n_obs=0, iters=25)
+    # goal layout: neq = 9, per-sample b, w_offset = w_speed = 0 (pkg/planners.py:387-412)
+    sc = highway_scene(env, basis, 4, 1.0, 16, 4)
+    x0, v0 = sc.initial_state[0], float(np.hypot(sc.initial_state[2], sc.initial_state[3]))
+    reach = max(v0, 0.3 * env.v_max) * env.horizon
+    pts = np.array([np.concatenate([np.zeros(4), np.zeros(4), [x0 + f * reach, y]])
+                    for f in (0.5, 0.7, 0.85, 1.0) for y in sc.lane_centers])
+    w = TrackingWeights(w_offset=0.0, w_speed=0.0)
+    run_lower("goal", sc, pts, n_obs=10, iters=50, with_goal=True, weights=w)
+
+
+def gen_cem_c2():
+    env = env_for()
+    basis = build_basis(10, 100, 5.0, "bernstein")
+    sc = highway_scene(env, basis, 4, 2.0, 24, 0)
+    solver = LowerLevelSolver(basis, TrackingWeights(), ParamLayout(4), ProjectionConfig(1.0, 100, 1e-3), 10)
+    env2 = PlannerEnvConfig(horizon=5.0, num_samples=100, max_obstacles=10, proj_iters=100, batch_size=1000,
+                            constraint_elites=150, elites=100, iterations=4)
+    cfg = bilevel_config_for(env2, sc, batch_size=1000, iterations=4)
+    rec = {k: [] for k in ("params", "xi", "residuals", "costs", "elite_idx", "cons_idx", "elite_aug", "mean", "cov",
+                           "iters_used", "conflicts", "history_max")}
+    dist = [SamplingDistribution(cfg.init_mean, cfg.init_cov)]
+
+    def hook(it, params, proj, costs, elite_idx):
+        cons, el, ea = rank_samples(proj.residuals, costs, cfg.constraint_elites, cfg.elites, cfg.residual_weight)
+        assert np.array_equal(el, elite_idx)
+        nd = update_distribution(dist[-1], params[el], ea, cfg.eta, cfg.gamma)
+        dist.append(nd)
+        rec["params"].append(params)
+        rec["xi"].append(proj.xi)
+        rec["residuals"].append(proj.residuals)
+        rec["costs"].append(costs)
+        rec["elite_idx"].append(el)
+        rec["cons_idx"].append(cons)
+        rec["elite_aug"].append(ea)
+        rec["mean"].append(nd.mean)
+        rec["cov"].append(nd.cov)
+        rec["iters_used"].append(proj.iterations_used)
+        rec["conflicts"].append(proj.clip_conflicts)
+        rec["history_max"].append(proj.residual_history.max(axis=1))
+        print(f"  cem it {it}: iters={proj.iterations_used} r0={np.sum(proj.residuals == 0)}", flush=True)
+
+    t0 = time.time()
+    res = solve_bilevel(sc, solver, cfg, np.random.default_rng(0), trace_hook=hook)
+    dt = time.time() - t0
+    stats = np.array([[s.iteration, s.elite_mean_upper_cost, s.best_augmented_cost, s.cov_trace, s.residual_min,
+                       s.residual_median, s.residual_max] for s in res.diagnostics])
+    out = {k: np.array(v) for k, v in rec.items()}
+    out.update(scene_arrays(sc))
+    out.update(init_mean=cfg.init_mean, init_cov=cfg.init_cov, stats=stats, best_index=res.best.index,
+               best_xi=np.concatenate([res.best.coeffs.cx, res.best.coeffs.cy]), best_cost=res.best.upper_cost,
+               best_residual=res.best.residual, best_aug=res.best.augmented_cost,
+               final_mean=res.distribution.mean, final_cov=res.distribution.cov,
+               cfg=np.array([cfg.batch_size, cfg.constraint_elites, cfg.elites, cfg.iterations, cfg.eta, cfg.gamma,
+                             cfg.residual_weight]), ref_seconds=dt)
+    np.savez_compressed(os.path.join(OUT, "cem_c2.npz"), **out)
+    print(f"cem_c2 written ({dt:.1f}s)")
+
+
+def gen_cem_small():
+    env = env_for(iters=40)
+    basis = build_basis(10, 100, 5.0, "bernstein")
+    sc = highway_scene(env, basis, 2, 1.5, 14, 3)
+    solver = LowerLevelSolver(basis, TrackingWeights(), ParamLayout(4), ProjectionConfig(1.0, 40, 1e-3), 10)
+    cfg = BiLevelConfig(batch_size=200, constraint_elites=60, elites=20, iterations=3, eta=0.7, gamma=0.9,
+                        residual_weight=1.0,
+                        init_mean=np.concatenate([np.full(4, sc.initial_state[1]), np.full(4, 10.0)]),
+                        init_cov=np.diag(np.concatenate([np.full(4, 1.5 ** 2), np.full(4, 3.0 ** 2)])))
+    t0 = time.time()
+    res = solve_bilevel(sc, solver, cfg, np.random.default_rng(3))
+    dt = time.time() - t0
+    stats = np.array([[s.iteration, s.elite_mean_upper_cost, s.best_augmented_cost, s.cov_trace, s.residual_min,
+                       s.residual_median, s.residual_max] for s in res.diagnostics])
+    out = scene_arrays(sc)
+    out.update(init_mean=cfg.init_mean, init_cov=cfg.init_cov, stats=stats, best_index=res.best.index,
+               best_params=res.best.params.to_vector(),
+               best_xi=np.concatenate([res.best.coeffs.cx, res.best.coeffs.cy]), best_cost=res.best.upper_cost,
+               best_residual=res.best.residual, best_aug=res.best.augmented_cost,
+               final_mean=res.distribution.mean, final_cov=res.distribution.cov, seed=3, am_iters=40,
+               cfg=np.array([cfg.batch_size, cfg.constraint_elites, cfg.elites, cfg.iterations, cfg.eta, cfg.gamma,
+                             cfg.residual_weight]), ref_seconds=dt)
+    np.savez_compressed(os.path.join(OUT, "cem_small.npz"), **out)
+    print(f"cem_small written ({dt:.1f}s), best idx {res.best.index}")
+
+
+def gen_scenes():
+    """Scenes only (for the product's synthetic scene generator parity)."""
+    out = {}
+    for seed in range(6):
+        for lanes, dens, veh, nobs, rng_ in ((4, 2.0, 24, 10, 120.0), (4, 3.0, 80, 50, 250.0), (2, 1.0, 12, 10, 120.0)):
+            env = env_for(n_obs=nobs, obstacle_range=rng_)
+            basis = build_basis(10, 100, 5.0, "bernstein")
+            sc = highway_scene(env, basis, lanes, dens, veh, seed)
+            tag = f"s{seed}_l{lanes}_d{dens}_v{veh}_o{nobs}"
+            out[tag + "_ox"], out[tag + "_oy"] = sc.spec.obstacles_x, sc.spec.obstacles_y
+            out[tag + "_b0"] = sc.initial_state
+            out[tag + "_lim"] = scene_arrays(sc)["limits"]
+    np.savez_compressed(os.path.join(OUT, "scenes.npz"), **out)
+    print("scenes written")
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", nargs="*", default=None)
+    a = ap.parse_args()
+    os.makedirs(OUT, exist_ok=True)
+    jobs = {"basis": gen_basis, "lower": gen_lower, "scenes": gen_scenes, "cem_small": gen_cem_small,
+            "cem_c2": gen_cem_c2}
+    for name, fn in jobs.items():
+        if a.only is None or name in a.only:
+            fn()
