@@ -1,0 +1,180 @@
+/*
+ * bilevel_b200.h — C ABI of the B200-native bi-level planner hot path.
+ *
+ * This is the drop-in boundary for the data-parallel path of the reference
+ * package `bilevel-drive` (arXiv 2212.02224): the batch Frenet trajectory
+ * optimizer (stage-1 QP + alternating-minimisation projection) and the CEM
+ * upper level.  The reference is pure Python with no FFI; each entry point
+ * below names the reference interface whose work it replaces
+ * (`pkg/` = pkg/src/bilevel_drive/).  INTEGRATION.md shows the ctypes binding.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  Every array argument may be a HOST
+ *     pointer (pageable or pinned; the library copies it over) or a DEVICE
+ *     pointer on the context's device (used in place, no copy).  Calls whose
+ *     outputs include a host pointer synchronise before returning; calls on
+ *     device pointers only are asynchronous on the context stream.
+ *   - Layouts are row-major and SAMPLE-MAJOR: a batch of B coefficient vectors
+ *     is B x 2n (the reference stores 2n x B column-per-sample; the Python shim
+ *     transposes).  Several independent scenes ("fleet") are stacked scene-major:
+ *     sample s of scene j lives at row j*B + s.
+ *   - Return 0 on success or a negative BD_ERR_* code; bd_last_error() gives text.
+ *   - One context per device; a context is not thread-safe.
+ */
+#ifndef BILEVEL_B200_H
+#define BILEVEL_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BD_ABI_VERSION 1
+
+#define BD_OK 0
+#define BD_ERR_VALUE (-1)      /* ValueError        pkg/batch_qp.py:99-106,223-227,265-269; pkg/projection.py:225-233 */
+#define BD_ERR_STRUCTURE (-2)  /* StructureError    pkg/batch_qp.py:39-40,127-140 */
+#define BD_ERR_NUMERICAL (-3)  /* NumericalFailure  pkg/batch_qp.py:43-44,272-279; pkg/projection.py:290-291 */
+#define BD_ERR_CUDA (-4)       /* CUDA runtime error (RuntimeError) */
+#define BD_ERR_STATE (-5)      /* constants not uploaded / call order */
+
+typedef struct bd_ctx bd_ctx;
+
+/* Scalars of ConstraintSpec (pkg/constraints.py:31-42). */
+typedef struct bd_limits {
+    double ellipse_a, ellipse_b, v_min, v_max, a_max, kappa_max, c_max, y_lb, y_ub;
+} bd_limits;
+
+/* BiLevelConfig (pkg/bilevel.py:72-97) plus the projection budget (pkg/projection.py:38-46). */
+typedef struct bd_cem_config {
+    int batch;          /* n-bar: samples per scene and CEM iteration          */
+    int n_cons;         /* constraint_elites n                                 */
+    int n_elite;        /* elites q                                            */
+    int iterations;     /* CEM iterations N                                    */
+    int am_iters;       /* ProjectionConfig.max_iters                          */
+    double eta, gamma, residual_weight, tol;
+    uint64_t seed;      /* Philox key when z == NULL (device RNG mode)         */
+} bd_cem_config;
+
+/* ------------------------------------------------------------------ lifecycle */
+int bd_abi_version(void);
+int bd_create(int device, bd_ctx** out);
+void bd_destroy(bd_ctx* ctx);
+const char* bd_last_error(const bd_ctx* ctx);
+/* Use an external cudaStream_t (e.g. torch's current stream); NULL restores the library stream. */
+int bd_set_stream(bd_ctx* ctx, void* cuda_stream);
+int bd_synchronize(bd_ctx* ctx);
+/* Tuning knobs: "lanes_per_sample" (0=auto, 4/8/16/32), "samples_per_cta" (0=auto). */
+int bd_set_option(bd_ctx* ctx, const char* key, int value);
+/* Kernel launches issued by this context since creation (instrumentation). */
+int64_t bd_launch_count(const bd_ctx* ctx);
+/* Synchronise and return (in *bits) the OR of the device error words of the last
+ * asynchronous call: 1 = non-finite iterate, 2 = stage-1 KKT residual above 1e-8. */
+int bd_error_bits(bd_ctx* ctx, int* bits);
+
+/* ------------------------------------------------------------------ constants
+ * Uploaded once per LowerLevelSolver (pkg/bilevel.py:204-215); the host keeps
+ * the LU factorizations (FACTORIZATION_COUNT, pkg/batch_qp.py:31-36).          */
+
+/* Sampled basis W, Wdot, Wddot, m x n row-major fp64 (build_basis, pkg/basis.py:156-179). */
+int bd_set_basis(bd_ctx* ctx, int m, int n, const double* W, const double* Wd, const double* Wdd);
+
+/* Stage-1 tracking QP (build_qp_structure / build_rhs_batch / solve_batch,
+ * pkg/batch_qp.py:152-280): set-point -> linear-cost maps q_map_x/q_map_y
+ * (n x m_seg), the bordered KKT and its inverse ((2n+neq)^2, fp64).           */
+int bd_set_stage1(bd_ctx* ctx, int m_seg, int with_goal, int neq, const double* q_map_x,
+                  const double* q_map_y, const double* kkt, const double* kkt_inv);
+
+/* Projection operator (ProjectionOperator.__init__, pkg/projection.py:189-214):
+ * inverse of the penalty-augmented KKT ((2n+neq)^2) and A_eq (neq x 2n).
+ * The x/y blocks must decouple (they do for every reference layout).         */
+int bd_set_projection(bd_ctx* ctx, int n_obs, double rho, int neq, const double* kkt_inv_aug,
+                      const double* a_eq);
+
+/* Scenes (PlanningScene / ConstraintSpec, pkg/constraints.py:19-92):
+ * obstacles S x n_obs x m, limits S, initial states S x 6, optional tabulated
+ * road curvature S x n_curv (np.interp semantics; n_curv = 0 for straight roads). */
+int bd_set_scenes(bd_ctx* ctx, int n_scenes, int n_obs, int m, const double* ox, const double* oy,
+                  const bd_limits* limits, const double* b0, int n_curv, const double* curv_x,
+                  const double* curv_k);
+
+/* ------------------------------------------------------------------ lower level */
+
+/* Stage-1 batch solve: solve_batch(build_rhs_batch(params)) (pkg/batch_qp.py:209-280),
+ * including the 1e-8*(1+|rhs|) KKT residual check -> BD_ERR_NUMERICAL.
+ * params (S*B) x dim; outputs xi_bar (S*B) x 2n, mu (S*B) x neq, b (S*B) x neq (each may be NULL). */
+int bd_stage1(bd_ctx* ctx, int n_scenes, int batch, const double* params, double* xi_bar, double* mu,
+              double* b_out);
+
+/* AM projection: ProjectionOperator.project (pkg/projection.py:216-339), incl. the
+ * residual evaluator (pkg/constraints.py:142-153) and the batch-global early exit
+ * (pkg/projection.py:329), per scene.  b may be NULL (scene b0, zero goal rows).
+ * Outputs: xi (S*B) x 2n, residuals S*B, optional upper cost S*B (pkg/bilevel.py:125-126),
+ * optional history S x max_iters x B (fp32; rows >= iterations_used are undefined),
+ * iterations_used S, clip_conflicts S.                                          */
+int bd_project(bd_ctx* ctx, int n_scenes, int batch, const double* xi_bar, const double* b, int max_iters,
+               double tol, double* xi, double* residuals, double* cost, float* history, int* iters_used,
+               int64_t* conflicts);
+
+/* LowerLevelSolver.solve + upper_cost_batch fused (pkg/bilevel.py:217-225,125-126). */
+int bd_solve_lower(bd_ctx* ctx, int n_scenes, int batch, const double* params, int max_iters, double tol,
+                   double* xi_bar, double* mu, double* xi, double* residuals, double* cost, float* history,
+                   int* iters_used, int64_t* conflicts);
+
+/* Trajectory evaluation on the basis grid: eval_trajectory / LowerLevelSolver.velocities
+ * (pkg/basis.py:182-195, pkg/bilevel.py:223-225).  xi N x 2n -> each output N x m (may be NULL). */
+int bd_eval(bd_ctx* ctx, int count, const double* xi, double* x, double* y, double* xd, double* yd,
+            double* xdd, double* ydd);
+
+/* Direct residual evaluator batch_residuals (pkg/constraints.py:142-153) on given coefficients,
+ * scene-major (S*B) x 2n -> S*B. */
+int bd_residuals(bd_ctx* ctx, int n_scenes, int batch, const double* xi, double* residuals);
+
+/* Generic batched KKT solve: solve_batch(structure, rhs) (pkg/batch_qp.py:258-280) for any
+ * bordered system with nvar + neq <= 32: sol = kkt_inv rhs per column, with the reference's
+ * residual check.  rhs and sol are count x (nvar+neq) (one row per sample). */
+int bd_kkt_solve(bd_ctx* ctx, int nvar, int neq, const double* kkt, const double* kkt_inv, int count,
+                 const double* rhs, double* sol);
+
+/* ------------------------------------------------------------------ upper level */
+
+/* SamplingDistribution.sample (pkg/bilevel.py:51-57): p = mean + z chol(cov)^T, with the
+ * reference's 1e-5 I fallback; z count x dim (e.g. from the caller's numpy Generator). */
+int bd_sample(bd_ctx* ctx, int dim, int count, const double* mean, const double* cov, const double* z,
+              double* params);
+
+/* rank_samples + update_distribution (pkg/bilevel.py:129-137,163-194) per scene.
+ * mean (S x dim) and cov (S x dim x dim) are updated in place.  Outputs (may be NULL):
+ * cons_idx S x n_cons, elite_idx S x n_elite, elite_aug S x n_elite,
+ * stats S x 6 = IterationStats fields (pkg/bilevel.py:100-108) after the update. */
+int bd_rank_refit(bd_ctx* ctx, int n_scenes, int batch, int dim, const double* residuals, const double* cost,
+                  const double* params, int n_cons, int n_elite, double residual_weight, double eta,
+                  double gamma, double* mean, double* cov, int64_t* cons_idx, int64_t* elite_idx,
+                  double* elite_aug, double* stats);
+
+/* One full CEM planning cycle per scene: solve_bilevel (pkg/bilevel.py:228-295).
+ * Samples p = mean + z L^T (pkg/bilevel.py:51-57) with z supplied (iterations x S x B x dim,
+ * e.g. from the caller's numpy Generator) or drawn on device with Philox (z == NULL).
+ * warm (S x B x dim or NULL) replaces the first iteration's draw (pkg/bilevel.py:250-251).
+ * Per-scene outputs (each may be NULL): best_index, best_params (dim), best_xi (2n),
+ * best_cost, best_residual, best_aug, stats (iterations x 6), final mean/cov,
+ * iterations_done (completed CEM iterations; < iterations means degraded, pkg/bilevel.py:254-261). */
+int bd_cem_cycle(bd_ctx* ctx, int n_scenes, const bd_cem_config* cfg, const double* init_mean,
+                 const double* init_cov, const double* z, const double* warm, int64_t* best_index,
+                 double* best_params, double* best_xi, double* best_cost, double* best_residual,
+                 double* best_aug, double* stats, double* final_mean, double* final_cov, int* iterations_done);
+
+/* ------------------------------------------------------------------ CVAE warm start
+ * Decoder MLP of the paper (not in the reference package):
+ * (obs 55 + z 2) -> 1024 -> 1024 -> 1024 -> 1024 -> 256 -> dim, BatchNorm folded
+ * into the Linear layers, ReLU between.  Weights fp32 row-major [out x in] + bias. */
+int bd_cvae_set_weights(bd_ctx* ctx, int n_layers, const int* dims, const float* const* weights,
+                        const float* const* biases);
+int bd_cvae_decode(bd_ctx* ctx, int count, const float* obs /* 55 */, const float* z /* count x 2 */,
+                   double* params /* count x dim */);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BILEVEL_B200_H */

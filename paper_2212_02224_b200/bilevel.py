@@ -1,0 +1,345 @@
+"""CEM upper level over the device lower level — drop-in for pkg/bilevel.py.
+
+``LowerLevelSolver.solve`` runs stage-1 + AM projection + upper cost as one device
+sequence (``bd_solve_lower``).  ``solve_bilevel`` runs the whole CEM cycle on the
+device (``bd_cem_cycle``: sample -> stage-1 -> AM -> exit scan / replay ->
+rank + refit per iteration, no host round trip); the Gaussian draws come from the
+caller's numpy Generator exactly as in the reference, so a seeded call reproduces
+the reference's samples.  With a ``trace_hook`` the loop is stepped from the host
+(still all compute on the device) so the hook sees every iteration.
+
+The array-level helpers (``upper_cost_batch``, ``rank_samples``, ``select_elites``,
+``update_distribution``) keep the reference signatures for callers holding host
+arrays; on the path their work is done by K3 (csrc/cem_kernels.cuh).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import logging
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._native import CemConfig, f64, ptr, upload_scenes
+from .basis import PolynomialBasis, TrajectoryCoeffs, eval_trajectory
+from .batch_qp import NumericalFailure, QPSolutionBatch, TrackingWeights, build_qp_structure
+from .behavior import BehaviorParams, ParamLayout, WarmStartSource
+from .constraints import PlanningScene
+from .projection import ProjectionBatchResult, ProjectionConfig, ProjectionOperator
+
+__all__ = [
+    "SamplingDistribution", "EliteRecord", "BiLevelConfig", "IterationStats", "BiLevelResult", "upper_cost",
+    "upper_cost_batch", "rank_samples", "select_elites", "DegenerateWeights", "update_distribution",
+    "LowerLevelSolver", "solve_bilevel",
+]
+
+log = logging.getLogger(__name__)
+
+_COV_REG = 1e-6
+
+
+@dataclass(frozen=True)
+class SamplingDistribution:
+    """Gaussian over behaviour vectors (pkg/bilevel.py:34-57)."""
+
+    mean: np.ndarray
+    cov: np.ndarray
+
+    def __post_init__(self) -> None:
+        mean = np.asarray(self.mean, dtype=float)
+        cov = np.asarray(self.cov, dtype=float)
+        if cov.shape != (mean.shape[0], mean.shape[0]):
+            raise ValueError(f"cov shape {cov.shape} does not match mean dim {mean.shape[0]}")
+        if not np.allclose(cov, cov.T):
+            raise ValueError("covariance must be symmetric")
+        object.__setattr__(self, "mean", mean)
+        object.__setattr__(self, "cov", cov)
+
+    def sample(self, n: int, rng: np.random.Generator) -> np.ndarray:
+        try:
+            L = np.linalg.cholesky(self.cov)
+        except np.linalg.LinAlgError:
+            L = np.linalg.cholesky(self.cov + 10 * _COV_REG * np.eye(self.cov.shape[0]))
+        return self.mean[None, :] + rng.standard_normal((n, self.mean.shape[0])) @ L.T
+
+
+@dataclass(frozen=True)
+class EliteRecord:
+    index: int
+    params: BehaviorParams
+    coeffs: TrajectoryCoeffs
+    upper_cost: float
+    residual: float
+    augmented_cost: float
+
+
+@dataclass(frozen=True)
+class BiLevelConfig:
+    """Alg. 1 knobs (pkg/bilevel.py:72-97)."""
+
+    batch_size: int = 1000
+    constraint_elites: int = 150
+    elites: int = 50
+    iterations: int = 5
+    eta: float = 0.7
+    gamma: float = 0.9
+    residual_weight: float = 1.0
+    init_mean: np.ndarray = field(default_factory=lambda: np.zeros(8))
+    init_cov: np.ndarray = field(default_factory=lambda: np.eye(8))
+
+    def __post_init__(self) -> None:
+        if not (self.elites <= self.constraint_elites <= self.batch_size):
+            raise ValueError(f"need elites <= constraint_elites <= batch_size, got "
+                             f"{self.elites} / {self.constraint_elites} / {self.batch_size}")
+        if not (0.0 < self.eta <= 1.0):
+            raise ValueError(f"eta must lie in (0, 1], got {self.eta}")
+        if self.gamma <= 0:
+            raise ValueError(f"gamma must be positive, got {self.gamma}")
+        if self.iterations < 1:
+            raise ValueError("need at least one iteration")
+        object.__setattr__(self, "init_mean", np.asarray(self.init_mean, dtype=float))
+        object.__setattr__(self, "init_cov", np.asarray(self.init_cov, dtype=float))
+
+
+@dataclass(frozen=True)
+class IterationStats:
+    iteration: int
+    elite_mean_upper_cost: float
+    best_augmented_cost: float
+    cov_trace: float
+    residual_min: float
+    residual_median: float
+    residual_max: float
+
+
+@dataclass(frozen=True)
+class BiLevelResult:
+    best: EliteRecord
+    diagnostics: list[IterationStats]
+    distribution: SamplingDistribution
+    degraded: bool = False
+
+
+# ----------------------------------------------------------------------------- array helpers
+def upper_cost(coeffs: TrajectoryCoeffs, basis: PolynomialBasis, v_max: float) -> float:
+    """sum_t (|v| - v_max)^2 of one trajectory (pkg/bilevel.py:119-122)."""
+    return float(((eval_trajectory(basis, coeffs).speed() - v_max) ** 2).sum())
+
+
+def upper_cost_batch(xdot: np.ndarray, ydot: np.ndarray, v_max: float) -> np.ndarray:
+    """(pkg/bilevel.py:125-126); on the path the cost is fused into K2's last sweep."""
+    return ((np.hypot(xdot, ydot) - v_max) ** 2).sum(axis=-1)
+
+
+def rank_samples(residuals: np.ndarray, costs: np.ndarray, n: int, q: int, residual_weight: float):
+    """Constraint-elite then elite sets, ties by index (pkg/bilevel.py:129-137)."""
+    cons_idx = np.argsort(residuals, kind="stable")[:n]
+    aug = costs[cons_idx] + residual_weight * residuals[cons_idx]
+    sub = np.lexsort((cons_idx, aug))[:q]
+    return cons_idx, cons_idx[sub], aug[sub]
+
+
+def select_elites(records: list[EliteRecord], n: int, q: int):
+    """Record-level variant (pkg/bilevel.py:140-156)."""
+    if n > len(records) or q > n:
+        raise ValueError(f"need q <= n <= len(records), got {q} / {n} / {len(records)}")
+    res = np.array([r.residual for r in records])
+    aug = np.array([r.augmented_cost for r in records])
+    idx = np.array([r.index for r in records])
+    order = np.lexsort((idx, res))[:n]
+    cons = [records[i] for i in order]
+    sub = np.lexsort((idx[order], aug[order]))[:q]
+    return cons, [cons[i] for i in sub]
+
+
+class DegenerateWeights(RuntimeError):
+    """All elite weights underflowed (pkg/bilevel.py:159-160)."""
+
+
+def _elite_weights(aug_costs: np.ndarray, gamma: float) -> np.ndarray:
+    w = np.exp(-(aug_costs - aug_costs.min()) / gamma)
+    total = w.sum()
+    if not np.isfinite(total) or total <= 0.0:
+        log.warning("elite weights degenerated; falling back to uniform")
+        return np.full_like(aug_costs, 1.0 / aug_costs.shape[0])
+    return w / total
+
+
+def update_distribution(dist: SamplingDistribution, elite_params: np.ndarray, elite_aug_costs: np.ndarray,
+                        eta: float, gamma: float) -> SamplingDistribution:
+    """Exponentiated-cost refit (pkg/bilevel.py:175-194)."""
+    P = np.atleast_2d(np.asarray(elite_params, dtype=float))
+    w = _elite_weights(np.asarray(elite_aug_costs, dtype=float), gamma)
+    mean = (1.0 - eta) * dist.mean + eta * (w @ P)
+    D = P - mean[None, :]
+    cov = (1.0 - eta) * dist.cov + eta * (D.T @ (w[:, None] * D)) + _COV_REG * np.eye(dist.mean.shape[0])
+    return SamplingDistribution(mean=mean, cov=0.5 * (cov + cov.T))
+
+
+# ----------------------------------------------------------------------------- lower level
+class LowerLevelSolver:
+    """Factorized QP + projection operators bound to one device context (pkg/bilevel.py:197-225)."""
+
+    def __init__(self, basis: PolynomialBasis, weights: TrackingWeights, layout: ParamLayout,
+                 proj_config: ProjectionConfig, num_obstacles: int, device: int = 0):
+        self.basis = basis
+        self.layout = layout
+        self.qp = build_qp_structure(basis, weights, layout)
+        self.projector = ProjectionOperator(basis, self.qp, num_obstacles, proj_config, device=device)
+        self._ctx = self.projector._ctx
+        qp = self.qp
+        self._ctx.call("bd_set_stage1", layout.m_seg, int(layout.with_goal), qp.num_eq, ptr(f64(qp.q_map_x)),
+                       ptr(f64(qp.q_map_y)), ptr(f64(qp.kkt)), ptr(f64(qp.kkt_inv)))
+        self.last_costs: np.ndarray | None = None
+
+    @property
+    def context(self):
+        return self._ctx
+
+    def _params(self, param_batch) -> np.ndarray:
+        P = f64(np.atleast_2d(np.asarray(param_batch, dtype=float)))
+        if P.shape[1] != self.layout.dim:
+            raise ValueError(f"behavior vectors have dim {P.shape[1]}, layout wants {self.layout.dim}")
+        if not np.isfinite(P).all():
+            raise ValueError("right-hand sides must be finite")
+        return P
+
+    def solve(self, param_batch: np.ndarray, scene: PlanningScene) -> tuple[QPSolutionBatch, ProjectionBatchResult]:
+        """Stage-1 + projection (+ upper cost, kept in ``last_costs``) on the device."""
+        P = self._params(param_batch)
+        self.projector._check_spec(scene.spec)
+        self.projector._ensure_scene(scene)
+        B = P.shape[0]
+        cfg = self.projector.config
+        n2, neq = 2 * self.basis.num_coeffs, self.qp.num_eq
+        xb = np.empty((B, n2))
+        mu = np.empty((B, neq))
+        xi = np.empty((B, n2))
+        res = np.empty(B)
+        cost = np.empty(B)
+        hist = np.empty((cfg.max_iters, B), dtype=np.float32)
+        used = np.zeros(1, dtype=np.int32)
+        conf = np.zeros(1, dtype=np.int64)
+        self._ctx.call("bd_solve_lower", 1, B, ptr(P), cfg.max_iters, float(cfg.tol), ptr(xb), ptr(mu), ptr(xi),
+                       ptr(res), ptr(cost), ptr(hist), ptr(used), ptr(conf))
+        self.last_costs = cost
+        k = int(used[0])
+        sol = QPSolutionBatch(xi=np.ascontiguousarray(xb.T), mu=np.ascontiguousarray(mu.T))
+        proj = ProjectionBatchResult(xi=np.ascontiguousarray(xi.T), residuals=res,
+                                     residual_history=hist[:k].astype(np.float64), iterations_used=k,
+                                     clip_conflicts=int(conf[0]))
+        return sol, proj
+
+    def velocities(self, xi: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+        """(xdot, ydot), each (B, m), evaluated on the device (pkg/bilevel.py:223-225)."""
+        X = f64(np.atleast_2d(np.asarray(xi, dtype=float)).T)
+        B, m = X.shape[0], self.basis.num_samples
+        xd = np.empty((B, m))
+        yd = np.empty((B, m))
+        self._ctx.call("bd_eval", B, ptr(X), None, None, ptr(xd), ptr(yd), None, None)
+        return xd, yd
+
+
+# ----------------------------------------------------------------------------- upper level
+def _stats(it: int, row) -> IterationStats:
+    return IterationStats(iteration=it, elite_mean_upper_cost=float(row[0]), best_augmented_cost=float(row[1]),
+                          cov_trace=float(row[2]), residual_min=float(row[3]), residual_median=float(row[4]),
+                          residual_max=float(row[5]))
+
+
+def solve_bilevel(scene: PlanningScene, solver: LowerLevelSolver, config: BiLevelConfig, rng: np.random.Generator,
+                  warm_start: WarmStartSource | None = None, trace_hook=None) -> BiLevelResult:
+    """Alg. 1 (pkg/bilevel.py:228-295) on the device.
+
+    Returns the elite record with the lowest augmented cost at the last completed
+    iteration; a numerical failure after iteration 1 returns the best so far with
+    ``degraded=True``, a failure in iteration 1 raises NumericalFailure.
+    """
+    if trace_hook is not None:
+        return _solve_bilevel_stepped(scene, solver, config, rng, warm_start, trace_hook)
+    layout = solver.layout
+    dim, B, N = layout.dim, config.batch_size, config.iterations
+    solver.projector._check_spec(scene.spec)
+    solver.projector._ensure_scene(scene)
+    pcfg = solver.projector.config
+    state0 = rng.bit_generator.state
+    warm = f64(warm_start.draw(B)) if warm_start is not None else None
+    n_draw = N - (1 if warm is not None else 0)
+    z = np.zeros((N, B, dim))
+    if n_draw:
+        z[N - n_draw:] = rng.standard_normal((n_draw, B, dim))
+    cfg = CemConfig(B, config.constraint_elites, config.elites, N, pcfg.max_iters, config.eta, config.gamma,
+                    config.residual_weight, pcfg.tol, 0)
+    bi = np.zeros(1, dtype=np.int64)
+    bp = np.zeros(dim)
+    bx = np.zeros(2 * solver.basis.num_coeffs)
+    bc, br, ba = np.zeros(1), np.zeros(1), np.zeros(1)
+    st = np.zeros((N, 6))
+    fm = np.zeros(dim)
+    fc = np.zeros((dim, dim))
+    done = np.zeros(1, dtype=np.int32)
+    solver.context.call("bd_cem_cycle", 1, ctypes.byref(cfg), ptr(f64(config.init_mean)), ptr(f64(config.init_cov)),
+                        ptr(z), ptr(warm), ptr(bi), ptr(bp), ptr(bx), ptr(bc), ptr(br), ptr(ba), ptr(st), ptr(fm),
+                        ptr(fc), ptr(done))
+    k = int(done[0])
+    attempted = N if k >= N else (1 if k <= 0 else k + 1)
+    consumed = attempted - (1 if warm is not None else 0)
+    if consumed != n_draw:   # leave the caller's generator exactly where the reference would
+        rng.bit_generator.state = state0
+        if consumed > 0:
+            rng.standard_normal((consumed, B, dim))
+    if k <= 0:
+        raise NumericalFailure("bilevel iteration 1 failed: non-finite projection iterate or KKT residual")
+    if k < N:
+        log.warning("bilevel iteration %d failed; returning best-so-far", k + 1)
+    best = EliteRecord(index=int(bi[0]), params=BehaviorParams.from_vector(bp, layout),
+                       coeffs=TrajectoryCoeffs.from_stacked(bx), upper_cost=float(bc[0]), residual=float(br[0]),
+                       augmented_cost=float(ba[0]))
+    return BiLevelResult(best=best, diagnostics=[_stats(i + 1, st[i]) for i in range(k)],
+                         distribution=SamplingDistribution(fm, fc), degraded=k < N)
+
+
+def _solve_bilevel_stepped(scene, solver, config, rng, warm_start, trace_hook) -> BiLevelResult:
+    ctx = solver.context
+    layout = solver.layout
+    dim, B = layout.dim, config.batch_size
+    mean, cov = f64(config.init_mean), f64(config.init_cov)
+    SamplingDistribution(mean, cov)
+    best = None
+    diagnostics: list[IterationStats] = []
+    degraded = False
+    for it in range(1, config.iterations + 1):
+        if it == 1 and warm_start is not None:
+            params = f64(warm_start.draw(B))
+        else:
+            z = f64(rng.standard_normal((B, dim)))
+            params = np.empty((B, dim))
+            ctx.call("bd_sample", dim, B, ptr(mean), ptr(cov), ptr(z), ptr(params))
+        try:
+            _, proj = solver.solve(params, scene)
+        except NumericalFailure:
+            if best is None:
+                raise
+            log.warning("bilevel iteration %d failed; returning best-so-far", it)
+            degraded = True
+            break
+        costs = solver.last_costs
+        n, q = config.constraint_elites, config.elites
+        cons = np.empty(n, dtype=np.int64)
+        elite = np.empty(q, dtype=np.int64)
+        eaug = np.empty(q)
+        st = np.empty(6)
+        mean, cov = mean.copy(), cov.copy()
+        ctx.call("bd_rank_refit", 1, B, dim, ptr(f64(proj.residuals)), ptr(f64(costs)), ptr(params), n, q,
+                 float(config.residual_weight), float(config.eta), float(config.gamma), ptr(mean), ptr(cov),
+                 ptr(cons), ptr(elite), ptr(eaug), ptr(st))
+        trace_hook(it, params, proj, costs, elite)
+        j = int(elite[0])
+        best = EliteRecord(index=j, params=BehaviorParams.from_vector(params[j], layout),
+                           coeffs=TrajectoryCoeffs.from_stacked(proj.xi[:, j]), upper_cost=float(costs[j]),
+                           residual=float(proj.residuals[j]), augmented_cost=float(eaug[0]))
+        diagnostics.append(_stats(it, st))
+    assert best is not None
+    return BiLevelResult(best=best, diagnostics=diagnostics, distribution=SamplingDistribution(mean, cov),
+                         degraded=degraded)

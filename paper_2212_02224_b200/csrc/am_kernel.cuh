@@ -1,0 +1,417 @@
+// K2: persistent alternating-minimisation projection kernel (sm_100a).
+//
+// Replaces ProjectionOperator.project (pkg/projection.py:216-339) together with
+// polar_decompose (:100-135), _clip_magnitudes (:138-169), the per-iteration
+// augmented KKT solve (:286-292), the direct residual evaluator
+// (pkg/constraints.py:95-153) and the upper cost (pkg/bilevel.py:125-126).
+//
+// Mapping.  A sample is owned by a group of P lanes inside one warp; lane p of
+// the group handles timesteps t = p, p+P, p+2P, ...  The basis rows, the
+// scene's obstacle tile and the aug-KKT inverse blocks are staged once per CTA
+// in shared memory; everything per (sample, obstacle, timestep) lives in
+// registers and never returns to HBM between iterations.
+//
+// Algebra (verified against the reference in fp64):
+//   * polar step in trig-free residual form: with w = (X-x_o)/a, (Y-y_o)/b and
+//     q = |w|^2, the clipped back-projection residual is w (1 - q^-1/2) for
+//     0 < q < 1, (-1, 0) for q == 0 and 0 otherwise (scaled by a, b);
+//     velocity/acceleration residuals are v (|v| - clip|v|)/|v|.
+//   * the KKT identity K Q~ + K_b A = I turns the per-iteration solve into the
+//     increment  c <- c + K (l - c - rho g)  with l = xi_bar + lambda, where g is
+//     the back-projected residual F^T(F c - h) and K the per-axis 11x11 block of
+//     the aug-KKT inverse; lambda <- lambda - rho/2 g.  The first step adds
+//     K_b (b - A xi_bar) so a xi_bar that does not satisfy A xi = b is handled
+//     exactly as the reference's direct solve would.
+//   * precision recipe: per-(o,t) and per-t work plus the W mat-vecs in fp32;
+//     the per-sample state (c, lambda, the K apply) in fp64.
+#pragma once
+
+#include "bd_common.cuh"
+
+namespace bd {
+
+struct AmArgs {
+    int m, neq, n_obs, n_curv, B, s_cta, max_iters;
+    double rho;
+    const float* wrow;          // m x WROW        [W | Wd | Wdd] rows, fp32
+    const double* kblk;         // 2 x NC x KROW   per-axis aug-KKT inverse blocks
+    const double* kb;           // NX x neq        xi-b block of the aug-KKT inverse
+    const double* aeq;          // neq x NX
+    const float2* obs;          // S x n_obs x m   (x_o / a, y_o / b)
+    const SceneLim* lim;        // S
+    const double* bscene;       // S x neq         shared b per scene (b0, zero goal rows)
+    const float* curv;          // S x 2 x n_curv  (xs then ks)
+    const double* xi_bar;       // (S*B) x NX
+    const double* b;            // (S*B) x neq or nullptr (use bscene)
+    double* xi_out;             // (S*B) x NX
+    double* resid_out;          // S*B
+    double* cost_out;           // S*B or nullptr
+    float* hist_out;            // S x max_iters x B or nullptr
+    unsigned* itmax;            // S x max_iters x ITMAX_SLOTS (float bits, atomicMax)
+    unsigned long long* conflicts;  // S
+    int* err;
+    const int* replay;          // nullptr, or per-scene iteration count of a replay launch (0 = skip)
+};
+
+// Shared-memory carve-up, identical on host and device.
+struct AmSmem {
+    size_t w, obs, k, kb, a, curv, scr, dap, kap, total;
+    __host__ __device__ AmSmem(int m, int n_obs, int neq, int n_curv, int s_cta, int threads, int P, bool curv_on) {
+        const int J = (m + P - 1) / P;
+        size_t o = 0;
+        w = o;    o = align_up(o + (size_t)m * WROW * 4, 16);
+        obs = o;  o = align_up(o + (size_t)n_obs * m * 8, 16);
+        k = o;    o = align_up(o + (size_t)2 * NC * KROW * 8, 16);
+        kb = o;   o = align_up(o + (size_t)NX * neq * 8, 16);
+        a = o;    o = align_up(o + (size_t)neq * NX * 8, 16);
+        curv = o; o = align_up(o + (size_t)2 * n_curv * 4, 16);
+        scr = o;  o = align_up(o + (size_t)s_cta * SCR_BYTES, 16);
+        dap = o;  o = align_up(o + (size_t)J * threads * 4, 16);
+        kap = o;  o = align_up(o + (curv_on ? (size_t)J * threads * 4 : 0), 16);
+        total = o;
+    }
+    // per-sample scratch: u (24 doubles) | c32 (24 floats) | pad -> 76 words: conflict-free LDS.128 across samples
+    static constexpr int SCR_BYTES = 304;
+};
+
+__device__ __forceinline__ float interp_table(float x, const float* xs, const float* ks, int n) {
+    // np.interp semantics (pkg/constraints.py:67-72): clamp to the end values outside [xs0, xs_{n-1}].
+    if (x != x) return x;
+    if (x <= xs[0]) return ks[0];
+    if (x >= xs[n - 1]) return ks[n - 1];
+    int lo = 0, hi = n - 1;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (xs[mid] <= x) lo = mid; else hi = mid;
+    }
+    const float slope = (ks[lo + 1] - ks[lo]) / (xs[lo + 1] - xs[lo]);
+    return ks[lo] + slope * (x - xs[lo]);
+}
+
+// Recursive-halving reduce-scatter over the P lanes of a group: afterwards slot
+// P*j of lane p holds the group sum of value index p + P*j.
+template <int P, int NV>
+__device__ __forceinline__ void group_reduce_scatter(float (&v)[NV], int lane) {
+#pragma unroll
+    for (int o = P / 2; o >= 1; o >>= 1) {
+        const bool hi = (lane & o) != 0;
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            if ((k & (P - 1) & ~(o - 1)) != 0) continue;
+            const float keep = hi ? v[k | o] : v[k];
+            const float send = hi ? v[k] : v[k | o];
+            v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+    }
+}
+
+// One sweep over this lane's timesteps at the current coefficients cf:
+// forward evaluation, polar split + coupled clips, back-projection of the
+// residuals (v[0..21]), the direct residual (v[22]) and the upper cost (v[23]).
+template <int P, bool CURV, bool INIT, int NV>
+__device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float2* __restrict__ osm,
+                                      const float* __restrict__ csm, const float (&cf)[NX], float (&v)[NV],
+                                      float* dap, float* kap, int dstride, int p, int m, int n_obs, int n_curv,
+                                      const SceneLim& L, int& conf) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] = 0.f;
+    int j = 0;
+    for (int t = p; t < m; t += P, ++j) {
+        float w[WROW];
+        const float4* wr = reinterpret_cast<const float4*>(wsm + t * WROW);
+#pragma unroll
+        for (int q = 0; q < WROW / 4; ++q) {
+            const float4 f = wr[q];
+            w[4 * q] = f.x; w[4 * q + 1] = f.y; w[4 * q + 2] = f.z; w[4 * q + 3] = f.w;
+        }
+        // forward: X = W c_x, ... (pkg/projection.py:295)
+        float X = 0.f, Y = 0.f, XD = 0.f, YD = 0.f, XDD = 0.f, YDD = 0.f;
+#pragma unroll
+        for (int k = 0; k < NC; ++k) {
+            X = fmaf(w[k], cf[k], X);
+            Y = fmaf(w[k], cf[NC + k], Y);
+            XD = fmaf(w[NC + k], cf[k], XD);
+            YD = fmaf(w[NC + k], cf[NC + k], YD);
+            XDD = fmaf(w[2 * NC + k], cf[k], XDD);
+            YDD = fmaf(w[2 * NC + k], cf[NC + k], YDD);
+        }
+        // velocity / acceleration polar split (pkg/projection.py:119-122) in unit-vector form
+        const float dv2 = fmaf(XD, XD, YD * YD);
+        const float da2 = fmaf(XDD, XDD, YDD * YDD);
+        const float iv = dv2 > 0.f ? rsqrtf(dv2) : 0.f;
+        const float ia = da2 > 0.f ? rsqrtf(da2) : 0.f;
+        const float dv = dv2 * iv, da = da2 * ia;
+        const float cv = dv2 > 0.f ? XD * iv : 1.f, sv = YD * iv;     // atan2(0,0) = 0
+        const float ca = da2 > 0.f ? XDD * ia : 1.f, sa = YDD * ia;
+        const float gap = fabsf(sa * cv - ca * sv);                   // |sin(alpha_a - alpha_v)|
+        // coupled clip window (pkg/projection.py:138-169)
+        const int di = j * dstride;
+        const float da_prev = INIT ? fminf(fmaxf(da, 0.f), L.a_max) : dap[di];
+        float vhi = L.v_max;
+        float kcur = 0.f;
+        if (CURV) {
+            kcur = fabsf(interp_table(X, csm, csm + n_curv, n_curv));
+            const float kuse = INIT ? kcur : kap[di];
+            const float cent = kuse * cv * cv;
+            if (cent > 1e-12f) vhi = fminf(L.v_max, sqrtf(L.c_max / cent));
+            kap[di] = kcur;
+        }
+        const float vlo = fmaxf(L.v_min, sqrtf(da_prev * gap * L.inv_k_max));
+        conf += (vlo > vhi) ? 1 : 0;
+        const float dvc = fminf(fmaxf(dv, fminf(vlo, vhi)), vhi);
+        const float ahi = fminf(L.a_max, dvc * dvc * L.k_max / fmaxf(gap, 1e-8f));
+        const float dac = fminf(fmaxf(da, 0.f), ahi);
+        dap[di] = dac;
+        // residuals F c - h of the velocity / acceleration blocks (pkg/projection.py:312-315)
+        float rvx, rvy, rax, ray;
+        if (dv2 > 0.f) { const float f = (dv - dvc) * iv; rvx = XD * f; rvy = YD * f; }
+        else { rvx = -dvc; rvy = 0.f; }
+        if (da2 > 0.f) { const float f = (da - dac) * ia; rax = XDD * f; ray = YDD * f; }
+        else { rax = -dac; ray = 0.f; }
+        // obstacle block (pkg/projection.py:316-322) + clearance violation (pkg/constraints.py:116-120)
+        const float xs = X * L.inv_a, ys = Y * L.inv_b;
+        float rox = 0.f, roy = 0.f, coll = 0.f;
+        const float2* op = osm + t;
+        for (int o = 0; o < n_obs; ++o) {
+            const float2 ob = op[o * m];
+            const float wc = xs - ob.x, ws = ys - ob.y;
+            const float q = fmaf(wc, wc, ws * ws);
+            if (q < 1.f) {
+                coll += 1.f - q;
+                if (q > 0.f) {
+                    const float f = 1.f - rsqrtf(q);
+                    rox = fmaf(wc, f, rox);
+                    roy = fmaf(ws, f, roy);
+                } else {
+                    rox -= 1.f;
+                }
+            }
+        }
+        // lane slack residual (pkg/projection.py:308-310,323)
+        const float up = fmaxf(Y - L.y_ub, 0.f), lo = fmaxf(L.y_lb - Y, 0.f);
+        const float rl = up - lo;
+        // back-projection g += Wd^T r_v + Wdd^T r_a + W^T r_o (+ lane)
+        const float tox = L.a * rox, toy = fmaf(L.b, roy, rl);
+#pragma unroll
+        for (int k = 0; k < NC; ++k) {
+            v[k] = fmaf(w[k], tox, fmaf(w[2 * NC + k], rax, fmaf(w[NC + k], rvx, v[k])));
+            v[NC + k] = fmaf(w[k], toy, fmaf(w[2 * NC + k], ray, fmaf(w[NC + k], rvy, v[NC + k])));
+        }
+        if (!INIT) {
+            // direct violations (pkg/constraints.py:124-138) and speed cost (pkg/bilevel.py:125-126)
+            float r = coll + up + lo;
+            r += fmaxf(dv - L.v_max, 0.f) + fmaxf(L.v_min - dv, 0.f);
+            r += fmaxf(da - L.a_max, 0.f);
+            const float sp = fmaxf(dv, 1e-6f);
+            r += fmaxf(fabsf(YDD * XD - XDD * YD) / (sp * sp * sp) - L.k_max, 0.f);
+            if (CURV) r += fmaxf(XD * XD * kcur - L.c_max, 0.f);
+            v[NX] += r;
+            const float e = dv - L.v_max;
+            v[NX + 1] = fmaf(e, e, v[NX + 1]);
+        }
+    }
+}
+
+template <int P, bool CURV>
+__global__ void __launch_bounds__(256) am_kernel(const AmArgs a) {
+    constexpr int NV = ((NX + 2 + P - 1) / P) * P;   // 22 back-projections + residual + cost, padded
+    constexpr int ROWS = (NX + P - 1) / P;           // coefficient rows owned per lane
+    extern __shared__ __align__(16) unsigned char smem[];
+
+    const int scene = blockIdx.y;
+    int iters = a.max_iters;
+    if (a.replay != nullptr) {
+        iters = a.replay[scene];
+        if (iters <= 0) return;
+    }
+    const int m = a.m, neq = a.neq, n_obs = a.n_obs;
+    const int threads = blockDim.x;
+    const AmSmem lay(m, n_obs, neq, a.n_curv, a.s_cta, threads, P, CURV);
+    float* wsm = reinterpret_cast<float*>(smem + lay.w);
+    float2* osm = reinterpret_cast<float2*>(smem + lay.obs);
+    double* ksm = reinterpret_cast<double*>(smem + lay.k);
+    double* kbsm = reinterpret_cast<double*>(smem + lay.kb);
+    double* asm_ = reinterpret_cast<double*>(smem + lay.a);
+    float* csm = reinterpret_cast<float*>(smem + lay.curv);
+
+    // ---- stage constants and the scene tile once per CTA
+    for (int i = threadIdx.x; i < m * WROW / 4; i += threads)
+        reinterpret_cast<float4*>(wsm)[i] = reinterpret_cast<const float4*>(a.wrow)[i];
+    const float2* og = a.obs + (size_t)scene * n_obs * m;
+    for (int i = threadIdx.x; i < n_obs * m; i += threads) osm[i] = og[i];
+    for (int i = threadIdx.x; i < 2 * NC * KROW; i += threads) ksm[i] = a.kblk[i];
+    for (int i = threadIdx.x; i < NX * neq; i += threads) { kbsm[i] = a.kb[i]; asm_[i] = a.aeq[i]; }
+    if (CURV)
+        for (int i = threadIdx.x; i < 2 * a.n_curv; i += threads) csm[i] = a.curv[(size_t)scene * 2 * a.n_curv + i];
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31;
+    const int p = lane % P;
+    const int slot = threadIdx.x / P;
+    const int local = blockIdx.x * a.s_cta + slot;
+    const bool active = local < a.B;
+    const size_t row = (size_t)scene * a.B + (active ? local : a.B - 1);
+    double* su = reinterpret_cast<double*>(smem + lay.scr + (size_t)slot * AmSmem::SCR_BYTES);
+    float* sc = reinterpret_cast<float*>(su + 24);
+    float* dap = reinterpret_cast<float*>(smem + lay.dap) + threadIdx.x;
+    float* kap = reinterpret_cast<float*>(smem + lay.kap) + threadIdx.x;
+    const SceneLim L = a.lim[scene];
+    const double rho = a.rho;
+
+    // ---- prologue: xi_bar, equality residual correction delta = K_b (b - A xi_bar)
+    for (int k = p; k < NX; k += P) su[k] = a.xi_bar[row * NX + k];
+    __syncwarp();
+    double eb[MAX_NEQ];
+    const double* brow = a.b ? a.b + row * neq : a.bscene + (size_t)scene * neq;
+    for (int e = 0; e < neq; ++e) {
+        double s = brow[e];
+        for (int i = 0; i < NX; ++i) s = fma(-asm_[e * NX + i], su[i], s);
+        eb[e] = s;
+    }
+    double c[ROWS], ell[ROWS], dl[ROWS];
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) {
+        const int k = p + P * r;
+        c[r] = ell[r] = dl[r] = 0.0;
+        if (k < NX) {
+            c[r] = ell[r] = su[k];
+            double s = 0.0;
+            for (int e = 0; e < neq; ++e) s = fma(kbsm[k * neq + e], eb[e], s);
+            dl[r] = s;
+            sc[k] = static_cast<float>(c[r]);
+        }
+    }
+    __syncwarp();
+    float cf[NX];
+#pragma unroll
+    for (int q = 0; q < NX / 2; ++q) {
+        const float2 f = reinterpret_cast<const float2*>(sc)[q];
+        cf[2 * q] = f.x; cf[2 * q + 1] = f.y;
+    }
+
+    int conf = 0;
+    bool bad = false;
+    float v[NV];
+    sweep<P, CURV, true>(wsm, osm, csm, cf, v, dap, kap, threads, p, m, n_obs, a.n_curv, L, conf);
+    group_reduce_scatter<P>(v, lane);
+
+    const int r_lane = NX % P, r_slot = (NX / P) * P;
+    const int c_lane = (NX + 1) % P, c_slot = ((NX + 1) / P) * P;
+    float resid = 0.f, cost = 0.f;
+    const int warp_global = blockIdx.x * (threads / 32) + (threadIdx.x >> 5);
+    unsigned* itm = a.itmax + (size_t)scene * a.max_iters * ITMAX_SLOTS + (warp_global % ITMAX_SLOTS);
+
+    for (int it = 0; it < iters; ++it) {
+        // ---- coefficient update: lambda step, then c <- c + K (l - c - rho g) (+ delta on the first step)
+        const bool first = (it == 0);
+#pragma unroll
+        for (int r = 0; r < ROWS; ++r) {
+            const int k = p + P * r;
+            if (k < NX) {
+                const double g = static_cast<double>(v[P * r]);
+                if (!first) ell[r] = fma(-0.5 * rho, g, ell[r]);
+                su[k + (k >= NC ? 1 : 0)] = ell[r] - c[r] - rho * g;   // per-axis stride 12 (16-B aligned)
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < ROWS; ++r) {
+            const int k = p + P * r;
+            if (k < NX) {
+                const int ax = k >= NC ? 1 : 0;
+                const int kk = k - ax * NC;
+                const double2* kr = reinterpret_cast<const double2*>(ksm + (ax * NC + kk) * KROW);
+                const double2* ur = reinterpret_cast<const double2*>(su + ax * KROW);
+                double s0 = first ? dl[r] : 0.0, s1 = 0.0;
+#pragma unroll
+                for (int q = 0; q < NC / 2; ++q) {
+                    const double2 kq = kr[q];
+                    const double2 uq = ur[q];
+                    s0 = fma(kq.x, uq.x, s0);
+                    s1 = fma(kq.y, uq.y, s1);
+                }
+                s0 = fma(kr[NC / 2].x, su[ax * KROW + NC - 1], s0);
+                c[r] += s0 + s1;
+                bad |= !isfinite(c[r]);
+                sc[k] = static_cast<float>(c[r]);
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < NX / 2; ++q) {
+            const float2 f = reinterpret_cast<const float2*>(sc)[q];
+            cf[2 * q] = f.x; cf[2 * q + 1] = f.y;
+        }
+        // ---- projections, back-projection, residual at the new iterate
+        sweep<P, CURV, false>(wsm, osm, csm, cf, v, dap, kap, threads, p, m, n_obs, a.n_curv, L, conf);
+        group_reduce_scatter<P>(v, lane);
+        resid = v[r_slot];
+        cost = v[c_slot];
+        // ---- residual history + batch max for the batch-global early exit (pkg/projection.py:327-330)
+        const bool owner = (p == r_lane);
+        if (a.hist_out && owner && active)
+            a.hist_out[((size_t)scene * a.max_iters + it) * a.B + local] = resid;
+        if (a.replay == nullptr) {
+            float mx = owner ? resid : 0.f;
+            if (P < 32) {
+#pragma unroll
+                for (int o = 16; o >= 1; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                if (lane == 0) atomicMax(itm + (size_t)it * ITMAX_SLOTS, float_key(mx));
+            } else if (owner) {
+                atomicMax(itm + (size_t)it * ITMAX_SLOTS, float_key(resid));
+            }
+        }
+    }
+
+    // ---- outputs
+    if (active) {
+#pragma unroll
+        for (int r = 0; r < ROWS; ++r) {
+            const int k = p + P * r;
+            if (k < NX) a.xi_out[row * NX + k] = c[r];
+        }
+        if (p == r_lane) a.resid_out[row] = static_cast<double>(resid);
+        if (a.cost_out && p == c_lane) a.cost_out[row] = static_cast<double>(cost);
+    } else {
+        conf = 0;
+        bad = false;
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) conf += __shfl_xor_sync(0xffffffffu, conf, o);
+    const unsigned anybad = __ballot_sync(0xffffffffu, bad);
+    if (lane == 0) {
+        if (conf) atomicAdd(a.conflicts + scene, (unsigned long long)conf);
+        if (anybad) atomicOr(a.err, ERR_NONFINITE);
+    }
+}
+
+// Batch-global early exit (pkg/projection.py:329): first iteration whose batch max
+// residual is <= tol.  Sets iterations_used and, if that is before max_iters, the
+// replay count (the replay re-runs the deterministic kernel for exactly that many
+// iterations) and clears the scene's conflict counter for the replay.
+__global__ void exit_scan_kernel(const unsigned* itmax, int max_iters, double tol, int* iters_used, int* replay,
+                                 unsigned long long* conflicts) {
+    const int scene = blockIdx.x;
+    const unsigned* base = itmax + (size_t)scene * max_iters * ITMAX_SLOTS;
+    int first = max_iters;
+    for (int it = threadIdx.x; it < max_iters; it += blockDim.x) {
+        unsigned mx = 0;
+        for (int s = 0; s < ITMAX_SLOTS; ++s) mx = max(mx, base[(size_t)it * ITMAX_SLOTS + s]);
+        const float f = __uint_as_float(mx);
+        if (static_cast<double>(f) <= tol && it < first) first = it;
+    }
+    for (int o = 16; o >= 1; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
+    __shared__ int red[32];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = first;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x + 31) / 32; ++w) first = min(first, red[w]);
+        const int used = first < max_iters ? first + 1 : max_iters;
+        iters_used[scene] = used;
+        const int rep = used < max_iters ? used : 0;
+        if (replay) replay[scene] = rep;
+        if (rep && conflicts) conflicts[scene] = 0ull;
+    }
+}
+
+}  // namespace bd

@@ -1,0 +1,896 @@
+// C-ABI implementation (include/bilevel_b200.h): device context, constant and
+// scene upload, pointer staging and the launch sequences of the hot path.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/bilevel_b200.h"
+#include "am_kernel.cuh"
+#include "bd_common.cuh"
+#include "cem_kernels.cuh"
+#include "aux_kernels.cuh"
+#include "cvae_kernel.cuh"
+
+using namespace bd;
+
+namespace {
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { if (p) cudaFree(p); }
+    cudaError_t ensure(size_t n) {
+        if (n <= bytes) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        cudaError_t e = cudaMalloc(&p, n);
+        if (e == cudaSuccess) bytes = n;
+        return e;
+    }
+    template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+struct PendingCopy {
+    void* dst;
+    const void* src;
+    size_t bytes;
+};
+
+}  // namespace
+
+struct bd_ctx {
+    int device = 0;
+    cudaStream_t own = nullptr;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    int64_t launches = 0;
+    int opt_lanes = 0, opt_spc = 0;
+    // basis
+    int m = 0;
+    DevBuf wrow, W64, Wd64, Wdd64;
+    // stage 1
+    int m_seg = 0, with_goal = 0, neq1 = 0, dim = 0;
+    DevBuf qmx, qmy, kkt1, kinv1;
+    // projection
+    int n_obs = -1, neq = 0;
+    double rho = 1.0;
+    DevBuf kblk, kb, aeq;
+    // scenes
+    int S = 0, scene_obs = 0, n_curv = 0;
+    DevBuf obs, lim, bscene, curvf, ox64, oy64, lim64, curv64;
+    // workspace
+    DevBuf w_xibar, w_b, w_mu, w_xi, w_res, w_cost, w_hist, w_itmax, w_iters, w_replay, w_conf, w_err, w_params;
+    DevBuf stage[8];
+    int n_stage = 0;
+    std::vector<PendingCopy> pending;
+    bool host_out = false;
+    // CEM state
+    DevBuf c_mean, c_cov, c_L, c_done, c_best_idx, c_best_p, c_best_xi, c_best_s, c_stats, c_cons, c_elite, c_eaug;
+    // CVAE
+    std::vector<int> cvae_dims;
+    std::vector<DevBuf*> cvae_w, cvae_b;
+    DevBuf cvae_h0, cvae_h1, cvae_obs, cvae_z;
+    ~bd_ctx() {
+        for (auto* b : cvae_w) delete b;
+        for (auto* b : cvae_b) delete b;
+    }
+};
+
+namespace {
+
+int fail(bd_ctx* c, int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (c) c->err = buf;
+    return code;
+}
+
+#define CU(call)                                                                                  \
+    do {                                                                                          \
+        cudaError_t e_ = (call);                                                                  \
+        if (e_ != cudaSuccess) return fail(ctx, BD_ERR_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+    } while (0)
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+// Inputs: device pointers are used in place, host pointers are copied to a staging buffer.
+template <class T>
+int stage_in(bd_ctx* ctx, const T* p, size_t count, const T** out) {
+    if (!p || count == 0 || is_device_ptr(p)) { *out = p; return 0; }
+    if (ctx->n_stage >= 8) return fail(ctx, BD_ERR_STATE, "too many staged inputs");
+    DevBuf& b = ctx->stage[ctx->n_stage++];
+    CU(b.ensure(count * sizeof(T)));
+    CU(cudaMemcpyAsync(b.p, p, count * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+    *out = b.as<T>();
+    return 0;
+}
+
+// Outputs: device pointers are written directly; host pointers get a workspace buffer + a D2H copy.
+template <class T>
+int stage_out(bd_ctx* ctx, T* user, size_t count, DevBuf& ws, T** out) {
+    if (!user || count == 0) { *out = nullptr; return 0; }
+    if (is_device_ptr(user)) { *out = user; return 0; }
+    CU(ws.ensure(count * sizeof(T)));
+    *out = ws.as<T>();
+    ctx->pending.push_back({user, ws.p, count * sizeof(T)});
+    ctx->host_out = true;
+    return 0;
+}
+
+// Same, but the kernel always needs a device buffer (the output is consumed internally).
+template <class T>
+int stage_out_req(bd_ctx* ctx, T* user, size_t count, DevBuf& ws, T** out) {
+    if (user && is_device_ptr(user)) { *out = user; return 0; }
+    CU(ws.ensure(count * sizeof(T)));
+    *out = ws.as<T>();
+    if (user) {
+        ctx->pending.push_back({user, ws.p, count * sizeof(T)});
+        ctx->host_out = true;
+    }
+    return 0;
+}
+
+void begin_call(bd_ctx* ctx) {
+    ctx->n_stage = 0;
+    ctx->pending.clear();
+    ctx->host_out = false;
+    cudaSetDevice(ctx->device);
+}
+
+int finish_call(bd_ctx* ctx, bool check_err, int n_err) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(ctx, BD_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
+    for (auto& pc : ctx->pending) CU(cudaMemcpyAsync(pc.dst, pc.src, pc.bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    const bool sync = ctx->host_out || check_err;
+    if (!sync) return 0;
+    CU(cudaStreamSynchronize(ctx->stream));
+    if (check_err && n_err > 0) {
+        std::vector<int> errs(n_err);
+        CU(cudaMemcpy(errs.data(), ctx->w_err.p, n_err * sizeof(int), cudaMemcpyDeviceToHost));
+        int bits = 0;
+        for (int v : errs) bits |= v;
+        if (bits & ERR_KKT_RESID) return fail(ctx, BD_ERR_NUMERICAL, "KKT residual exceeds tolerance");
+        if (bits & ERR_NONFINITE) return fail(ctx, BD_ERR_NUMERICAL, "projection iterate is not finite");
+    }
+    return 0;
+}
+
+template <class K>
+void raise_smem(K kernel, size_t bytes) {
+    if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+int pick_lanes(bd_ctx* ctx, long total) {
+    if (ctx->opt_lanes) return ctx->opt_lanes;
+    if (total <= 2500) return 32;
+    if (total <= 5000) return 16;
+    if (total <= 12000) return 8;
+    return 4;
+}
+
+template <int P, bool CURV>
+int launch_am_t(bd_ctx* ctx, AmArgs a, int threads, bool replay_pass) {
+    const AmSmem lay(a.m, a.n_obs, a.neq, a.n_curv, a.s_cta, threads, P, CURV);
+    if (lay.total > 227 * 1024) return fail(ctx, BD_ERR_VALUE, "AM kernel needs %zu B of shared memory", lay.total);
+    raise_smem(am_kernel<P, CURV>, lay.total);
+    dim3 grid((a.B + a.s_cta - 1) / a.s_cta, ctx->S);
+    if (!replay_pass) a.replay = nullptr;
+    am_kernel<P, CURV><<<grid, threads, lay.total, ctx->stream>>>(a);
+    ctx->launches++;
+    return 0;
+}
+
+int launch_am(bd_ctx* ctx, AmArgs a, bool replay_pass) {
+    const long total = (long)a.B * ctx->S;
+    const int P = pick_lanes(ctx, total);
+    int threads = ctx->opt_spc ? ctx->opt_spc * P : (P == 32 ? 64 : 128);
+    if (threads % 32 || threads > 256 || threads < 32) return fail(ctx, BD_ERR_VALUE, "bad samples_per_cta");
+    a.s_cta = threads / P;
+    const bool curv = a.n_curv > 0;
+#define AM_CASE(PP)                                                                       \
+    case PP:                                                                              \
+        return curv ? launch_am_t<PP, true>(ctx, a, threads, replay_pass)                 \
+                    : launch_am_t<PP, false>(ctx, a, threads, replay_pass);
+    switch (P) {
+        AM_CASE(4)
+        AM_CASE(8)
+        AM_CASE(16)
+        AM_CASE(32)
+        default: return fail(ctx, BD_ERR_VALUE, "lanes_per_sample must be 4, 8, 16 or 32");
+    }
+#undef AM_CASE
+}
+
+int require_solver(bd_ctx* ctx, bool need_stage1) {
+    if (!ctx->m) return fail(ctx, BD_ERR_STATE, "basis not set");
+    if (ctx->n_obs < 0) return fail(ctx, BD_ERR_STATE, "projection not set");
+    if (!ctx->S) return fail(ctx, BD_ERR_STATE, "scenes not set");
+    if (ctx->scene_obs != ctx->n_obs)
+        return fail(ctx, BD_ERR_VALUE, "operator was built for %d obstacles, spec has %d", ctx->n_obs, ctx->scene_obs);
+    if (need_stage1 && !ctx->dim) return fail(ctx, BD_ERR_STATE, "stage-1 QP not set");
+    if (need_stage1 && ctx->neq1 != ctx->neq) return fail(ctx, BD_ERR_STATE, "stage-1 / projection neq mismatch");
+    return 0;
+}
+
+// Projection core: xi_bar, b device pointers -> outputs in device buffers.
+int run_projection(bd_ctx* ctx, int B, const double* xi_bar, const double* b, int iters, double tol, double* xi,
+                   double* res, double* cost, float* hist, int* iters_used, unsigned long long* conf) {
+    const int S = ctx->S;
+    CU(ctx->w_itmax.ensure((size_t)S * iters * ITMAX_SLOTS * 4));
+    CU(ctx->w_replay.ensure((size_t)S * 4));
+    CU(cudaMemsetAsync(ctx->w_itmax.p, 0, (size_t)S * iters * ITMAX_SLOTS * 4, ctx->stream));
+    CU(cudaMemsetAsync(conf, 0, (size_t)S * 8, ctx->stream));
+    AmArgs a{};
+    a.m = ctx->m; a.neq = ctx->neq; a.n_obs = ctx->n_obs; a.n_curv = ctx->n_curv; a.B = B; a.max_iters = iters;
+    a.rho = ctx->rho;
+    a.wrow = ctx->wrow.as<float>(); a.kblk = ctx->kblk.as<double>(); a.kb = ctx->kb.as<double>();
+    a.aeq = ctx->aeq.as<double>(); a.obs = ctx->obs.as<float2>(); a.lim = ctx->lim.as<SceneLim>();
+    a.bscene = ctx->bscene.as<double>(); a.curv = ctx->curvf.as<float>();
+    a.xi_bar = xi_bar; a.b = b; a.xi_out = xi; a.resid_out = res; a.cost_out = cost; a.hist_out = hist;
+    a.itmax = ctx->w_itmax.as<unsigned>(); a.conflicts = conf; a.err = ctx->w_err.as<int>();
+    a.replay = ctx->w_replay.as<int>();
+    int rc = launch_am(ctx, a, false);
+    if (rc) return rc;
+    exit_scan_kernel<<<S, 128, 0, ctx->stream>>>(a.itmax, iters, tol, iters_used, ctx->w_replay.as<int>(), conf);
+    ctx->launches++;
+    return launch_am(ctx, a, true);
+}
+
+int run_stage1(bd_ctx* ctx, int B, const double* params, double* xi_bar, double* mu, double* b_out) {
+    S1Args s{};
+    s.total = ctx->S * B; s.B = B; s.dim = ctx->dim; s.neq = ctx->neq1; s.m_seg = ctx->m_seg;
+    s.with_goal = ctx->with_goal; s.nr = NX + ctx->neq1; s.nvar = NX;
+    s.qmx = ctx->qmx.as<double>(); s.qmy = ctx->qmy.as<double>(); s.kkt = ctx->kkt1.as<double>();
+    s.kinv = ctx->kinv1.as<double>(); s.params = params; s.bscene = ctx->bscene.as<double>();
+    s.xi_bar = xi_bar; s.mu = mu; s.b_out = b_out; s.err = ctx->w_err.as<int>();
+    const int warps = 8;
+    const size_t smem = (size_t)(2 * s.nr * s.nr + 2 * NC * s.m_seg) * 8;
+    raise_smem(stage1_kernel, smem);
+    stage1_kernel<<<(s.total + warps - 1) / warps, warps * 32, smem, ctx->stream>>>(s);
+    ctx->launches++;
+    return 0;
+}
+
+}  // namespace
+
+// =====================================================================================
+extern "C" {
+
+int bd_abi_version(void) { return BD_ABI_VERSION; }
+
+int bd_create(int device, bd_ctx** out) {
+    if (!out) return BD_ERR_VALUE;
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return BD_ERR_CUDA;
+    }
+    if (device < 0 || device >= n) return BD_ERR_VALUE;
+    bd_ctx* ctx = new bd_ctx();
+    ctx->device = device;
+    cudaSetDevice(device);
+    if (cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking) != cudaSuccess) {
+        delete ctx;
+        return BD_ERR_CUDA;
+    }
+    ctx->stream = ctx->own;
+    *out = ctx;
+    return 0;
+}
+
+void bd_destroy(bd_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->own) cudaStreamDestroy(ctx->own);
+    delete ctx;
+}
+
+const char* bd_last_error(const bd_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int bd_set_stream(bd_ctx* ctx, void* s) {
+    if (!ctx) return BD_ERR_VALUE;
+    ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own;
+    return 0;
+}
+
+int bd_synchronize(bd_ctx* ctx) {
+    if (!ctx) return BD_ERR_VALUE;
+    cudaSetDevice(ctx->device);
+    CU(cudaStreamSynchronize(ctx->stream));
+    return 0;
+}
+
+int bd_set_option(bd_ctx* ctx, const char* key, int value) {
+    if (!ctx || !key) return BD_ERR_VALUE;
+    if (!strcmp(key, "lanes_per_sample")) {
+        if (value != 0 && value != 4 && value != 8 && value != 16 && value != 32)
+            return fail(ctx, BD_ERR_VALUE, "lanes_per_sample must be 0, 4, 8, 16 or 32");
+        ctx->opt_lanes = value;
+        return 0;
+    }
+    if (!strcmp(key, "samples_per_cta")) {
+        ctx->opt_spc = value < 0 ? 0 : value;
+        return 0;
+    }
+    return fail(ctx, BD_ERR_VALUE, "unknown option %s", key);
+}
+
+int64_t bd_launch_count(const bd_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+int bd_error_bits(bd_ctx* ctx, int* bits) {
+    if (!ctx || !bits) return BD_ERR_VALUE;
+    cudaSetDevice(ctx->device);
+    CU(cudaStreamSynchronize(ctx->stream));
+    *bits = 0;
+    if (!ctx->S || !ctx->w_err.p) return 0;
+    std::vector<int> errs(ctx->S);
+    CU(cudaMemcpy(errs.data(), ctx->w_err.p, ctx->S * sizeof(int), cudaMemcpyDeviceToHost));
+    for (int v : errs) *bits |= v;
+    return 0;
+}
+
+int bd_set_basis(bd_ctx* ctx, int m, int n, const double* W, const double* Wd, const double* Wdd) {
+    if (!ctx) return BD_ERR_VALUE;
+    if (n != NC) return fail(ctx, BD_ERR_VALUE, "this build supports order-10 bases (n=%d), got n=%d", NC, n);
+    if (m < n || m > 4096 || !W || !Wd || !Wdd) return fail(ctx, BD_ERR_VALUE, "bad basis shape m=%d", m);
+    begin_call(ctx);
+    std::vector<float> rows((size_t)m * WROW, 0.f);
+    for (int t = 0; t < m; ++t)
+        for (int k = 0; k < NC; ++k) {
+            rows[(size_t)t * WROW + k] = (float)W[t * n + k];
+            rows[(size_t)t * WROW + NC + k] = (float)Wd[t * n + k];
+            rows[(size_t)t * WROW + 2 * NC + k] = (float)Wdd[t * n + k];
+        }
+    CU(ctx->wrow.ensure(rows.size() * 4));
+    CU(cudaMemcpy(ctx->wrow.p, rows.data(), rows.size() * 4, cudaMemcpyHostToDevice));
+    const size_t bytes = (size_t)m * n * 8;
+    CU(ctx->W64.ensure(bytes));
+    CU(ctx->Wd64.ensure(bytes));
+    CU(ctx->Wdd64.ensure(bytes));
+    CU(cudaMemcpy(ctx->W64.p, W, bytes, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(ctx->Wd64.p, Wd, bytes, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(ctx->Wdd64.p, Wdd, bytes, cudaMemcpyHostToDevice));
+    ctx->m = m;
+    return 0;
+}
+
+int bd_set_stage1(bd_ctx* ctx, int m_seg, int with_goal, int neq, const double* qmx, const double* qmy,
+                  const double* kkt, const double* kinv) {
+    if (!ctx) return BD_ERR_VALUE;
+    const int dim = 2 * m_seg + (with_goal ? 2 : 0);
+    if (m_seg < 1 || dim > MAX_DIM || neq < 1 || neq > MAX_NEQ || NX + neq > 32)
+        return fail(ctx, BD_ERR_VALUE, "unsupported stage-1 layout m_seg=%d neq=%d", m_seg, neq);
+    if (with_goal && neq < 9) return fail(ctx, BD_ERR_VALUE, "goal layout needs 9 equality rows");
+    begin_call(ctx);
+    const int nr = NX + neq;
+    CU(ctx->qmx.ensure((size_t)NC * m_seg * 8));
+    CU(ctx->qmy.ensure((size_t)NC * m_seg * 8));
+    CU(ctx->kkt1.ensure((size_t)nr * nr * 8));
+    CU(ctx->kinv1.ensure((size_t)nr * nr * 8));
+    CU(cudaMemcpy(ctx->qmx.p, qmx, (size_t)NC * m_seg * 8, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(ctx->qmy.p, qmy, (size_t)NC * m_seg * 8, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(ctx->kkt1.p, kkt, (size_t)nr * nr * 8, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(ctx->kinv1.p, kinv, (size_t)nr * nr * 8, cudaMemcpyHostToDevice));
+    ctx->m_seg = m_seg;
+    ctx->with_goal = with_goal ? 1 : 0;
+    ctx->neq1 = neq;
+    ctx->dim = dim;
+    return 0;
+}
+
+int bd_set_projection(bd_ctx* ctx, int n_obs, double rho, int neq, const double* kinv, const double* a_eq) {
+    if (!ctx) return BD_ERR_VALUE;
+    if (n_obs < 0 || neq < 1 || neq > MAX_NEQ || !(rho > 0) || !kinv || !a_eq)
+        return fail(ctx, BD_ERR_VALUE, "bad projection arguments");
+    begin_call(ctx);
+    const int nr = NX + neq;
+    for (int i = 0; i < NC; ++i)
+        for (int j = NC; j < NX; ++j)
+            if (kinv[i * nr + j] != 0.0 || kinv[j * nr + i] != 0.0)
+                return fail(ctx, BD_ERR_STRUCTURE, "augmented KKT inverse couples the x and y blocks");
+    std::vector<double> kb((size_t)2 * NC * KROW, 0.0), kbx((size_t)NX * neq), ae((size_t)neq * NX);
+    for (int ax = 0; ax < 2; ++ax)
+        for (int i = 0; i < NC; ++i)
+            for (int j = 0; j < NC; ++j) kb[(ax * NC + i) * KROW + j] = kinv[(ax * NC + i) * nr + ax * NC + j];
+    for (int i = 0; i < NX; ++i)
+        for (int e = 0; e < neq; ++e) kbx[i * neq + e] = kinv[i * nr + NX + e];
+    memcpy(ae.data(), a_eq, ae.size() * 8);
+    CU(ctx->kblk.ensure(kb.size() * 8));
+    CU(ctx->kb.ensure(kbx.size() * 8));
+    CU(ctx->aeq.ensure(ae.size() * 8));
+    CU(cudaMemcpy(ctx->kblk.p, kb.data(), kb.size() * 8, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(ctx->kb.p, kbx.data(), kbx.size() * 8, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(ctx->aeq.p, ae.data(), ae.size() * 8, cudaMemcpyHostToDevice));
+    ctx->n_obs = n_obs;
+    ctx->rho = rho;
+    ctx->neq = neq;
+    return 0;
+}
+
+int bd_set_scenes(bd_ctx* ctx, int S, int n_obs, int m, const double* ox, const double* oy, const bd_limits* L,
+                  const double* b0, int n_curv, const double* cx, const double* ck) {
+    if (!ctx) return BD_ERR_VALUE;
+    if (S < 1 || n_obs < 0 || !L || !b0 || n_curv < 0 || n_curv > 1024)
+        return fail(ctx, BD_ERR_VALUE, "bad scene arguments");
+    if (ctx->m && m != ctx->m) return fail(ctx, BD_ERR_VALUE, "constraint spec and basis disagree on the time grid");
+    if (n_curv > 0 && (!cx || !ck)) return fail(ctx, BD_ERR_VALUE, "curvature table missing");
+    if (n_obs > 0 && (!ox || !oy)) return fail(ctx, BD_ERR_VALUE, "obstacles missing");
+    begin_call(ctx);
+    const int neq = ctx->neq ? ctx->neq : 6;
+    const size_t no = (size_t)S * n_obs * m;
+    std::vector<float2> obs(no ? no : 1);
+    std::vector<SceneLim> lim(S);
+    std::vector<double> bs((size_t)S * neq, 0.0), l64((size_t)S * 9);
+    for (int s = 0; s < S; ++s) {
+        const bd_limits& l = L[s];
+        if (!(l.v_min < l.v_max) || !(l.ellipse_a > 0) || !(l.ellipse_b > 0) || !(l.a_max > 0) ||
+            !(l.kappa_max > 0) || !(l.c_max > 0) || !(l.y_lb < l.y_ub))
+            return fail(ctx, BD_ERR_VALUE, "invalid constraint limits for scene %d", s);
+        SceneLim& q = lim[s];
+        q.a = (float)l.ellipse_a; q.b = (float)l.ellipse_b;
+        q.inv_a = (float)(1.0 / l.ellipse_a); q.inv_b = (float)(1.0 / l.ellipse_b);
+        q.v_min = (float)l.v_min; q.v_max = (float)l.v_max; q.a_max = (float)l.a_max;
+        q.k_max = (float)l.kappa_max; q.inv_k_max = (float)(1.0 / l.kappa_max); q.c_max = (float)l.c_max;
+        q.y_lb = (float)l.y_lb; q.y_ub = (float)l.y_ub;
+        const double v9[9] = {l.ellipse_a, l.ellipse_b, l.v_min, l.v_max, l.a_max, l.kappa_max, l.c_max, l.y_lb, l.y_ub};
+        memcpy(&l64[(size_t)s * 9], v9, sizeof v9);
+        for (int e = 0; e < 6 && e < neq; ++e) bs[(size_t)s * neq + e] = b0[s * 6 + e];
+        for (size_t i = 0; i < (size_t)n_obs * m; ++i) {
+            const size_t g = (size_t)s * n_obs * m + i;
+            obs[g] = make_float2((float)(ox[g] / l.ellipse_a), (float)(oy[g] / l.ellipse_b));
+        }
+    }
+    CU(ctx->obs.ensure(obs.size() * sizeof(float2)));
+    CU(ctx->lim.ensure(lim.size() * sizeof(SceneLim)));
+    CU(ctx->bscene.ensure(bs.size() * 8));
+    CU(ctx->lim64.ensure(l64.size() * 8));
+    CU(cudaMemcpy(ctx->obs.p, obs.data(), obs.size() * sizeof(float2), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(ctx->lim.p, lim.data(), lim.size() * sizeof(SceneLim), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(ctx->bscene.p, bs.data(), bs.size() * 8, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(ctx->lim64.p, l64.data(), l64.size() * 8, cudaMemcpyHostToDevice));
+    CU(ctx->ox64.ensure(no ? no * 8 : 8));
+    CU(ctx->oy64.ensure(no ? no * 8 : 8));
+    if (no) {
+        CU(cudaMemcpy(ctx->ox64.p, ox, no * 8, cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(ctx->oy64.p, oy, no * 8, cudaMemcpyHostToDevice));
+    }
+    if (n_curv > 0) {
+        std::vector<float> cf((size_t)S * 2 * n_curv);
+        std::vector<double> cd((size_t)S * 2 * n_curv);
+        for (int s = 0; s < S; ++s)
+            for (int i = 0; i < n_curv; ++i) {
+                if (i > 0 && !(cx[s * n_curv + i] > cx[s * n_curv + i - 1]))
+                    return fail(ctx, BD_ERR_VALUE, "curvature abscissae must increase");
+                cd[(size_t)s * 2 * n_curv + i] = cx[s * n_curv + i];
+                cd[(size_t)s * 2 * n_curv + n_curv + i] = ck[s * n_curv + i];
+                cf[(size_t)s * 2 * n_curv + i] = (float)cx[s * n_curv + i];
+                cf[(size_t)s * 2 * n_curv + n_curv + i] = (float)ck[s * n_curv + i];
+            }
+        CU(ctx->curvf.ensure(cf.size() * 4));
+        CU(ctx->curv64.ensure(cd.size() * 8));
+        CU(cudaMemcpy(ctx->curvf.p, cf.data(), cf.size() * 4, cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(ctx->curv64.p, cd.data(), cd.size() * 8, cudaMemcpyHostToDevice));
+    }
+    CU(ctx->w_err.ensure((size_t)S * 4));
+    CU(cudaMemset(ctx->w_err.p, 0, (size_t)S * 4));
+    ctx->S = S;
+    ctx->scene_obs = n_obs;
+    ctx->n_curv = n_curv;
+    return 0;
+}
+
+int bd_stage1(bd_ctx* ctx, int S, int B, const double* params, double* xi_bar, double* mu, double* b_out) {
+    if (!ctx) return BD_ERR_VALUE;
+    int rc = require_solver(ctx, true);
+    if (rc) return rc;
+    if (S != ctx->S || B < 1 || !params) return fail(ctx, BD_ERR_VALUE, "bad batch (S=%d, B=%d)", S, B);
+    begin_call(ctx);
+    const size_t tot = (size_t)S * B;
+    const double* dp;
+    double *dx, *dm, *db;
+    if ((rc = stage_in(ctx, params, tot * ctx->dim, &dp))) return rc;
+    if ((rc = stage_out(ctx, xi_bar, tot * NX, ctx->w_xibar, &dx))) return rc;
+    if ((rc = stage_out(ctx, mu, tot * ctx->neq1, ctx->w_mu, &dm))) return rc;
+    if ((rc = stage_out(ctx, b_out, tot * ctx->neq1, ctx->w_b, &db))) return rc;
+    CU(cudaMemsetAsync(ctx->w_err.p, 0, (size_t)S * 4, ctx->stream));
+    if ((rc = run_stage1(ctx, B, dp, dx, dm, db))) return rc;
+    return finish_call(ctx, ctx->host_out, S);
+}
+
+int bd_project(bd_ctx* ctx, int S, int B, const double* xi_bar, const double* b, int iters, double tol, double* xi,
+               double* res, double* cost, float* hist, int* iters_used, int64_t* conflicts) {
+    if (!ctx) return BD_ERR_VALUE;
+    int rc = require_solver(ctx, false);
+    if (rc) return rc;
+    if (S != ctx->S || B < 1 || !xi_bar || !xi || !res || iters < 1 || !(tol > 0))
+        return fail(ctx, BD_ERR_VALUE, "bad projection call (S=%d, B=%d, iters=%d)", S, B, iters);
+    begin_call(ctx);
+    const size_t tot = (size_t)S * B;
+    const double *dxb, *dbb;
+    double *dxi, *dres, *dcost;
+    float* dh;
+    int* dit;
+    unsigned long long* dconf;
+    if ((rc = stage_in(ctx, xi_bar, tot * NX, &dxb))) return rc;
+    if ((rc = stage_in(ctx, b, b ? tot * ctx->neq : 0, &dbb))) return rc;
+    if ((rc = stage_out(ctx, xi, tot * NX, ctx->w_xi, &dxi))) return rc;
+    if ((rc = stage_out(ctx, res, tot, ctx->w_res, &dres))) return rc;
+    if ((rc = stage_out(ctx, cost, tot, ctx->w_cost, &dcost))) return rc;
+    if ((rc = stage_out(ctx, hist, (size_t)S * iters * B, ctx->w_hist, &dh))) return rc;
+    if ((rc = stage_out_req(ctx, iters_used, (size_t)S, ctx->w_iters, &dit))) return rc;
+    if ((rc = stage_out_req(ctx, reinterpret_cast<unsigned long long*>(conflicts), (size_t)S, ctx->w_conf, &dconf)))
+        return rc;
+    CU(cudaMemsetAsync(ctx->w_err.p, 0, (size_t)S * 4, ctx->stream));
+    if ((rc = run_projection(ctx, B, dxb, dbb, iters, tol, dxi, dres, dcost, dh, dit, dconf))) return rc;
+    return finish_call(ctx, ctx->host_out, S);
+}
+
+int bd_solve_lower(bd_ctx* ctx, int S, int B, const double* params, int iters, double tol, double* xi_bar,
+                   double* mu, double* xi, double* res, double* cost, float* hist, int* iters_used,
+                   int64_t* conflicts) {
+    if (!ctx) return BD_ERR_VALUE;
+    int rc = require_solver(ctx, true);
+    if (rc) return rc;
+    if (S != ctx->S || B < 1 || !params || !xi || !res || iters < 1 || !(tol > 0))
+        return fail(ctx, BD_ERR_VALUE, "bad solve call (S=%d, B=%d, iters=%d)", S, B, iters);
+    begin_call(ctx);
+    const size_t tot = (size_t)S * B;
+    const double* dp;
+    double *dxb, *dmu, *dxi, *dres, *dcost, *db = nullptr;
+    float* dh;
+    int* dit;
+    unsigned long long* dconf;
+    if ((rc = stage_in(ctx, params, tot * ctx->dim, &dp))) return rc;
+    if ((rc = stage_out_req(ctx, xi_bar, tot * NX, ctx->w_xibar, &dxb))) return rc;
+    if ((rc = stage_out(ctx, mu, tot * ctx->neq, ctx->w_mu, &dmu))) return rc;
+    if ((rc = stage_out(ctx, xi, tot * NX, ctx->w_xi, &dxi))) return rc;
+    if ((rc = stage_out(ctx, res, tot, ctx->w_res, &dres))) return rc;
+    if ((rc = stage_out(ctx, cost, tot, ctx->w_cost, &dcost))) return rc;
+    if ((rc = stage_out(ctx, hist, (size_t)S * iters * B, ctx->w_hist, &dh))) return rc;
+    if ((rc = stage_out_req(ctx, iters_used, (size_t)S, ctx->w_iters, &dit))) return rc;
+    if ((rc = stage_out_req(ctx, reinterpret_cast<unsigned long long*>(conflicts), (size_t)S, ctx->w_conf, &dconf)))
+        return rc;
+    if (ctx->with_goal) {
+        CU(ctx->w_b.ensure(tot * ctx->neq * 8));
+        db = ctx->w_b.as<double>();
+    }
+    CU(cudaMemsetAsync(ctx->w_err.p, 0, (size_t)S * 4, ctx->stream));
+    if ((rc = run_stage1(ctx, B, dp, dxb, dmu, db))) return rc;
+    if ((rc = run_projection(ctx, B, dxb, db, iters, tol, dxi, dres, dcost, dh, dit, dconf))) return rc;
+    return finish_call(ctx, ctx->host_out, S);
+}
+
+int bd_eval(bd_ctx* ctx, int count, const double* xi, double* x, double* y, double* xd, double* yd, double* xdd,
+            double* ydd) {
+    if (!ctx) return BD_ERR_VALUE;
+    if (!ctx->m) return fail(ctx, BD_ERR_STATE, "basis not set");
+    if (count < 1 || !xi) return fail(ctx, BD_ERR_VALUE, "bad eval call");
+    begin_call(ctx);
+    int rc;
+    const size_t n = (size_t)count * ctx->m;
+    const double* dxi;
+    double* o[6];
+    double* user[6] = {x, y, xd, yd, xdd, ydd};
+    if ((rc = stage_in(ctx, xi, (size_t)count * NX, &dxi))) return rc;
+    DevBuf* ws[6] = {&ctx->stage[2], &ctx->stage[3], &ctx->stage[4], &ctx->stage[5], &ctx->stage[6], &ctx->stage[7]};
+    for (int q = 0; q < 6; ++q)
+        if ((rc = stage_out(ctx, user[q], n, *ws[q], &o[q]))) return rc;
+    eval_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(count, ctx->m, ctx->W64.as<double>(),
+                                                                       ctx->Wd64.as<double>(), ctx->Wdd64.as<double>(),
+                                                                       dxi, o[0], o[1], o[2], o[3], o[4], o[5]);
+    ctx->launches++;
+    return finish_call(ctx, false, 0);
+}
+
+int bd_residuals(bd_ctx* ctx, int S, int B, const double* xi, double* out) {
+    if (!ctx) return BD_ERR_VALUE;
+    if (!ctx->m || !ctx->S) return fail(ctx, BD_ERR_STATE, "basis / scenes not set");
+    if (S != ctx->S || B < 1 || !xi || !out) return fail(ctx, BD_ERR_VALUE, "bad residual call");
+    begin_call(ctx);
+    int rc;
+    const size_t tot = (size_t)S * B;
+    const double* dxi;
+    double* dout;
+    if ((rc = stage_in(ctx, xi, tot * NX, &dxi))) return rc;
+    if ((rc = stage_out(ctx, out, tot, ctx->w_res, &dout))) return rc;
+    ResArgs r{};
+    r.total = (int)tot; r.B = B; r.m = ctx->m; r.n_obs = ctx->scene_obs; r.n_curv = ctx->n_curv;
+    r.W = ctx->W64.as<double>(); r.Wd = ctx->Wd64.as<double>(); r.Wdd = ctx->Wdd64.as<double>();
+    r.ox = ctx->ox64.as<double>(); r.oy = ctx->oy64.as<double>(); r.lim = ctx->lim64.as<double>();
+    r.curv = ctx->curv64.as<double>(); r.xi = dxi; r.out = dout;
+    residual_kernel<<<(unsigned)((tot + 7) / 8), 256, 0, ctx->stream>>>(r);
+    ctx->launches++;
+    return finish_call(ctx, false, 0);
+}
+
+int bd_kkt_solve(bd_ctx* ctx, int nvar, int neq, const double* kkt, const double* kinv, int count,
+                 const double* rhs, double* sol) {
+    if (!ctx) return BD_ERR_VALUE;
+    const int nr = nvar + neq;
+    if (nvar < 1 || neq < 0 || nr > 32 || count < 1 || !kkt || !kinv || !rhs || !sol)
+        return fail(ctx, BD_ERR_VALUE, "bd_kkt_solve supports nvar + neq <= 32");
+    begin_call(ctx);
+    int rc;
+    const double *dk, *dki, *dr;
+    double* ds;
+    if ((rc = stage_in(ctx, kkt, (size_t)nr * nr, &dk))) return rc;
+    if ((rc = stage_in(ctx, kinv, (size_t)nr * nr, &dki))) return rc;
+    if ((rc = stage_in(ctx, rhs, (size_t)count * nr, &dr))) return rc;
+    if ((rc = stage_out(ctx, sol, (size_t)count * nr, ctx->w_xibar, &ds))) return rc;
+    CU(ctx->w_err.ensure(4 * (size_t)(ctx->S > 1 ? ctx->S : 1)));
+    CU(cudaMemsetAsync(ctx->w_err.p, 0, 4, ctx->stream));
+    S1Args s{};
+    s.total = count; s.B = count; s.nr = nr; s.nvar = nvar; s.neq = neq;
+    s.kkt = dk; s.kinv = dki; s.rhs_in = dr; s.sol_out = ds; s.err = ctx->w_err.as<int>();
+    const size_t smem = (size_t)(2 * nr * nr) * 8;
+    raise_smem(stage1_kernel, smem);
+    stage1_kernel<<<(count + 7) / 8, 256, smem, ctx->stream>>>(s);
+    ctx->launches++;
+    return finish_call(ctx, true, 1);
+}
+
+int bd_sample(bd_ctx* ctx, int dim, int count, const double* mean, const double* cov, const double* z,
+              double* params) {
+    if (!ctx) return BD_ERR_VALUE;
+    if (dim < 1 || dim > MAX_DIM || count < 1 || !mean || !cov || !z || !params)
+        return fail(ctx, BD_ERR_VALUE, "bad sample call");
+    begin_call(ctx);
+    int rc;
+    const double *dm, *dc, *dz;
+    double* dp;
+    if ((rc = stage_in(ctx, mean, (size_t)dim, &dm))) return rc;
+    if ((rc = stage_in(ctx, cov, (size_t)dim * dim, &dc))) return rc;
+    if ((rc = stage_in(ctx, z, (size_t)count * dim, &dz))) return rc;
+    if ((rc = stage_out(ctx, params, (size_t)count * dim, ctx->w_params, &dp))) return rc;
+    const int blocks = count / 256 + 1 < 64 ? count / 256 + 1 : 64;
+    sample_one_kernel<<<blocks, 256, 0, ctx->stream>>>(dim, count, dm, dc, dz, dp);
+    ctx->launches++;
+    return finish_call(ctx, false, 0);
+}
+
+int bd_rank_refit(bd_ctx* ctx, int S, int B, int dim, const double* resid, const double* cost, const double* params,
+                  int n_cons, int n_elite, double w_res, double eta, double gamma, double* mean, double* cov,
+                  int64_t* cons_idx, int64_t* elite_idx, double* elite_aug, double* stats) {
+    if (!ctx) return BD_ERR_VALUE;
+    if (S < 1 || B < 1 || !resid || !cost || !params || !mean || !cov || dim < 1 || dim > MAX_DIM)
+        return fail(ctx, BD_ERR_VALUE, "bad rank_refit call");
+    if (!(n_elite <= n_cons && n_cons <= B) || n_elite < 1 || n_cons > 1024)
+        return fail(ctx, BD_ERR_VALUE, "need 1 <= elites <= constraint_elites <= min(batch, 1024)");
+    if (B > 8192) return fail(ctx, BD_ERR_VALUE, "rank_refit supports at most 8192 samples per scene");
+    begin_call(ctx);
+    int rc;
+    const size_t tot = (size_t)S * B;
+    const double *dr, *dc, *dp;
+    if ((rc = stage_in(ctx, resid, tot, &dr))) return rc;
+    if ((rc = stage_in(ctx, cost, tot, &dc))) return rc;
+    if ((rc = stage_in(ctx, params, tot * dim, &dp))) return rc;
+    CU(ctx->c_mean.ensure((size_t)S * dim * 8));
+    CU(ctx->c_cov.ensure((size_t)S * dim * dim * 8));
+    CU(ctx->c_L.ensure((size_t)S * dim * dim * 8));
+    CU(ctx->c_done.ensure((size_t)S * 4));
+    CU(ctx->c_best_idx.ensure((size_t)S * 8));
+    CU(ctx->c_best_p.ensure((size_t)S * dim * 8));
+    CU(ctx->c_best_xi.ensure((size_t)S * NX * 8));
+    CU(ctx->c_best_s.ensure((size_t)S * 3 * 8));
+    CU(ctx->w_err.ensure((size_t)S * 4));
+    CU(ctx->w_xi.ensure(tot * NX * 8));
+    CU(cudaMemcpyAsync(ctx->c_mean.p, mean, (size_t)S * dim * 8, cudaMemcpyDefault, ctx->stream));
+    CU(cudaMemcpyAsync(ctx->c_cov.p, cov, (size_t)S * dim * dim * 8, cudaMemcpyDefault, ctx->stream));
+    CU(cudaMemsetAsync(ctx->w_err.p, 0, (size_t)S * 4, ctx->stream));
+    CU(cudaMemsetAsync(ctx->c_done.p, 0, (size_t)S * 4, ctx->stream));
+    int64_t *dci, *dei;
+    double *dea, *dst;
+    if ((rc = stage_out(ctx, cons_idx, (size_t)S * n_cons, ctx->c_cons, &dci))) return rc;
+    if ((rc = stage_out(ctx, elite_idx, (size_t)S * n_elite, ctx->c_elite, &dei))) return rc;
+    if ((rc = stage_out(ctx, elite_aug, (size_t)S * n_elite, ctx->c_eaug, &dea))) return rc;
+    if ((rc = stage_out(ctx, stats, (size_t)S * 6, ctx->c_stats, &dst))) return rc;
+    CemState s{};
+    s.S = S; s.B = B; s.dim = dim; s.n_cons = n_cons; s.n_elite = n_elite; s.iters = 1;
+    s.eta = eta; s.gamma = gamma; s.w_res = w_res;
+    s.mean = ctx->c_mean.as<double>(); s.cov = ctx->c_cov.as<double>(); s.L = ctx->c_L.as<double>();
+    s.err = ctx->w_err.as<int>(); s.done = ctx->c_done.as<int>();
+    s.resid = dr; s.cost = dc; s.params = dp; s.xi = ctx->w_xi.as<double>();
+    s.cons_idx = reinterpret_cast<long long*>(dci); s.elite_idx = reinterpret_cast<long long*>(dei);
+    s.elite_aug = dea; s.stats = dst;
+    s.best_index = ctx->c_best_idx.as<long long>(); s.best_params = ctx->c_best_p.as<double>();
+    s.best_xi = ctx->c_best_xi.as<double>(); s.best_scal = ctx->c_best_s.as<double>();
+    int np2 = 1;
+    while (np2 < B) np2 <<= 1;
+    const size_t smem = (size_t)np2 * 12;
+    raise_smem(rank_refit_kernel, smem);
+    rank_refit_kernel<<<S, 1024, smem, ctx->stream>>>(s, 0, np2);
+    ctx->launches++;
+    CU(cudaMemcpyAsync(mean, ctx->c_mean.p, (size_t)S * dim * 8, cudaMemcpyDefault, ctx->stream));
+    CU(cudaMemcpyAsync(cov, ctx->c_cov.p, (size_t)S * dim * dim * 8, cudaMemcpyDefault, ctx->stream));
+    if (!is_device_ptr(mean) || !is_device_ptr(cov)) ctx->host_out = true;
+    return finish_call(ctx, false, 0);
+}
+
+int bd_cem_cycle(bd_ctx* ctx, int S, const bd_cem_config* cfg, const double* init_mean, const double* init_cov,
+                 const double* z, const double* warm, int64_t* best_index, double* best_params, double* best_xi,
+                 double* best_cost, double* best_residual, double* best_aug, double* stats, double* final_mean,
+                 double* final_cov, int* iterations_done) {
+    if (!ctx || !cfg) return BD_ERR_VALUE;
+    int rc = require_solver(ctx, true);
+    if (rc) return rc;
+    const int B = cfg->batch, dim = ctx->dim, N = cfg->iterations;
+    if (S != ctx->S || B < 1 || N < 1 || cfg->am_iters < 1 || !(cfg->tol > 0) || !init_mean || !init_cov)
+        return fail(ctx, BD_ERR_VALUE, "bad CEM configuration");
+    if (!(cfg->n_elite <= cfg->n_cons && cfg->n_cons <= B) || cfg->n_elite < 1 || cfg->n_cons > 1024)
+        return fail(ctx, BD_ERR_VALUE, "need elites <= constraint_elites <= batch_size (<= 1024 constraint elites)");
+    if (!(cfg->eta > 0 && cfg->eta <= 1) || !(cfg->gamma > 0)) return fail(ctx, BD_ERR_VALUE, "bad eta / gamma");
+    if (B > 8192) return fail(ctx, BD_ERR_VALUE, "CEM batch above 8192 per scene is not supported by this build");
+    begin_call(ctx);
+    const size_t tot = (size_t)S * B;
+    const double *dz = nullptr, *dwarm = nullptr, *dm0, *dc0;
+    if ((rc = stage_in(ctx, init_mean, (size_t)S * dim, &dm0))) return rc;
+    if ((rc = stage_in(ctx, init_cov, (size_t)S * dim * dim, &dc0))) return rc;
+    if ((rc = stage_in(ctx, z, z ? (size_t)N * tot * dim : 0, &dz))) return rc;
+    if ((rc = stage_in(ctx, warm, warm ? tot * dim : 0, &dwarm))) return rc;
+    CU(ctx->c_mean.ensure((size_t)S * dim * 8));
+    CU(ctx->c_cov.ensure((size_t)S * dim * dim * 8));
+    CU(ctx->c_L.ensure((size_t)S * dim * dim * 8));
+    CU(ctx->c_done.ensure((size_t)S * 4));
+    CU(ctx->c_best_idx.ensure((size_t)S * 8));
+    CU(ctx->c_best_p.ensure((size_t)S * dim * 8));
+    CU(ctx->c_best_xi.ensure((size_t)S * NX * 8));
+    CU(ctx->c_best_s.ensure((size_t)S * 3 * 8));
+    CU(ctx->c_stats.ensure((size_t)S * N * 6 * 8));
+    CU(ctx->w_params.ensure(tot * dim * 8));
+    CU(ctx->w_xibar.ensure(tot * NX * 8));
+    CU(ctx->w_xi.ensure(tot * NX * 8));
+    CU(ctx->w_res.ensure(tot * 8));
+    CU(ctx->w_cost.ensure(tot * 8));
+    CU(ctx->w_iters.ensure((size_t)S * 4));
+    CU(ctx->w_conf.ensure((size_t)S * 8));
+    double* db = nullptr;
+    if (ctx->with_goal) {
+        CU(ctx->w_b.ensure(tot * ctx->neq * 8));
+        db = ctx->w_b.as<double>();
+    }
+    CemState s{};
+    s.S = S; s.B = B; s.dim = dim; s.n_cons = cfg->n_cons; s.n_elite = cfg->n_elite; s.iters = N;
+    s.eta = cfg->eta; s.gamma = cfg->gamma; s.w_res = cfg->residual_weight;
+    s.mean = ctx->c_mean.as<double>(); s.cov = ctx->c_cov.as<double>(); s.L = ctx->c_L.as<double>();
+    s.err = ctx->w_err.as<int>(); s.done = ctx->c_done.as<int>();
+    s.resid = ctx->w_res.as<double>(); s.cost = ctx->w_cost.as<double>(); s.params = ctx->w_params.as<double>();
+    s.xi = ctx->w_xi.as<double>(); s.stats = ctx->c_stats.as<double>();
+    s.best_index = ctx->c_best_idx.as<long long>(); s.best_params = ctx->c_best_p.as<double>();
+    s.best_xi = ctx->c_best_xi.as<double>(); s.best_scal = ctx->c_best_s.as<double>();
+    cem_init_kernel<<<S, 64, 0, ctx->stream>>>(s, dm0, dc0);
+    ctx->launches++;
+    int np2 = 1;
+    while (np2 < B) np2 <<= 1;
+    const size_t rsmem = (size_t)np2 * 12;
+    raise_smem(rank_refit_kernel, rsmem);
+    for (int it = 0; it < N; ++it) {
+        const double* zi = dz ? dz + (size_t)it * tot * dim : nullptr;
+        sample_kernel<<<(unsigned)((tot + 127) / 128), 128, 0, ctx->stream>>>(s, it, zi, it == 0 ? dwarm : nullptr,
+                                                                             cfg->seed, ctx->w_params.as<double>());
+        ctx->launches++;
+        if ((rc = run_stage1(ctx, B, ctx->w_params.as<double>(), ctx->w_xibar.as<double>(), nullptr, db))) return rc;
+        if ((rc = run_projection(ctx, B, ctx->w_xibar.as<double>(), db, cfg->am_iters, cfg->tol,
+                                 ctx->w_xi.as<double>(), ctx->w_res.as<double>(), ctx->w_cost.as<double>(), nullptr,
+                                 ctx->w_iters.as<int>(), ctx->w_conf.as<unsigned long long>())))
+            return rc;
+        rank_refit_kernel<<<S, 1024, rsmem, ctx->stream>>>(s, it, np2);
+        ctx->launches++;
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(ctx, BD_ERR_CUDA, "CEM launch: %s", cudaGetErrorString(e));
+    // outputs
+    struct Out { void* dst; const void* src; size_t bytes; };
+    const Out outs[] = {
+        {best_index, ctx->c_best_idx.p, (size_t)S * 8},
+        {best_params, ctx->c_best_p.p, (size_t)S * dim * 8},
+        {best_xi, ctx->c_best_xi.p, (size_t)S * NX * 8},
+        {stats, ctx->c_stats.p, (size_t)S * N * 6 * 8},
+        {final_mean, ctx->c_mean.p, (size_t)S * dim * 8},
+        {final_cov, ctx->c_cov.p, (size_t)S * dim * dim * 8},
+        {iterations_done, ctx->c_done.p, (size_t)S * 4},
+    };
+    bool any_host = false;
+    for (const Out& o : outs)
+        if (o.dst) {
+            CU(cudaMemcpyAsync(o.dst, o.src, o.bytes, cudaMemcpyDefault, ctx->stream));
+            any_host |= !is_device_ptr(o.dst);
+        }
+    double* scal[3] = {best_cost, best_residual, best_aug};
+    for (int q = 0; q < 3; ++q)
+        if (scal[q]) {
+            CU(cudaMemcpy2DAsync(scal[q], 8, ctx->c_best_s.as<double>() + q, 24, 8, S, cudaMemcpyDefault, ctx->stream));
+            any_host |= !is_device_ptr(scal[q]);
+        }
+    if (any_host) CU(cudaStreamSynchronize(ctx->stream));
+    return 0;
+}
+
+// ------------------------------------------------------------------ CVAE decoder
+int bd_cvae_set_weights(bd_ctx* ctx, int n_layers, const int* dims, const float* const* W, const float* const* b) {
+    if (!ctx || n_layers < 1 || n_layers > 16 || !dims || !W || !b) return BD_ERR_VALUE;
+    begin_call(ctx);
+    for (auto* p : ctx->cvae_w) delete p;
+    for (auto* p : ctx->cvae_b) delete p;
+    ctx->cvae_w.clear();
+    ctx->cvae_b.clear();
+    ctx->cvae_dims.assign(dims, dims + n_layers + 1);
+    for (int l = 0; l < n_layers; ++l) {
+        const size_t nw = (size_t)dims[l] * dims[l + 1], nb = dims[l + 1];
+        if (dims[l] < 1 || dims[l + 1] < 1) return fail(ctx, BD_ERR_VALUE, "bad layer dims");
+        auto* wb = new DevBuf();
+        auto* bb = new DevBuf();
+        ctx->cvae_w.push_back(wb);
+        ctx->cvae_b.push_back(bb);
+        CU(wb->ensure(nw * 4));
+        CU(bb->ensure(nb * 4));
+        CU(cudaMemcpy(wb->p, W[l], nw * 4, cudaMemcpyDefault));
+        CU(cudaMemcpy(bb->p, b[l], nb * 4, cudaMemcpyDefault));
+    }
+    return 0;
+}
+
+int bd_cvae_decode(bd_ctx* ctx, int count, const float* obs, const float* z, double* params) {
+    if (!ctx || count < 1 || !obs || !z || !params) return BD_ERR_VALUE;
+    if (ctx->cvae_w.empty()) return fail(ctx, BD_ERR_STATE, "CVAE weights not set");
+    begin_call(ctx);
+    int rc;
+    const auto& d = ctx->cvae_dims;
+    const int L = (int)ctx->cvae_w.size();
+    const int zdim = d[0] - CVAE_OBS;
+    if (zdim < 1) return fail(ctx, BD_ERR_VALUE, "first layer must take 55 observation + latent inputs");
+    const float *dobs, *dz;
+    if ((rc = stage_in(ctx, obs, (size_t)CVAE_OBS, &dobs))) return rc;
+    if ((rc = stage_in(ctx, z, (size_t)count * zdim, &dz))) return rc;
+    int widest = 0;
+    for (int l = 1; l <= L; ++l) widest = widest > d[l] ? widest : d[l];
+    CU(ctx->cvae_h0.ensure((size_t)count * widest * 4));
+    CU(ctx->cvae_h1.ensure((size_t)count * widest * 4));
+    double* dout;
+    DevBuf& ws = ctx->stage[7];
+    if ((rc = stage_out(ctx, params, (size_t)count * d[L], ws, &dout))) return rc;
+    // layer 0: scene part W[:, :55] obs is shared by every sample
+    cvae_first_layer<<<dim3((d[1] + 127) / 128, (count + 31) / 32), dim3(128), 0, ctx->stream>>>(
+        count, d[1], zdim, ctx->cvae_w[0]->as<float>(), ctx->cvae_b[0]->as<float>(), dobs, dz,
+        ctx->cvae_h0.as<float>());
+    ctx->launches++;
+    float* cur = ctx->cvae_h0.as<float>();
+    float* nxt = ctx->cvae_h1.as<float>();
+    for (int l = 1; l < L; ++l) {
+        const bool last = (l == L - 1);
+        dim3 grid((d[l + 1] + CVAE_BN - 1) / CVAE_BN, (count + CVAE_BM - 1) / CVAE_BM);
+        cvae_linear<<<grid, CVAE_THREADS, 0, ctx->stream>>>(count, d[l], d[l + 1], cur, ctx->cvae_w[l]->as<float>(),
+                                                            ctx->cvae_b[l]->as<float>(), nxt, last ? 0 : 1);
+        ctx->launches++;
+        float* t = cur;
+        cur = nxt;
+        nxt = t;
+    }
+    cvae_to_double<<<(unsigned)(((size_t)count * d[L] + 255) / 256), 256, 0, ctx->stream>>>(cur, dout,
+                                                                                           (size_t)count * d[L]);
+    ctx->launches++;
+    return finish_call(ctx, false, 0);
+}
+
+}  // extern "C"

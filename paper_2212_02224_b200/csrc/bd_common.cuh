@@ -1,0 +1,34 @@
+// Shared definitions for the sm_100a kernels of the bi-level planner hot path.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace bd {
+
+constexpr int NC = 11;             // coefficients per axis: Bernstein order 10 (pkg/basis.py:156-179)
+constexpr int NX = 2 * NC;         // stacked xi = (c_x, c_y)
+constexpr int WROW = 36;           // one timestep of [W | Wd | Wdd] in fp32, padded to 9 x float4
+constexpr int KROW = 12;           // fp64 row stride of the per-axis aug-KKT inverse blocks (6 x double2)
+constexpr int MAX_NEQ = 9;         // 6 initial-state rows (+3 goal rows), pkg/batch_qp.py:181-193
+constexpr int MAX_DIM = 16;        // behaviour vector length (2*m_seg [+2])
+constexpr int ITMAX_SLOTS = 32;    // spread slots for the per-iteration batch max (early exit)
+
+// Error bits of the device error word.
+constexpr int ERR_NONFINITE = 1;   // NumericalFailure: non-finite iterate (pkg/projection.py:290-291)
+constexpr int ERR_KKT_RESID = 2;   // NumericalFailure: stage-1 KKT residual (pkg/batch_qp.py:272-279)
+
+// Per-scene scalars in the form the AM kernel consumes (ConstraintSpec, pkg/constraints.py:31-42).
+struct SceneLim {
+    float a, b, inv_a, inv_b;
+    float v_min, v_max, a_max, k_max, inv_k_max, c_max, y_lb, y_ub;
+};
+
+__device__ __forceinline__ unsigned float_key(float r) {
+    // residuals are >= 0 (sums of max(0, .)), so their IEEE bits order like the values; NaN sorts last.
+    return __float_as_uint(r);
+}
+
+__host__ __device__ __forceinline__ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace bd

@@ -1,0 +1,292 @@
+// K3 select + refit and K4 sampler of the CEM upper level (sm_100a).
+//
+// rank_samples (pkg/bilevel.py:129-137), _elite_weights / update_distribution
+// (:163-194), IterationStats (:100-108, :282-292), the best EliteRecord
+// (:272-280) and SamplingDistribution.sample (:51-57).
+#pragma once
+
+#include "bd_common.cuh"
+
+namespace bd {
+
+// Order-preserving map of a double onto uint64 (numpy: -0 == +0, NaN last).
+__device__ __forceinline__ unsigned long long ordered_bits(double x) {
+    if (x == 0.0) x = 0.0;
+    const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// In-place ascending bitonic sort of (key, idx) pairs in shared memory, ties by idx
+// (== np.argsort(kind="stable") / np.lexsort((idx, key)) on distinct indices).
+__device__ void block_bitonic_sort(unsigned long long* key, int* idx, int n_pow2) {
+    for (int k = 2; k <= n_pow2; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < n_pow2; i += blockDim.x) {
+                const int l = i ^ j;
+                if (l > i) {
+                    const unsigned long long ki = key[i], kl = key[l];
+                    const int ii = idx[i], il = idx[l];
+                    const bool gt = (ki > kl) || (ki == kl && ii > il);
+                    if (gt == ((i & k) == 0)) { key[i] = kl; key[l] = ki; idx[i] = il; idx[l] = ii; }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// Cholesky of a dim x dim SPD matrix (row-major, fp64) by one thread; false if not PD.
+__device__ bool chol_small(const double* A, double* L, int d) {
+    for (int i = 0; i < d * d; ++i) L[i] = 0.0;
+    for (int j = 0; j < d; ++j) {
+        double s = A[j * d + j];
+        for (int k = 0; k < j; ++k) s -= L[j * d + k] * L[j * d + k];
+        if (!(s > 0.0)) return false;
+        const double ljj = sqrt(s);
+        L[j * d + j] = ljj;
+        for (int i = j + 1; i < d; ++i) {
+            double t = A[i * d + j];
+            for (int k = 0; k < j; ++k) t -= L[i * d + k] * L[j * d + k];
+            L[i * d + j] = t / ljj;
+        }
+    }
+    return true;
+}
+
+// SamplingDistribution.sample's factor: chol(cov), falling back to chol(cov + 1e-5 I) (pkg/bilevel.py:52-55).
+__device__ void sampling_factor(const double* cov, double* L, int d) {
+    if (chol_small(cov, L, d)) return;
+    double tmp[MAX_DIM * MAX_DIM];
+    for (int i = 0; i < d * d; ++i) tmp[i] = cov[i];
+    for (int i = 0; i < d; ++i) tmp[i * d + i] += 1e-5;
+    if (!chol_small(tmp, L, d))
+        for (int i = 0; i < d * d; ++i) L[i] = __longlong_as_double(0x7ff8000000000000ll);  // NaN: numpy would raise
+}
+
+// ---------------------------------------------------------------- Philox4x32-10 normals
+__device__ __forceinline__ void philox_round(uint32_t (&c)[4], uint32_t (&k)[2]) {
+    const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+    const uint32_t hi0 = __umulhi(M0, c[0]), lo0 = M0 * c[0];
+    const uint32_t hi1 = __umulhi(M1, c[2]), lo1 = M1 * c[2];
+    const uint32_t n0 = hi1 ^ c[1] ^ k[0], n2 = hi0 ^ c[3] ^ k[1];
+    c[0] = n0; c[1] = lo1; c[2] = n2; c[3] = lo0;
+    k[0] += 0x9E3779B9u; k[1] += 0xBB67AE85u;
+}
+
+__device__ __forceinline__ void philox4(uint32_t (&c)[4], uint64_t seed) {
+    uint32_t k[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+#pragma unroll
+    for (int r = 0; r < 10; ++r) philox_round(c, k);
+}
+
+// Standard normals keyed by (seed, scene, CEM iteration, sample index): identical for any GPU count.
+__device__ void philox_normals(uint64_t seed, uint32_t scene, uint32_t it, uint32_t sample, double* z, int d) {
+    for (int base = 0; base < d; base += 4) {
+        uint32_t c[4] = {sample, it, scene, (uint32_t)(base / 4)};
+        philox4(c, seed);
+        for (int q = 0; q < 4 && base + q < d; q += 2) {
+            const double u1 = ((double)c[q] + 0.5) * 2.3283064365386963e-10;     // (0, 1)
+            const double u2 = ((double)c[q + 1] + 0.5) * 2.3283064365386963e-10;
+            const double r = sqrt(-2.0 * log(u1));
+            double s, co;
+            sincospi(2.0 * u2, &s, &co);
+            z[base + q] = r * co;
+            if (base + q + 1 < d) z[base + q + 1] = r * s;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- CEM state
+struct CemState {
+    int S, B, dim, n_cons, n_elite, iters;
+    double eta, gamma, w_res;
+    double* mean;       // S x dim
+    double* cov;        // S x dim x dim
+    double* L;          // S x dim x dim   sampling factor of cov
+    int* err;           // S   sticky error bits (stage-1 / AM)
+    int* done;          // S   completed CEM iterations (-1 = failed in iteration 1)
+    // per-iteration data
+    const double* resid;   // S*B
+    const double* cost;    // S*B
+    const double* params;  // S*B x dim
+    const double* xi;      // S*B x NX
+    // outputs
+    long long* cons_idx;   // S x n_cons   (nullable)
+    long long* elite_idx;  // S x n_elite  (nullable)
+    double* elite_aug;     // S x n_elite  (nullable)
+    double* stats;         // S x iters x 6 (nullable)
+    long long* best_index; // S
+    double* best_params;   // S x dim
+    double* best_xi;       // S x NX
+    double* best_scal;     // S x 3: cost, residual, aug
+};
+
+// Initial factor of the configured Gaussian (pkg/bilevel.py:244).
+__global__ void cem_init_kernel(CemState s, const double* mean0, const double* cov0) {
+    const int scene = blockIdx.x;
+    const int d = s.dim;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) s.mean[scene * d + i] = mean0[scene * d + i];
+    for (int i = threadIdx.x; i < d * d; i += blockDim.x) s.cov[scene * d * d + i] = cov0[scene * d * d + i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        sampling_factor(s.cov + scene * d * d, s.L + scene * d * d, d);
+        s.err[scene] = 0;
+        s.done[scene] = 0;
+    }
+}
+
+// p = mean + z L^T (pkg/bilevel.py:51-57) or the warm-start tile (pkg/behavior.py:113-115).
+__global__ void sample_kernel(CemState s, int it, const double* z, const double* warm, uint64_t seed,
+                              double* params) {
+    const int id = blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= s.S * s.B) return;
+    const int scene = id / s.B, j = id % s.B;
+    const int d = s.dim;
+    if (s.err[scene]) return;
+    double* out = params + (size_t)id * d;
+    if (warm != nullptr) {
+        for (int q = 0; q < d; ++q) out[q] = warm[(size_t)id * d + q];
+        return;
+    }
+    double zz[MAX_DIM];
+    if (z != nullptr) {
+        for (int q = 0; q < d; ++q) zz[q] = z[(size_t)id * d + q];
+    } else {
+        philox_normals(seed, scene, it, j, zz, d);
+    }
+    const double* L = s.L + scene * d * d;
+    const double* mu = s.mean + scene * d;
+    for (int r = 0; r < d; ++r) {
+        double acc = 0.0;
+        for (int q = 0; q < d; ++q) acc = fma(zz[q], L[r * d + q], acc);
+        out[r] = mu[r] + acc;
+    }
+}
+
+// rank_samples + update_distribution + IterationStats + best record for one CEM
+// iteration, one CTA per scene.  Requires B <= 8192 (shared-memory sort).
+__global__ void __launch_bounds__(1024) rank_refit_kernel(CemState s, int it, int npow2) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int scene = blockIdx.x;
+    const int d = s.dim;
+    if (s.err[scene] != 0) {            // this iteration (or an earlier one) failed: freeze
+        if (threadIdx.x == 0 && s.done[scene] == it) s.done[scene] = (it == 0) ? -1 : it;
+        return;
+    }
+    unsigned long long* key = reinterpret_cast<unsigned long long*>(smem);
+    int* idx = reinterpret_cast<int*>(key + npow2);
+    __shared__ unsigned long long key2[1024];
+    __shared__ int idx2[1024];
+    __shared__ double w[1024];
+    __shared__ double red[32];
+    __shared__ double mu_new[MAX_DIM];
+    const size_t base = (size_t)scene * s.B;
+    for (int i = threadIdx.x; i < npow2; i += blockDim.x) {
+        key[i] = i < s.B ? ordered_bits(s.resid[base + i]) : ~0ull;
+        idx[i] = i < s.B ? i : 0x7fffffff;
+    }
+    __syncthreads();
+    block_bitonic_sort(key, idx, npow2);
+    // constraint elites: first n of the stable residual order; aug = cost + w r
+    const int n = s.n_cons, q = s.n_elite;
+    int np2 = 1;
+    while (np2 < n) np2 <<= 1;
+    for (int i = threadIdx.x; i < np2; i += blockDim.x) {
+        if (i < n) {
+            const int j = idx[i];
+            const double aug = s.cost[base + j] + s.w_res * s.resid[base + j];
+            key2[i] = ordered_bits(aug);
+            idx2[i] = j;
+            if (s.cons_idx) s.cons_idx[(size_t)scene * n + i] = j;
+        } else {
+            key2[i] = ~0ull;
+            idx2[i] = 0x7fffffff;
+        }
+    }
+    __syncthreads();
+    block_bitonic_sort(key2, idx2, np2);
+    // elite weights exp(-(aug - min aug)/gamma), uniform fallback (pkg/bilevel.py:163-172)
+    const double amin = s.cost[base + idx2[0]] + s.w_res * s.resid[base + idx2[0]];
+    double part = 0.0;
+    for (int i = threadIdx.x; i < q; i += blockDim.x) {
+        const int j = idx2[i];
+        const double aug = s.cost[base + j] + s.w_res * s.resid[base + j];
+        w[i] = exp(-(aug - amin) / s.gamma);
+        part += w[i];
+        if (s.elite_idx) s.elite_idx[(size_t)scene * q + i] = j;
+        if (s.elite_aug) s.elite_aug[(size_t)scene * q + i] = aug;
+    }
+    for (int o = 16; o >= 1; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
+    __syncthreads();
+    __shared__ double total;
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+        total = t;
+    }
+    __syncthreads();
+    const bool uniform = !(isfinite(total) && total > 0.0);
+    for (int i = threadIdx.x; i < q; i += blockDim.x) w[i] = uniform ? 1.0 / q : w[i] / total;
+    __syncthreads();
+    // weighted mean / covariance refit (pkg/bilevel.py:175-194), fp64, one thread per entry
+    const double eta = s.eta;
+    double* mean = s.mean + scene * d;
+    double* cov = s.cov + scene * d * d;
+    if (threadIdx.x < d) {
+        double acc = 0.0;
+        for (int i = 0; i < q; ++i) acc = fma(w[i], s.params[(base + idx2[i]) * d + threadIdx.x], acc);
+        mu_new[threadIdx.x] = (1.0 - eta) * mean[threadIdx.x] + eta * acc;
+    }
+    __syncthreads();
+    __shared__ double cnew[MAX_DIM * MAX_DIM];
+    if (threadIdx.x < d * d) {
+        const int r = threadIdx.x / d, c = threadIdx.x % d;
+        double acc = 0.0;
+        for (int i = 0; i < q; ++i) {
+            const double* pi = s.params + (base + idx2[i]) * d;
+            acc = fma(w[i] * (pi[r] - mu_new[r]), pi[c] - mu_new[c], acc);
+        }
+        cnew[threadIdx.x] = (1.0 - eta) * cov[threadIdx.x] + eta * acc + (r == c ? 1e-6 : 0.0);
+    }
+    __syncthreads();
+    if (threadIdx.x < d * d) {
+        const int r = threadIdx.x / d, c = threadIdx.x % d;
+        cov[threadIdx.x] = 0.5 * (cnew[r * d + c] + cnew[c * d + r]);
+    }
+    if (threadIdx.x < d) mean[threadIdx.x] = mu_new[threadIdx.x];
+    // elite-mean upper cost
+    double cs = 0.0;
+    for (int i = threadIdx.x; i < q; i += blockDim.x) cs += s.cost[base + idx2[i]];
+    for (int o = 16; o >= 1; o >>= 1) cs += __shfl_xor_sync(0xffffffffu, cs, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cs;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+        sampling_factor(cov, s.L + scene * d * d, d);
+        // IterationStats (pkg/bilevel.py:282-292)
+        const int B = s.B;
+        const double rmin = s.resid[base + idx[0]], rmax = s.resid[base + idx[B - 1]];
+        const double rmed = (B & 1) ? s.resid[base + idx[B / 2]]
+                                    : 0.5 * (s.resid[base + idx[B / 2 - 1]] + s.resid[base + idx[B / 2]]);
+        double tr = 0.0;
+        for (int i = 0; i < d; ++i) tr += cov[i * d + i];
+        if (s.stats) {
+            double* st = s.stats + ((size_t)scene * s.iters + it) * 6;
+            st[0] = t / q; st[1] = amin; st[2] = tr; st[3] = rmin; st[4] = rmed; st[5] = rmax;
+        }
+        // best EliteRecord = elite[0] (pkg/bilevel.py:272-280)
+        const int jb = idx2[0];
+        s.best_index[scene] = jb;
+        for (int k = 0; k < d; ++k) s.best_params[scene * d + k] = s.params[(base + jb) * d + k];
+        for (int k = 0; k < NX; ++k) s.best_xi[scene * NX + k] = s.xi[(base + jb) * NX + k];
+        s.best_scal[scene * 3 + 0] = s.cost[base + jb];
+        s.best_scal[scene * 3 + 1] = s.resid[base + jb];
+        s.best_scal[scene * 3 + 2] = amin;
+        s.done[scene] = it + 1;
+    }
+}
+
+}  // namespace bd

@@ -1,0 +1,139 @@
+"""GPU parity of the CUDA path against the reference's golden vectors (and the oracle).
+
+Tolerances (BASELINE.json north_star "1e-4 relative (fp32)"):
+  coefficients  per sample & axis  |dc|_inf / max(|c_ref|_inf, 1) <= 1e-4
+  upper cost                       |dc_u| <= 1e-4 max(|c_u|, 1)
+  residuals                        |dr| <= 1e-3 (1 + r)      (also the elite tie band)
+  stage-1 xi_bar (fp64 on device)  <= 1e-9 relative
+"""
+
+import numpy as np
+import pytest
+
+from tests.golden_io import LOWER_CASES, load, rel_err_per_sample_axis
+
+pytestmark = pytest.mark.gpu
+
+XI_TOL = 1e-4
+COST_TOL = 1e-4
+RES_TOL = 1e-3
+
+
+def _solver(g, lanes=0):
+    import paper_2212_02224_b200 as bd
+    basis = bd.build_basis(10, int(g["m"]), float(g["T"]), "bernstein")
+    k_p, k_v, ws, wo, wv = g["weights"]
+    solver = bd.LowerLevelSolver(basis, bd.TrackingWeights(k_p, k_v, ws, wo, wv),
+                                 bd.ParamLayout(4, bool(g["with_goal"])),
+                                 bd.ProjectionConfig(float(g["rho"]), int(g["max_iters"]), float(g["tol"])),
+                                 g["ox"].shape[0])
+    if lanes:
+        solver.context.set_option("lanes_per_sample", lanes)
+    return solver
+
+
+def _scene(g):
+    import paper_2212_02224_b200 as bd
+    a, b, vmin, vmax, amax, kmax, cmax, ylb, yub = g["limits"]
+    curv = (g["curv_x"], g["curv_k"]) if "curv_x" in g else None
+    spec = bd.ConstraintSpec(g["ox"], g["oy"], a, b, vmax, amax, kmax, cmax, ylb, yub, vmin, curv)
+    return bd.PlanningScene(g["b0"], spec, g["lane_centers"])
+
+
+def _check_lower(g, sol, proj, costs):
+    np.testing.assert_allclose(sol.xi, g["xi_bar"], rtol=1e-9, atol=1e-9)
+    np.testing.assert_allclose(sol.mu, g["mu"], rtol=1e-7, atol=1e-6)
+    assert proj.iterations_used == int(g["iterations_used"])
+    err = rel_err_per_sample_axis(proj.xi, g["xi"])
+    assert err <= XI_TOL, f"xi rel err {err:.3g}"
+    dr = np.abs(proj.residuals - g["residuals"])
+    assert np.all(dr <= RES_TOL * (1.0 + g["residuals"])), f"max |dr| {dr.max():.3g}"
+    dc = np.abs(costs - g["costs"])
+    assert np.all(dc <= COST_TOL * np.maximum(np.abs(g["costs"]), 1.0)), f"max cost err {dc.max():.3g}"
+    h = g["history"]
+    assert proj.residual_history.shape == h.shape
+    assert np.all(np.abs(proj.residual_history - h) <= 2 * RES_TOL * (1.0 + h))
+    conf = int(g["clip_conflicts"])
+    assert abs(proj.clip_conflicts - conf) <= max(2, 1e-3 * conf)
+
+
+@pytest.mark.parametrize("case", LOWER_CASES)
+def test_lower_level_solve_matches_reference(case):
+    g = load("lower_" + case)
+    solver = _solver(g)
+    sol, proj = solver.solve(g["params"], _scene(g))
+    _check_lower(g, sol, proj, solver.last_costs)
+
+
+@pytest.mark.parametrize("lanes", [4, 8, 16, 32])
+@pytest.mark.parametrize("case", ["c1_s0", "canon", "dense50", "curve"])
+def test_every_lane_mapping_matches_reference(case, lanes):
+    g = load("lower_" + case)
+    solver = _solver(g, lanes)
+    sol, proj = solver.solve(g["params"], _scene(g))
+    _check_lower(g, sol, proj, solver.last_costs)
+
+
+def test_projection_operator_on_reference_xi_bar():
+    g = load("lower_c1_s1")
+    solver = _solver(g)
+    B = g["params"].shape[0]
+    b = np.repeat(g["b0"][:, None], B, axis=1)
+    proj = solver.projector.project(g["xi_bar"], b, _scene(g).spec)
+    assert rel_err_per_sample_axis(proj.xi, g["xi"]) <= XI_TOL
+    assert proj.iterations_used == int(g["iterations_used"])
+
+
+def test_velocities_and_residual_evaluator_fp64():
+    from paper_2212_02224_b200.constraints import residuals_from_coeffs
+    g = load("lower_c1_s0")
+    solver = _solver(g)
+    xd, yd = solver.velocities(g["xi"])
+    W = solver.basis.Wdot
+    np.testing.assert_allclose(xd, g["xi"][:11].T @ W.T, rtol=1e-12, atol=1e-10)
+    np.testing.assert_allclose(yd, g["xi"][11:].T @ W.T, rtol=1e-12, atol=1e-10)
+    r = residuals_from_coeffs(solver, _scene(g), g["xi"])
+    np.testing.assert_allclose(r, g["residuals"], rtol=1e-9, atol=1e-9)
+
+
+def test_solve_batch_generic_device():
+    import paper_2212_02224_b200 as bd
+    rng = np.random.default_rng(0)
+    A = rng.standard_normal((3, 10))
+    M = rng.standard_normal((10, 10))
+    st = bd.structure_from_matrices(M @ M.T + np.eye(10), A)
+    rhs = bd.QPRightHandSideBatch(rng.standard_normal((10, 64)), rng.standard_normal((3, 64)))
+    sol = bd.solve_batch(st, rhs)
+    for j in range(64):
+        ref = np.linalg.solve(st.kkt, np.concatenate([-rhs.q_batch[:, j], rhs.b_batch[:, j]]))
+        np.testing.assert_allclose(np.concatenate([sol.xi[:, j], sol.mu[:, j]]), ref, rtol=1e-8, atol=1e-10)
+    # unconstrained Q = I, q = -v -> xi = v
+    st = bd.structure_from_matrices(np.eye(4), np.zeros((0, 4)))
+    v = rng.standard_normal((4, 5))
+    sol = bd.solve_batch(st, bd.QPRightHandSideBatch(-v, np.zeros((0, 5))))
+    np.testing.assert_allclose(sol.xi, v, atol=1e-14)
+
+
+def test_factorization_counter_two_per_solver_zero_per_solve():
+    from paper_2212_02224_b200 import batch_qp
+    g = load("lower_b1")
+    before = batch_qp.FACTORIZATION_COUNT
+    solver = _solver(g)
+    assert batch_qp.FACTORIZATION_COUNT == before + 2
+    solver.solve(g["params"], _scene(g))
+    solver.solve(g["params"], _scene(g))
+    assert batch_qp.FACTORIZATION_COUNT == before + 2
+
+
+def test_errors_follow_reference():
+    import paper_2212_02224_b200 as bd
+    g = load("lower_b1")
+    solver = _solver(g)
+    with pytest.raises(ValueError):
+        solver.solve(np.zeros((3, 7)), _scene(g))
+    sc = _scene(g)
+    bad = bd.ConstraintSpec(sc.spec.obstacles_x[:5], sc.spec.obstacles_y[:5], 7.0, 2.8, 20.0, 6.0, 0.2, 3.0, -2, 14)
+    with pytest.raises(ValueError, match="obstacles"):
+        solver.solve(g["params"], bd.PlanningScene(g["b0"], bad))
+    with pytest.raises(bd.NumericalFailure):
+        solver.solve(np.full((2, 8), 1e300), _scene(g))
