@@ -136,8 +136,12 @@ class Context:
         raise RuntimeError(msg)
 
     def call(self, name: str, *args):
+        """Call bd_<name>(ctx, *args); numpy arrays / torch tensors are passed by pointer and
+        stay referenced for the duration of the call."""
         fn = getattr(self.lib, name)
-        self.check(fn(self.h, *args), name)
+        conv = [ptr(a) if isinstance(a, np.ndarray) or hasattr(a, "data_ptr") else a for a in args]
+        self.check(fn(self.h, *conv), name)
+        del args
 
     def launches(self) -> int:
         return int(self.lib.bd_launch_count(self.h))

@@ -189,8 +189,8 @@ class LowerLevelSolver:
         self.projector = ProjectionOperator(basis, self.qp, num_obstacles, proj_config, device=device)
         self._ctx = self.projector._ctx
         qp = self.qp
-        self._ctx.call("bd_set_stage1", layout.m_seg, int(layout.with_goal), qp.num_eq, ptr(f64(qp.q_map_x)),
-                       ptr(f64(qp.q_map_y)), ptr(f64(qp.kkt)), ptr(f64(qp.kkt_inv)))
+        self._ctx.call("bd_set_stage1", layout.m_seg, int(layout.with_goal), qp.num_eq, f64(qp.q_map_x),
+                       f64(qp.q_map_y), f64(qp.kkt), f64(qp.kkt_inv))
         self.last_costs: np.ndarray | None = None
 
     @property
@@ -279,7 +279,7 @@ def solve_bilevel(scene: PlanningScene, solver: LowerLevelSolver, config: BiLeve
     fm = np.zeros(dim)
     fc = np.zeros((dim, dim))
     done = np.zeros(1, dtype=np.int32)
-    solver.context.call("bd_cem_cycle", 1, ctypes.byref(cfg), ptr(f64(config.init_mean)), ptr(f64(config.init_cov)),
+    solver.context.call("bd_cem_cycle", 1, ctypes.byref(cfg), f64(config.init_mean), f64(config.init_cov),
                         ptr(z), ptr(warm), ptr(bi), ptr(bp), ptr(bx), ptr(bc), ptr(br), ptr(ba), ptr(st), ptr(fm),
                         ptr(fc), ptr(done))
     k = int(done[0])
@@ -331,7 +331,7 @@ def _solve_bilevel_stepped(scene, solver, config, rng, warm_start, trace_hook) -
         eaug = np.empty(q)
         st = np.empty(6)
         mean, cov = mean.copy(), cov.copy()
-        ctx.call("bd_rank_refit", 1, B, dim, ptr(f64(proj.residuals)), ptr(f64(costs)), ptr(params), n, q,
+        ctx.call("bd_rank_refit", 1, B, dim, f64(proj.residuals), f64(costs), ptr(params), n, q,
                  float(config.residual_weight), float(config.eta), float(config.gamma), ptr(mean), ptr(cov),
                  ptr(cons), ptr(elite), ptr(eaug), ptr(st))
         trace_hook(it, params, proj, costs, elite)

@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(256) am_kernel(const AmArgs a) {
     const unsigned anybad = __ballot_sync(0xffffffffu, bad);
     if (lane == 0) {
         if (conf) atomicAdd(a.conflicts + scene, (unsigned long long)conf);
-        if (anybad) atomicOr(a.err, ERR_NONFINITE);
+        if (anybad) atomicOr(a.err + scene, ERR_NONFINITE);
     }
 }
 

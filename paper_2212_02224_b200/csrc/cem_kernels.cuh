@@ -11,7 +11,8 @@ namespace bd {
 
 // Order-preserving map of a double onto uint64 (numpy: -0 == +0, NaN last).
 __device__ __forceinline__ unsigned long long ordered_bits(double x) {
-    if (x == 0.0) x = 0.0;
+    if (x != x) return 0xFFFFFFFFFFFFFFFEull;          // every NaN sorts after all numbers, before padding
+    if (x == 0.0) return 0x8000000000000000ull;       // -0 == +0
     const unsigned long long b = (unsigned long long)__double_as_longlong(x);
     return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }

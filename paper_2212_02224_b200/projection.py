@@ -142,9 +142,9 @@ class ProjectionOperator:
         Q[n:, n:] = Qx + config.rho * 2.0 * WtW
         self.aug = structure_from_matrices(Q, qp.A_eq)
         self._ctx = context if context is not None else Context(device)
-        self._ctx.call("bd_set_basis", basis.num_samples, n, ptr(f64(W)), ptr(f64(Wd)), ptr(f64(Wdd)))
-        self._ctx.call("bd_set_projection", num_obstacles, float(config.rho), qp.num_eq, ptr(f64(self.aug.kkt_inv)),
-                       ptr(f64(qp.A_eq)))
+        self._ctx.call("bd_set_basis", basis.num_samples, n, f64(W), f64(Wd), f64(Wdd))
+        self._ctx.call("bd_set_projection", num_obstacles, float(config.rho), qp.num_eq, f64(self.aug.kkt_inv),
+                       f64(qp.A_eq))
         self._scene_key = None
 
     # ------------------------------------------------------------------ scenes
