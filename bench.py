@@ -1,0 +1,323 @@
+"""Benchmark: optimal trajectories/s (100 AM iterations) and the CEM plan-cycle latency.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--scenes-per-gpu S]
+
+Workload (BASELINE.json configs[1] run as a fleet, config 5 style): every step is one full
+CEM planning cycle -- B=1000 set-point samples, 10 obstacles, 4 CEM iterations, top-150
+constraint elites / top-100 elites, 100 AM iterations, m=100 timesteps over 5 s, order-10
+Bernstein basis -- for each of S synthetic highway scenes per GPU (independent scenes are
+sharded over ranks, no collective on the data path: weak scaling).  value = S*N * 4 * 1000
+trajectories / max-over-ranks device time.  The single-scene config-2 cycle latency
+(p50/p99, host call -> host-visible best xi) is measured through the public solve_bilevel.
+
+--impl reference times the reference algorithm on the host cores (the float64 numpy oracle
+restatement in oracle/, one process per core): each step every core runs one CEM iteration
+of the same workload on a bounded sample of B=100 samples of its own scene.
+"""
+
+from __future__ import annotations
+
+import os
+
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+os.environ.setdefault("OMP_NUM_THREADS", "1")
+
+import argparse  # noqa: E402
+import json  # noqa: E402
+import subprocess  # noqa: E402
+import sys  # noqa: E402
+import time  # noqa: E402
+
+import numpy as np  # noqa: E402
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "optimal trajectories/sec (100 iters)"
+B_CEM, N_CEM, N_CONS, N_ELITE, AM_ITERS, N_OBS, M, T = 1000, 4, 150, 100, 100, 10, 100, 5.0
+F_IT = 24 * M * 11 + 15 * M * N_OBS + 60 * M + 8 * 11 * 11 + 10 * 11   # algorithmic flop / sample / AM iteration
+REF_B = 100
+
+
+# ----------------------------------------------------------------------------- reference arm (host)
+def _ref_worker(args):
+    """One CEM iteration (sample -> stage-1 -> 100-iteration AM -> rank -> refit) of the
+    oracle restatement on B samples of scene `seed` (pkg/bilevel.py:249-292)."""
+    seed, B = args
+    import oracle as O
+    from paper_2212_02224_b200.scenes import highway_scene
+    sc = highway_scene(seed)
+    sp = sc.spec
+    _, W, Wd, Wdd = O.basis_matrices(10, M, T)
+    qp = O.tracking_qp(W, Wd, Wdd, 4)
+    aug = O.aug_qp(W, Wd, Wdd, qp.A_eq, N_OBS, 1.0)
+    lim = O.Limits(sp.obstacles_x, sp.obstacles_y, sp.ellipse_a, sp.ellipse_b, sp.v_max, sp.a_max, sp.kappa_max,
+                   sp.c_max, sp.y_lb, sp.y_ub, sp.v_min)
+    x0 = sc.initial_state
+    mean = np.concatenate([np.full(4, x0[1]), np.full(4, np.hypot(x0[2], x0[3]))])
+    cov = np.diag(np.concatenate([np.full(4, 1.5 ** 2), np.full(4, 3.0 ** 2)]))
+    t0 = time.perf_counter()
+    O.cem_cycle(qp, aug, W, Wd, Wdd, x0, lim, mean, cov, batch=B, n_cons=min(N_CONS, B), n_elite=min(N_ELITE, B),
+                iters=1, eta=0.7, gamma=0.9, w_res=1.0, rng=np.random.default_rng(seed), am_iters=AM_ITERS)
+    return time.perf_counter() - t0
+
+
+def cpu_reference(steps: int, warmup: int, cores: int | None = None):
+    import multiprocessing as mp
+    cores = cores or os.cpu_count() or 1
+    ctx = mp.get_context("fork")
+    times = []
+    with ctx.Pool(cores) as pool:
+        for s in range(warmup + steps):
+            t0 = time.perf_counter()
+            pool.map(_ref_worker, [(1000 * s + c, REF_B) for c in range(cores)])
+            if s >= warmup:
+                times.append(time.perf_counter() - t0)
+    t = float(np.mean(times))
+    return {"value": cores * REF_B / t, "unit": "trajectories/s", "cores": cores, "kind": "port",
+            "sample": f"per step: {cores} processes x one CEM iteration (B={REF_B}, 10 obstacles, 100 AM iterations, "
+                      f"rank+refit) of the float64 oracle restatement; {steps} steps, {t:.2f} s/step"}, t
+
+
+def run_reference(args, rank: int):
+    if rank != 0:
+        return
+    ref, t = cpu_reference(args.steps, args.warmup)
+    line = {"metric": METRIC, "value": ref["value"], "unit": ref["unit"], "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"CEM iteration on host cores, B={REF_B} samples per core, 10 obstacles, "
+                                   "100 AM iterations, m=100, order-10 Bernstein"},
+            "impl": "reference", "cpu_baseline": ref,
+            "e2e": {"value": ref["value"], "unit": ref["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- B200 arm
+class ClockSampler:
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=clocks.sm,clocks.max.sm,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=10)
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except (ValueError, IndexError):
+                continue
+            for nm, flag in zip(names, parts[3:7]):
+                if flag.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def make_planner(device: int):
+    import paper_2212_02224_b200 as bd
+    from paper_2212_02224_b200.fleet import FleetPlanner
+    basis = bd.build_basis(10, M, T, "bernstein")
+    cfg = bd.BiLevelConfig(B_CEM, N_CONS, N_ELITE, N_CEM, 0.7, 0.9, 1.0)
+    return FleetPlanner(basis, bd.TrackingWeights(), bd.ParamLayout(4), bd.ProjectionConfig(1.0, AM_ITERS, 1e-3),
+                        N_OBS, cfg, device=device)
+
+
+def cem_latency(device: int, cycles: int = 30):
+    """Single-scene config-2 cycle through the public drop-in solve_bilevel (host numpy in/out)."""
+    import paper_2212_02224_b200 as bd
+    from paper_2212_02224_b200.fleet import initial_distribution
+    from paper_2212_02224_b200.scenes import highway_scene
+    basis = bd.build_basis(10, M, T, "bernstein")
+    solver = bd.LowerLevelSolver(basis, bd.TrackingWeights(), bd.ParamLayout(4),
+                                 bd.ProjectionConfig(1.0, AM_ITERS, 1e-3), N_OBS, device=device)
+    scene = highway_scene(0)
+    mean, cov = initial_distribution(scene)
+    cfg = bd.BiLevelConfig(B_CEM, N_CONS, N_ELITE, N_CEM, 0.7, 0.9, 1.0, mean, cov)
+    for s in range(3):
+        bd.solve_bilevel(scene, solver, cfg, np.random.default_rng(s))
+    ts = []
+    for s in range(cycles):
+        rng = np.random.default_rng(100 + s)
+        t0 = time.perf_counter()
+        res = bd.solve_bilevel(scene, solver, cfg, rng)
+        ts.append(1e3 * (time.perf_counter() - t0))
+        assert np.isfinite(res.best.upper_cost)
+    return {"p50_ms": float(np.percentile(ts, 50)), "p99_ms": float(np.percentile(ts, 99)), "cycles": cycles,
+            "config": "B=1000, 10 obstacles, 4 CEM iterations, n=150, q=100, 100 AM iterations; host call to "
+                      "host-visible best xi via solve_bilevel (numpy Generator draws, H2D+D2H included)"}
+
+
+def run_b200(args, rank: int, world: int, dist):
+    import torch
+
+    from paper_2212_02224_b200.fleet import initial_distribution
+    from paper_2212_02224_b200.scenes import highway_scene
+
+    dev = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(dev)
+    S = args.scenes_per_gpu
+    planner = make_planner(dev)
+    ctx = planner.context
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    scenes = [highway_scene(rank * S + j) for j in range(S)]
+    planner.set_scenes(scenes)
+    mc = [initial_distribution(sc) for sc in scenes]
+    mean = torch.tensor(np.stack([m for m, _ in mc]), dtype=torch.float64, device=dev)
+    cov = torch.tensor(np.stack([c for _, c in mc]), dtype=torch.float64, device=dev)
+    outs = {"best_index": torch.zeros(S, dtype=torch.int64, device=dev),
+            "best_xi": torch.zeros(S, 22, dtype=torch.float64, device=dev),
+            "best_cost": torch.zeros(S, dtype=torch.float64, device=dev),
+            "iterations_done": torch.zeros(S, dtype=torch.int32, device=dev)}
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
+    fp32_peak = ctx.probe("fp32_tflops")
+
+    for w in range(args.warmup):
+        planner.plan_device(S, 7 + w, mean, cov, outs, scene_offset=rank * S)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    ctx.set_option("timing", 1)
+    ctx.stat("reset")
+    launches0 = ctx.launches()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(dev) as clk:
+        torch.cuda.synchronize()
+        for k in range(args.steps):
+            flush.zero_()                       # L2 flush between timed steps (outside the events)
+            ev[k][0].record(stream)
+            planner.plan_device(S, 1000 + k, mean, cov, outs, scene_offset=rank * S)
+            ev[k][1].record(stream)
+        torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    ctx.set_option("timing", 0)
+    launches = ctx.launches() - launches0
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = float(np.sum(step_ms))
+    am_ms = ctx.stat("am_ms")
+    am_n = ctx.stat("am_launches")
+    am_si = ctx.stat("am_sample_iters")
+    done = outs["iterations_done"].cpu().numpy()
+    assert np.all(done == N_CEM), f"CEM cycles incomplete: {done}"
+    assert torch.isfinite(outs["best_cost"]).all()
+    t_max = total_ms
+    if dist is not None:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_max = float(t.item())
+    traj = S * world * N_CEM * B_CEM * args.steps
+    value = traj / (t_max / 1e3)
+
+    # end to end through the public API: host scenes in, host results out, every step
+    e2e_scenes = [highway_scene(10_000 + rank * S + j) for j in range(S)]
+    planner.plan(e2e_scenes, seed=1)       # warm the host path
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for k in range(max(1, min(args.steps, 5))):
+        planner._scenes_key = None          # force the scene upload (H2D) every step
+        res = planner.plan(e2e_scenes, seed=2 + k, scene_offset=10_000 + rank * S)
+    e2e_steps = max(1, min(args.steps, 5))
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if dist is not None:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    h2d = S * (2 * N_OBS * M * 8 + 9 * 8 + 6 * 8) + S * (8 + 64) * 8
+    d2h = res.best_index.nbytes + res.best_params.nbytes + res.best_xi.nbytes + 3 * S * 8 + res.stats.nbytes + \
+        res.final_mean.nbytes + res.final_cov.nbytes + res.iterations_done.nbytes
+
+    if rank != 0:
+        return
+    am_avg_ms = am_ms / max(am_n, 1.0)
+    flop_per_launch = F_IT * am_si / max(am_n, 1.0)
+    achieved = flop_per_launch / (am_avg_ms * 1e-3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "am_kernel_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            traffic = json.load(fh).get("dram_bytes_per_launch")
+    line = {
+        "metric": METRIC, "value": value, "unit": "trajectories/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32+f64",
+        "data": "synthetic highway scenes (seeded spawn_world+build_scene recipe), device Philox set-point draws",
+        "config": {"workload": f"CEM plan cycles: {S} scenes/GPU x (B=1000 samples, 10 obstacles, 4 CEM iterations, "
+                               "top-150/top-100 elites, 100 AM iterations, m=100 over 5 s, order-10 Bernstein)",
+                   "scenes_per_gpu": S, "batch": B_CEM, "cem_iterations": N_CEM, "am_iterations": AM_ITERS,
+                   "obstacles": N_OBS, "parallelism": f"scenes sharded over {world} GPU(s), no data-path collective",
+                   "l2": "flushed (256 MB write) between timed steps"},
+        "e2e": {"value": S * world * N_CEM * B_CEM / e2e_s, "unit": "trajectories/s",
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "api": "FleetPlanner.plan (host scenes -> bd_set_scenes + bd_cem_cycle -> host results)"},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
+                     "frac": achieved / fp32_peak, "traffic": traffic,
+                     "kernel": "am_kernel (fused AM projection)", "flop_per_launch": flop_per_launch,
+                     "avg_launch_ms": am_avg_ms, "kernel_share_of_step": am_ms / max(total_ms, 1e-9),
+                     "peak_source": "bd_probe fp32_tflops (FFMA probe measured live; MEASURED_PEAKS.json has no "
+                                    "FP32 CUDA-core figure)"},
+        "clocks": clk.summary(),
+    }
+    if world == 1:
+        line["cem_cycle_latency"] = cem_latency(dev)
+        ref, _ = cpu_reference(steps=2, warmup=1)
+        line["cpu_baseline"] = ref
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--scenes-per-gpu", type=int, default=64)
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+        if args.impl == "b200":
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        tdist.init_process_group("nccl" if args.impl == "b200" else "gloo")
+        dist = tdist
+    if args.impl == "reference":
+        run_reference(args, rank)
+    else:
+        from paper_2212_02224_b200.build import LIB, build
+        if rank == 0 and not os.path.exists(LIB):
+            build()
+        if dist is not None:
+            dist.barrier()
+        run_b200(args, rank, world, dist)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -55,6 +55,7 @@ typedef struct bd_cem_config {
     int am_iters;       /* ProjectionConfig.max_iters                          */
     double eta, gamma, residual_weight, tol;
     uint64_t seed;      /* Philox key when z == NULL (device RNG mode)         */
+    int scene_offset;   /* global index of scene 0 (Philox counter; shard-invariant fleets) */
 } bd_cem_config;
 
 /* ------------------------------------------------------------------ lifecycle */
@@ -65,10 +66,17 @@ const char* bd_last_error(const bd_ctx* ctx);
 /* Use an external cudaStream_t (e.g. torch's current stream); NULL restores the library stream. */
 int bd_set_stream(bd_ctx* ctx, void* cuda_stream);
 int bd_synchronize(bd_ctx* ctx);
-/* Tuning knobs: "lanes_per_sample" (0=auto, 4/8/16/32), "samples_per_cta" (0=auto). */
+/* Knobs: "lanes_per_sample" (0=auto, 4/8/16/32), "samples_per_cta" (0=auto), "timing" (0/1). */
 int bd_set_option(bd_ctx* ctx, const char* key, int value);
 /* Kernel launches issued by this context since creation (instrumentation). */
 int64_t bd_launch_count(const bd_ctx* ctx);
+/* Instrumentation (enable with bd_set_option(ctx, "timing", 1)): "am_ms" = summed CUDA-event
+ * time of the AM kernel launches (recorded on the launching stream), "am_launches",
+ * "am_sample_iters" = samples x iterations executed; "reset" clears them. Synchronises. */
+int bd_get_stat(bd_ctx* ctx, const char* key, double* value);
+/* Measurement probes for roofline denominators: "fp32_tflops" = dense FFMA throughput of an
+ * all-SM register-resident kernel (CUDA events, current clocks). */
+int bd_probe(bd_ctx* ctx, const char* what, double* value);
 /* Synchronise and return (in *bits) the OR of the device error words of the last
  * asynchronous call: 1 = non-finite iterate, 2 = stage-1 KKT residual above 1e-8. */
 int bd_error_bits(bd_ctx* ctx, int* bits);

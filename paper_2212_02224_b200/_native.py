@@ -29,6 +29,8 @@ SIGNATURES = {
     "bd_set_option": (c_int, [_P, c_char_p, c_int]),
     "bd_launch_count": (c_int64, [_P]),
     "bd_error_bits": (c_int, [_P, POINTER(c_int)]),
+    "bd_get_stat": (c_int, [_P, c_char_p, POINTER(c_double)]),
+    "bd_probe": (c_int, [_P, c_char_p, POINTER(c_double)]),
     "bd_set_basis": (c_int, [_P, c_int, c_int, _P, _P, _P]),
     "bd_set_stage1": (c_int, [_P, c_int, c_int, c_int, _P, _P, _P, _P]),
     "bd_set_projection": (c_int, [_P, c_int, c_double, c_int, _P, _P]),
@@ -58,7 +60,7 @@ class CemConfig(ctypes.Structure):
     """bd_cem_config: BiLevelConfig (pkg/bilevel.py:72-97) + projection budget."""
     _fields_ = [("batch", c_int), ("n_cons", c_int), ("n_elite", c_int), ("iterations", c_int),
                 ("am_iters", c_int), ("eta", c_double), ("gamma", c_double), ("residual_weight", c_double),
-                ("tol", c_double), ("seed", c_uint64)]
+                ("tol", c_double), ("seed", c_uint64), ("scene_offset", c_int)]
 
 
 _lib = None
@@ -154,6 +156,16 @@ class Context:
 
     def synchronize(self):
         self.call("bd_synchronize")
+
+    def stat(self, key: str) -> float:
+        v = c_double(0.0)
+        self.call("bd_get_stat", key.encode(), ctypes.byref(v))
+        return v.value
+
+    def probe(self, what: str) -> float:
+        v = c_double(0.0)
+        self.call("bd_probe", what.encode(), ctypes.byref(v))
+        return v.value
 
     def error_bits(self) -> int:
         bits = c_int(0)

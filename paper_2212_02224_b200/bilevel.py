@@ -270,7 +270,7 @@ def solve_bilevel(scene: PlanningScene, solver: LowerLevelSolver, config: BiLeve
     if n_draw:
         z[N - n_draw:] = rng.standard_normal((n_draw, B, dim))
     cfg = CemConfig(B, config.constraint_elites, config.elites, N, pcfg.max_iters, config.eta, config.gamma,
-                    config.residual_weight, pcfg.tol, 0)
+                    config.residual_weight, pcfg.tol, 0, 0)
     bi = np.zeros(1, dtype=np.int64)
     bp = np.zeros(dim)
     bx = np.zeros(2 * solver.basis.num_coeffs)

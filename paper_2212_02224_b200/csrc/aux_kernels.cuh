@@ -76,7 +76,9 @@ __global__ void __launch_bounds__(256) stage1_kernel(const S1Args a) {
         res = fmax(res, __shfl_xor_sync(0xffffffffu, res, o));
         scale = fmax(scale, __shfl_xor_sync(0xffffffffu, scale, o));
     }
-    if (lane == 0 && !(res <= 1e-8 * (1.0 + scale))) atomicOr(a.err + (a.rhs_in ? 0 : row / a.B), ERR_KKT_RESID);
+    const bool finite_rhs = __all_sync(0xffffffffu, isfinite(rhs));
+    if (lane == 0 && !finite_rhs) atomicOr(a.err + (a.rhs_in ? 0 : row / a.B), ERR_BAD_RHS);
+    else if (lane == 0 && !(res <= 1e-8 * (1.0 + scale))) atomicOr(a.err + (a.rhs_in ? 0 : row / a.B), ERR_KKT_RESID);
     if (a.rhs_in) {
         if (i < a.nr) a.sol_out[(size_t)row * a.nr + i] = sol;
         return;

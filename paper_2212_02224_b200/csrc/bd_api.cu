@@ -54,6 +54,10 @@ struct bd_ctx {
     std::string err;
     int64_t launches = 0;
     int opt_lanes = 0, opt_spc = 0;
+    // instrumentation
+    bool timing = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_used, ev_free;
+    double am_ms = 0.0, am_launches = 0.0, am_sample_iters = 0.0;
     // basis
     int m = 0;
     DevBuf wrow, W64, Wd64, Wdd64;
@@ -80,12 +84,29 @@ struct bd_ctx {
     std::vector<DevBuf*> cvae_w, cvae_b;
     DevBuf cvae_h0, cvae_h1, cvae_obs, cvae_z;
     ~bd_ctx() {
+        for (auto& e : ev_used) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+        for (auto& e : ev_free) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
         for (auto* b : cvae_w) delete b;
         for (auto* b : cvae_b) delete b;
     }
 };
 
 namespace {
+
+// FP32 issue-rate probe: 8 independent FFMA chains per thread, register resident.
+__global__ void __launch_bounds__(256) ffma_probe_kernel(float* out, int iters, float a, float b) {
+    float v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = threadIdx.x * 1e-3f + k;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = fmaf(v[k], a, b);
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += v[k];
+    if (s == 12345.f) out[0] = s;
+}
 
 int fail(bd_ctx* c, int code, const char* fmt, ...) {
     char buf[512];
@@ -169,6 +190,7 @@ int finish_call(bd_ctx* ctx, bool check_err, int n_err) {
         CU(cudaMemcpy(errs.data(), ctx->w_err.p, n_err * sizeof(int), cudaMemcpyDeviceToHost));
         int bits = 0;
         for (int v : errs) bits |= v;
+        if (bits & ERR_BAD_RHS) return fail(ctx, BD_ERR_VALUE, "right-hand sides must be finite");
         if (bits & ERR_KKT_RESID) return fail(ctx, BD_ERR_NUMERICAL, "KKT residual exceeds tolerance");
         if (bits & ERR_NONFINITE) return fail(ctx, BD_ERR_NUMERICAL, "projection iterate is not finite");
     }
@@ -195,8 +217,26 @@ int launch_am_t(bd_ctx* ctx, AmArgs a, int threads, bool replay_pass) {
     raise_smem(am_kernel<P, CURV>, lay.total);
     dim3 grid((a.B + a.s_cta - 1) / a.s_cta, ctx->S);
     if (!replay_pass) a.replay = nullptr;
+    std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+    const bool timed = ctx->timing && !replay_pass;   // replay guards exit at once unless an early exit fired
+    if (timed) {
+        if (ctx->ev_free.empty()) {
+            cudaEventCreate(&ev.first);
+            cudaEventCreate(&ev.second);
+        } else {
+            ev = ctx->ev_free.back();
+            ctx->ev_free.pop_back();
+        }
+        cudaEventRecord(ev.first, ctx->stream);
+    }
     am_kernel<P, CURV><<<grid, threads, lay.total, ctx->stream>>>(a);
     ctx->launches++;
+    if (timed) {
+        cudaEventRecord(ev.second, ctx->stream);
+        ctx->ev_used.push_back(ev);
+        ctx->am_launches += 1;
+        ctx->am_sample_iters += (double)a.B * ctx->S * a.max_iters;
+    }
     return 0;
 }
 
@@ -330,6 +370,10 @@ int bd_set_option(bd_ctx* ctx, const char* key, int value) {
         ctx->opt_lanes = value;
         return 0;
     }
+    if (!strcmp(key, "timing")) {
+        ctx->timing = value != 0;
+        return 0;
+    }
     if (!strcmp(key, "samples_per_cta")) {
         ctx->opt_spc = value < 0 ? 0 : value;
         return 0;
@@ -338,6 +382,50 @@ int bd_set_option(bd_ctx* ctx, const char* key, int value) {
 }
 
 int64_t bd_launch_count(const bd_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+int bd_get_stat(bd_ctx* ctx, const char* key, double* value) {
+    if (!ctx || !key || !value) return BD_ERR_VALUE;
+    cudaSetDevice(ctx->device);
+    CU(cudaStreamSynchronize(ctx->stream));
+    for (auto& e : ctx->ev_used) {
+        float ms = 0.f;
+        CU(cudaEventElapsedTime(&ms, e.first, e.second));
+        ctx->am_ms += ms;
+        ctx->ev_free.push_back(e);
+    }
+    ctx->ev_used.clear();
+    if (!strcmp(key, "am_ms")) *value = ctx->am_ms;
+    else if (!strcmp(key, "am_launches")) *value = ctx->am_launches;
+    else if (!strcmp(key, "am_sample_iters")) *value = ctx->am_sample_iters;
+    else if (!strcmp(key, "reset")) { ctx->am_ms = ctx->am_launches = ctx->am_sample_iters = 0.0; *value = 0.0; }
+    else return fail(ctx, BD_ERR_VALUE, "unknown stat %s", key);
+    return 0;
+}
+
+int bd_probe(bd_ctx* ctx, const char* what, double* value) {
+    if (!ctx || !what || !value) return BD_ERR_VALUE;
+    if (strcmp(what, "fp32_tflops")) return fail(ctx, BD_ERR_VALUE, "unknown probe %s", what);
+    cudaSetDevice(ctx->device);
+    int sms = 0;
+    CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+    DevBuf out;
+    CU(out.ensure(64));
+    const int blocks = sms * 8, threads = 256, iters = 1 << 16;
+    cudaEvent_t e0, e1;
+    CU(cudaEventCreate(&e0));
+    CU(cudaEventCreate(&e1));
+    ffma_probe_kernel<<<blocks, threads, 0, ctx->stream>>>(out.as<float>(), iters / 16, 0.999f, 1e-3f);  // warm
+    CU(cudaEventRecord(e0, ctx->stream));
+    ffma_probe_kernel<<<blocks, threads, 0, ctx->stream>>>(out.as<float>(), iters, 0.999f, 1e-3f);
+    CU(cudaEventRecord(e1, ctx->stream));
+    CU(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *value = 2.0 * 8.0 * (double)iters * blocks * threads / (ms * 1e-3) / 1e12;
+    return 0;
+}
 
 int bd_error_bits(bd_ctx* ctx, int* bits) {
     if (!ctx || !bits) return BD_ERR_VALUE;
@@ -787,8 +875,8 @@ int bd_cem_cycle(bd_ctx* ctx, int S, const bd_cem_config* cfg, const double* ini
     raise_smem(rank_refit_kernel, rsmem);
     for (int it = 0; it < N; ++it) {
         const double* zi = dz ? dz + (size_t)it * tot * dim : nullptr;
-        sample_kernel<<<(unsigned)((tot + 127) / 128), 128, 0, ctx->stream>>>(s, it, zi, it == 0 ? dwarm : nullptr,
-                                                                             cfg->seed, ctx->w_params.as<double>());
+        sample_kernel<<<(unsigned)((tot + 127) / 128), 128, 0, ctx->stream>>>(
+            s, it, zi, it == 0 ? dwarm : nullptr, cfg->seed, cfg->scene_offset, ctx->w_params.as<double>());
         ctx->launches++;
         if ((rc = run_stage1(ctx, B, ctx->w_params.as<double>(), ctx->w_xibar.as<double>(), nullptr, db))) return rc;
         if ((rc = run_projection(ctx, B, ctx->w_xibar.as<double>(), db, cfg->am_iters, cfg->tol,

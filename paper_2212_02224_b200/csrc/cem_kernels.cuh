@@ -138,7 +138,7 @@ __global__ void cem_init_kernel(CemState s, const double* mean0, const double* c
 
 // p = mean + z L^T (pkg/bilevel.py:51-57) or the warm-start tile (pkg/behavior.py:113-115).
 __global__ void sample_kernel(CemState s, int it, const double* z, const double* warm, uint64_t seed,
-                              double* params) {
+                              int scene_offset, double* params) {
     const int id = blockIdx.x * blockDim.x + threadIdx.x;
     if (id >= s.S * s.B) return;
     const int scene = id / s.B, j = id % s.B;
@@ -153,7 +153,7 @@ __global__ void sample_kernel(CemState s, int it, const double* z, const double*
     if (z != nullptr) {
         for (int q = 0; q < d; ++q) zz[q] = z[(size_t)id * d + q];
     } else {
-        philox_normals(seed, scene, it, j, zz, d);
+        philox_normals(seed, scene + scene_offset, it, j, zz, d);
     }
     const double* L = s.L + scene * d * d;
     const double* mu = s.mean + scene * d;

@@ -135,7 +135,7 @@ def test_device_rng_cycle_is_deterministic_and_contracts():
     g = load("cem_c2")
     solver = _solver_c2(g)
     solver.projector._ensure_scene(_scene(g))
-    cfg = CemConfig(1000, 150, 100, 4, 100, 0.7, 0.9, 1.0, 1e-3, 1234)
+    cfg = CemConfig(1000, 150, 100, 4, 100, 0.7, 0.9, 1.0, 1e-3, 1234, 0)
     outs = []
     for _ in range(2):
         st = np.zeros((4, 6))

@@ -135,5 +135,12 @@ def test_errors_follow_reference():
     bad = bd.ConstraintSpec(sc.spec.obstacles_x[:5], sc.spec.obstacles_y[:5], 7.0, 2.8, 20.0, 6.0, 0.2, 3.0, -2, 14)
     with pytest.raises(ValueError, match="obstacles"):
         solver.solve(g["params"], bd.PlanningScene(g["b0"], bad))
-    with pytest.raises(bd.NumericalFailure):
+    # set-points whose tracking cost overflows: the reference's QPRightHandSideBatch rejects them
+    with pytest.raises(ValueError, match="finite"):
         solver.solve(np.full((2, 8), 1e300), _scene(g))
+    with pytest.raises(ValueError):
+        solver.solve(np.full((2, 8), np.nan), _scene(g))
+    # a non-finite iterate raises NumericalFailure (pkg/projection.py:290-291); the fp32 sweep
+    # overflows for positions beyond ~1e19 m (documented range limit of the fp32 recipe)
+    with pytest.raises(bd.NumericalFailure):
+        solver.solve(np.full((2, 8), 1e25), _scene(g))

@@ -41,7 +41,7 @@ def test_abi_version(lib):
 
 def test_struct_layouts():
     assert ctypes.sizeof(_native.Limits) == 9 * 8
-    assert ctypes.sizeof(_native.CemConfig) == 5 * 4 + 4 + 4 * 8 + 8  # 5 ints, pad, 4 doubles, u64
+    assert ctypes.sizeof(_native.CemConfig) == 5 * 4 + 4 + 4 * 8 + 8 + 8  # 5 ints, pad, 4 doubles, u64, int+pad
 
 
 def test_no_cpu_fallback_without_gpu(lib):
