@@ -180,7 +180,8 @@ def run_b200(args, rank: int, world: int, dist):
     S = args.scenes_per_gpu
     planner = make_planner(dev)
     ctx = planner.context
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream(device=dev)       # a real (non-null) stream shared by the library and the events
+    torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
     scenes = [highway_scene(rank * S + j) for j in range(S)]
     planner.set_scenes(scenes)

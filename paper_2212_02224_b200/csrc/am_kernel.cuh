@@ -112,7 +112,7 @@ template <int P, bool CURV, bool INIT, int NV>
 __device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float2* __restrict__ osm,
                                       const float* __restrict__ csm, const float (&cf)[NX], float (&v)[NV],
                                       float* dap, float* kap, int dstride, int p, int m, int n_obs, int n_curv,
-                                      const SceneLim& L, int& conf) {
+                                      const SceneLim& L, int& conf, bool& ovf) {
 #pragma unroll
     for (int k = 0; k < NV; ++k) v[k] = 0.f;
     int j = 0;
@@ -138,6 +138,8 @@ __device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float
         // velocity / acceleration polar split (pkg/projection.py:119-122) in unit-vector form
         const float dv2 = fmaf(XD, XD, YD * YD);
         const float da2 = fmaf(XDD, XDD, YDD * YDD);
+        // fp32 range guard: |x| beyond 1e18 m (or a non-finite derivative) cannot be swept in fp32
+        ovf |= !(fmaxf(fabsf(X), fabsf(Y)) < 1e18f && dv2 < 3e38f && da2 < 3e38f);
         const float iv = dv2 > 0.f ? rsqrtf(dv2) : 0.f;
         const float ia = da2 > 0.f ? rsqrtf(da2) : 0.f;
         const float dv = dv2 * iv, da = da2 * ia;
@@ -290,9 +292,9 @@ __global__ void __launch_bounds__(256) am_kernel(const AmArgs a) {
     }
 
     int conf = 0;
-    bool bad = false;
+    bool bad = false, ovf = false;
     float v[NV];
-    sweep<P, CURV, true>(wsm, osm, csm, cf, v, dap, kap, threads, p, m, n_obs, a.n_curv, L, conf);
+    sweep<P, CURV, true>(wsm, osm, csm, cf, v, dap, kap, threads, p, m, n_obs, a.n_curv, L, conf, ovf);
     group_reduce_scatter<P>(v, lane);
 
     const int r_lane = NX % P, r_slot = (NX / P) * P;
@@ -343,7 +345,7 @@ __global__ void __launch_bounds__(256) am_kernel(const AmArgs a) {
             cf[2 * q] = f.x; cf[2 * q + 1] = f.y;
         }
         // ---- projections, back-projection, residual at the new iterate
-        sweep<P, CURV, false>(wsm, osm, csm, cf, v, dap, kap, threads, p, m, n_obs, a.n_curv, L, conf);
+        sweep<P, CURV, false>(wsm, osm, csm, cf, v, dap, kap, threads, p, m, n_obs, a.n_curv, L, conf, ovf);
         group_reduce_scatter<P>(v, lane);
         resid = v[r_slot];
         cost = v[c_slot];
@@ -375,13 +377,16 @@ __global__ void __launch_bounds__(256) am_kernel(const AmArgs a) {
     } else {
         conf = 0;
         bad = false;
+        ovf = false;
     }
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) conf += __shfl_xor_sync(0xffffffffu, conf, o);
     const unsigned anybad = __ballot_sync(0xffffffffu, bad);
+    const unsigned anyovf = __ballot_sync(0xffffffffu, ovf);
     if (lane == 0) {
         if (conf) atomicAdd(a.conflicts + scene, (unsigned long long)conf);
         if (anybad) atomicOr(a.err + scene, ERR_NONFINITE);
+        if (anyovf) atomicOr(a.err + scene, ERR_RANGE);
     }
 }
 
