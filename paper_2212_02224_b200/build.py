@@ -19,7 +19,9 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "_lib", "libbilevel_b200.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
+         # fp32 only: approximate division / sqrt (<= 2 ulp) inside the 1e-4 parity budget; fp64 untouched
+         "-prec-div=false", "-prec-sqrt=false", "-ftz=true"]
 
 
 def sources() -> list[str]:

@@ -37,7 +37,7 @@ struct AmArgs {
     const double* kblk;         // 2 x NC x KROW   per-axis aug-KKT inverse blocks
     const double* kb;           // NX x neq        xi-b block of the aug-KKT inverse
     const double* aeq;          // neq x NX
-    const float2* obs;          // S x n_obs x m   (x_o / a, y_o / b)
+    const float2* obs;          // S x m x n_obs   (x_o / a, y_o / b), n_obs padded to even with far rows
     const SceneLim* lim;        // S
     const double* bscene;       // S x neq         shared b per scene (b0, zero goal rows)
     const float* curv;          // S x 2 x n_curv  (xs then ks)
@@ -60,7 +60,7 @@ struct AmSmem {
         const int J = (m + P - 1) / P;
         size_t o = 0;
         w = o;    o = align_up(o + (size_t)m * WROW * 4, 16);
-        obs = o;  o = align_up(o + (size_t)n_obs * m * 8, 16);
+        obs = o;  o = align_up(o + (size_t)n_obs * m * 8, 16);          // n_obs already padded to even
         k = o;    o = align_up(o + (size_t)2 * NC * KROW * 8, 16);
         kb = o;   o = align_up(o + (size_t)NX * neq * 8, 16);
         a = o;    o = align_up(o + (size_t)neq * NX * 8, 16);
@@ -70,8 +70,9 @@ struct AmSmem {
         kap = o;  o = align_up(o + (curv_on ? (size_t)J * threads * 4 : 0), 16);
         total = o;
     }
-    // per-sample scratch: u (24 doubles) | c32 (24 floats) | pad -> 76 words: conflict-free LDS.128 across samples
-    static constexpr int SCR_BYTES = 304;
+    // per-sample scratch: u (24 doubles) | c32 (24 floats) | lambda-state l (24 doubles) | first-step
+    // correction (24 doubles) | pad -> 196 words (== 4 mod 32 banks: conflict-free LDS.128 across samples)
+    static constexpr int SCR_BYTES = 784;
 };
 
 __device__ __forceinline__ float interp_table(float x, const float* xs, const float* ks, int n) {
@@ -161,7 +162,7 @@ __device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float
         const float vlo = fmaxf(L.v_min, sqrtf(da_prev * gap * L.inv_k_max));
         conf += (vlo > vhi) ? 1 : 0;
         const float dvc = fminf(fmaxf(dv, fminf(vlo, vhi)), vhi);
-        const float ahi = fminf(L.a_max, dvc * dvc * L.k_max / fmaxf(gap, 1e-8f));
+        const float ahi = fminf(L.a_max, __fdividef(dvc * dvc * L.k_max, fmaxf(gap, 1e-8f)));
         const float dac = fminf(fmaxf(da, 0.f), ahi);
         dap[di] = dac;
         // residuals F c - h of the velocity / acceleration blocks (pkg/projection.py:312-315)
@@ -170,30 +171,49 @@ __device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float
         else { rvx = -dvc; rvy = 0.f; }
         if (da2 > 0.f) { const float f = (da - dac) * ia; rax = XDD * f; ray = YDD * f; }
         else { rax = -dac; ray = 0.f; }
-        // obstacle block (pkg/projection.py:316-322) + clearance violation (pkg/constraints.py:116-120)
+        // obstacle block (pkg/projection.py:316-322) + clearance violation (pkg/constraints.py:116-120).
+        // Common path: branch-free min of the normalised squared distances over the tile row of
+        // this timestep (obstacles [t][o], two per LDS.128); only a lane inside some ellipse
+        // (q < 1) takes the exact per-obstacle path.
         const float xs = X * L.inv_a, ys = Y * L.inv_b;
         float rox = 0.f, roy = 0.f, coll = 0.f;
-        const float2* op = osm + t;
-        for (int o = 0; o < n_obs; ++o) {
-            const float2 ob = op[o * m];
-            const float wc = xs - ob.x, ws = ys - ob.y;
-            const float q = fmaf(wc, wc, ws * ws);
-            if (q < 1.f) {
-                coll += 1.f - q;
-                if (q > 0.f) {
-                    const float f = 1.f - rsqrtf(q);
-                    rox = fmaf(wc, f, rox);
-                    roy = fmaf(ws, f, roy);
-                } else {
-                    rox -= 1.f;
+        const float4* op = reinterpret_cast<const float4*>(osm + t * n_obs);   // n_obs padded to even
+        float qmin = 3.0e38f;
+#pragma unroll 5
+        for (int o = 0; o < n_obs / 2; ++o) {
+            const float4 ob = op[o];
+            const float wc0 = xs - ob.x, ws0 = ys - ob.y, wc1 = xs - ob.z, ws1 = ys - ob.w;
+            qmin = fminf(qmin, fminf(fmaf(wc0, wc0, ws0 * ws0), fmaf(wc1, wc1, ws1 * ws1)));
+        }
+        if (qmin < 1.f) {
+            const float2* o2 = osm + t * n_obs;
+            for (int o = 0; o < n_obs; ++o) {
+                const float2 ob = o2[o];
+                const float wc = xs - ob.x, ws = ys - ob.y;
+                const float q = fmaf(wc, wc, ws * ws);
+                if (q < 1.f) {
+                    coll += 1.f - q;
+                    if (q > 0.f) {
+                        const float f = 1.f - rsqrtf(q);
+                        rox = fmaf(wc, f, rox);
+                        roy = fmaf(ws, f, roy);
+                    } else {
+                        rox -= 1.f;                // atan2(0,0) = 0: h - X = (a, 0)
+                    }
                 }
             }
         }
         // lane slack residual (pkg/projection.py:308-310,323)
         const float up = fmaxf(Y - L.y_ub, 0.f), lo = fmaxf(L.y_lb - Y, 0.f);
         const float rl = up - lo;
-        // back-projection g += Wd^T r_v + Wdd^T r_a + W^T r_o (+ lane)
+        // back-projection g += Wd^T r_v + Wdd^T r_a + W^T r_o (+ lane); the basis row is re-read
+        // from shared memory rather than held across the clip/obstacle section (register budget)
         const float tox = L.a * rox, toy = fmaf(L.b, roy, rl);
+#pragma unroll
+        for (int q = 0; q < WROW / 4; ++q) {
+            const float4 f = wr[q];
+            w[4 * q] = f.x; w[4 * q + 1] = f.y; w[4 * q + 2] = f.z; w[4 * q + 3] = f.w;
+        }
 #pragma unroll
         for (int k = 0; k < NC; ++k) {
             v[k] = fmaf(w[k], tox, fmaf(w[2 * NC + k], rax, fmaf(w[NC + k], rvx, v[k])));
@@ -205,7 +225,7 @@ __device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float
             r += fmaxf(dv - L.v_max, 0.f) + fmaxf(L.v_min - dv, 0.f);
             r += fmaxf(da - L.a_max, 0.f);
             const float sp = fmaxf(dv, 1e-6f);
-            r += fmaxf(fabsf(YDD * XD - XDD * YD) / (sp * sp * sp) - L.k_max, 0.f);
+            r += fmaxf(__fdividef(fabsf(YDD * XD - XDD * YD), sp * sp * sp) - L.k_max, 0.f);
             if (CURV) r += fmaxf(XD * XD * kcur - L.c_max, 0.f);
             v[NX] += r;
             const float e = dv - L.v_max;
@@ -215,7 +235,7 @@ __device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float
 }
 
 template <int P, bool CURV>
-__global__ void __launch_bounds__(256) am_kernel(const AmArgs a) {
+__global__ void __launch_bounds__(256, 2) am_kernel(const AmArgs a) {
     constexpr int NV = ((NX + 2 + P - 1) / P) * P;   // 22 back-projections + residual + cost, padded
     constexpr int ROWS = (NX + P - 1) / P;           // coefficient rows owned per lane
     extern __shared__ __align__(16) unsigned char smem[];
@@ -270,16 +290,19 @@ __global__ void __launch_bounds__(256) am_kernel(const AmArgs a) {
         for (int i = 0; i < NX; ++i) s = fma(-asm_[e * NX + i], su[i], s);
         eb[e] = s;
     }
-    double c[ROWS], ell[ROWS], dl[ROWS];
+    double c[ROWS];
+    double* ell = su + 36;          // l = xi_bar + lambda, owned rows only (no cross-lane traffic)
+    double* dl = su + 60;           // K_b (b - A xi_bar), used by the first update only
 #pragma unroll
     for (int r = 0; r < ROWS; ++r) {
         const int k = p + P * r;
-        c[r] = ell[r] = dl[r] = 0.0;
+        c[r] = 0.0;
         if (k < NX) {
-            c[r] = ell[r] = su[k];
+            c[r] = su[k];
+            ell[k] = c[r];
             double s = 0.0;
             for (int e = 0; e < neq; ++e) s = fma(kbsm[k * neq + e], eb[e], s);
-            dl[r] = s;
+            dl[k] = s;
             sc[k] = static_cast<float>(c[r]);
         }
     }
@@ -311,8 +334,12 @@ __global__ void __launch_bounds__(256) am_kernel(const AmArgs a) {
             const int k = p + P * r;
             if (k < NX) {
                 const double g = static_cast<double>(v[P * r]);
-                if (!first) ell[r] = fma(-0.5 * rho, g, ell[r]);
-                su[k + (k >= NC ? 1 : 0)] = ell[r] - c[r] - rho * g;   // per-axis stride 12 (16-B aligned)
+                double l = ell[k];
+                if (!first) {
+                    l = fma(-0.5 * rho, g, l);
+                    ell[k] = l;
+                }
+                su[k + (k >= NC ? 1 : 0)] = l - c[r] - rho * g;   // per-axis stride 12 (16-B aligned)
             }
         }
         __syncwarp();
@@ -324,7 +351,7 @@ __global__ void __launch_bounds__(256) am_kernel(const AmArgs a) {
                 const int kk = k - ax * NC;
                 const double2* kr = reinterpret_cast<const double2*>(ksm + (ax * NC + kk) * KROW);
                 const double2* ur = reinterpret_cast<const double2*>(su + ax * KROW);
-                double s0 = first ? dl[r] : 0.0, s1 = 0.0;
+                double s0 = first ? dl[k] : 0.0, s1 = 0.0;
 #pragma unroll
                 for (int q = 0; q < NC / 2; ++q) {
                     const double2 kq = kr[q];

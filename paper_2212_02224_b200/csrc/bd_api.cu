@@ -69,7 +69,7 @@ struct bd_ctx {
     double rho = 1.0;
     DevBuf kblk, kb, aeq;
     // scenes
-    int S = 0, scene_obs = 0, n_curv = 0;
+    int S = 0, scene_obs = 0, obs_pad = 0, n_curv = 0;
     DevBuf obs, lim, bscene, curvf, ox64, oy64, lim64, curv64;
     // workspace
     DevBuf w_xibar, w_b, w_mu, w_xi, w_res, w_cost, w_hist, w_itmax, w_iters, w_replay, w_conf, w_err, w_params;
@@ -283,7 +283,7 @@ int run_projection(bd_ctx* ctx, int B, const double* xi_bar, const double* b, in
     CU(cudaMemsetAsync(ctx->w_itmax.p, 0, (size_t)S * iters * ITMAX_SLOTS * 4, ctx->stream));
     CU(cudaMemsetAsync(conf, 0, (size_t)S * 8, ctx->stream));
     AmArgs a{};
-    a.m = ctx->m; a.neq = ctx->neq; a.n_obs = ctx->n_obs; a.n_curv = ctx->n_curv; a.B = B; a.max_iters = iters;
+    a.m = ctx->m; a.neq = ctx->neq; a.n_obs = ctx->obs_pad; a.n_curv = ctx->n_curv; a.B = B; a.max_iters = iters;
     a.rho = ctx->rho;
     a.wrow = ctx->wrow.as<float>(); a.kblk = ctx->kblk.as<double>(); a.kb = ctx->kb.as<double>();
     a.aeq = ctx->aeq.as<double>(); a.obs = ctx->obs.as<float2>(); a.lim = ctx->lim.as<SceneLim>();
@@ -530,7 +530,8 @@ int bd_set_scenes(bd_ctx* ctx, int S, int n_obs, int m, const double* ox, const 
     begin_call(ctx);
     const int neq = ctx->neq ? ctx->neq : 6;
     const size_t no = (size_t)S * n_obs * m;
-    std::vector<float2> obs(no ? no : 1);
+    const int nop = (n_obs + 1) / 2 * 2;                         // even: two obstacles per LDS.128
+    std::vector<float2> obs((size_t)S * nop * m + 1, make_float2(1e18f, 1e18f));
     std::vector<SceneLim> lim(S);
     std::vector<double> bs((size_t)S * neq, 0.0), l64((size_t)S * 9);
     for (int s = 0; s < S; ++s) {
@@ -547,10 +548,11 @@ int bd_set_scenes(bd_ctx* ctx, int S, int n_obs, int m, const double* ox, const 
         const double v9[9] = {l.ellipse_a, l.ellipse_b, l.v_min, l.v_max, l.a_max, l.kappa_max, l.c_max, l.y_lb, l.y_ub};
         memcpy(&l64[(size_t)s * 9], v9, sizeof v9);
         for (int e = 0; e < 6 && e < neq; ++e) bs[(size_t)s * neq + e] = b0[s * 6 + e];
-        for (size_t i = 0; i < (size_t)n_obs * m; ++i) {
-            const size_t g = (size_t)s * n_obs * m + i;
-            obs[g] = make_float2((float)(ox[g] / l.ellipse_a), (float)(oy[g] / l.ellipse_b));
-        }
+        for (int o = 0; o < n_obs; ++o)
+            for (int t = 0; t < m; ++t) {
+                const size_t g = ((size_t)s * n_obs + o) * m + t;
+                obs[((size_t)s * m + t) * nop + o] = make_float2((float)(ox[g] / l.ellipse_a), (float)(oy[g] / l.ellipse_b));
+            }
     }
     CU(ctx->obs.ensure(obs.size() * sizeof(float2)));
     CU(ctx->lim.ensure(lim.size() * sizeof(SceneLim)));
@@ -587,6 +589,7 @@ int bd_set_scenes(bd_ctx* ctx, int S, int n_obs, int m, const double* ox, const 
     CU(cudaMemset(ctx->w_err.p, 0, (size_t)S * 4));
     ctx->S = S;
     ctx->scene_obs = n_obs;
+    ctx->obs_pad = nop;
     ctx->n_curv = n_curv;
     return 0;
 }

@@ -29,6 +29,11 @@ if a.lanes:
 rec = HighwayRecipe(n_obs=a.obs, density=3.0 if a.obs > 10 else 2.0, vehicle_count=80 if a.obs > 10 else 24,
                     obstacle_range=250.0 if a.obs > 10 else 120.0)
 scenes = [highway_scene(s, rec) for s in range(a.scenes)]
+r = fp.plan(scenes, seed=0)
+fp.context.set_option("timing", 1)
+fp.context.stat("reset")
 for c in range(a.cycles):
     r = fp.plan(scenes, seed=c)
-print("done", r.iterations_done.min(), float(np.mean(r.best_cost)))
+ms, n, si = fp.context.stat("am_ms"), fp.context.stat("am_launches"), fp.context.stat("am_sample_iters")
+print(f"S={a.scenes} B={a.batch} obs={a.obs} lanes={a.lanes or 'auto'}: am {ms / n:.3f} ms/launch, "
+      f"{si / (ms * 1e-3) / 1e9:.3f} G sample-iters/s, done {r.iterations_done.min()} cost {float(np.mean(r.best_cost)):.1f}")
