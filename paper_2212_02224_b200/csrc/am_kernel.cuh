@@ -37,7 +37,7 @@ struct AmArgs {
     const double* kblk;         // 2 x NC x KROW   per-axis aug-KKT inverse blocks
     const double* kb;           // NX x neq        xi-b block of the aug-KKT inverse
     const double* aeq;          // neq x NX
-    const float2* obs;          // S x m x n_obs   (x_o / a, y_o / b), n_obs padded to even with far rows
+    const float4* obs;          // S x m x n_obs/2 pairs (-x0/a, -x1/a, -y0/b, -y1/b), n_obs padded to even
     const SceneLim* lim;        // S
     const double* bscene;       // S x neq         shared b per scene (b0, zero goal rows)
     const float* curv;          // S x 2 x n_curv  (xs then ks)
@@ -106,13 +106,14 @@ __device__ __forceinline__ void group_reduce_scatter(float (&v)[NV], int lane) {
     }
 }
 
-// One sweep over this lane's timesteps at the current coefficients cf:
-// forward evaluation, polar split + coupled clips, back-projection of the
-// residuals (v[0..21]), the direct residual (v[22]) and the upper cost (v[23]).
+// One sweep over this lane's timesteps at the current coefficients cxy[k] = (c_x[k], c_y[k]):
+// forward evaluation, polar split + coupled clips, back-projection of the residuals
+// (v[2k] = g_x[k], v[2k+1] = g_y[k]), the direct residual (v[22]) and the upper cost (v[23]).
+// The x/y pairs run as packed fp32x2 (FFMA2 with the basis value broadcast).
 template <int P, bool CURV, bool INIT, int NV>
-__device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float2* __restrict__ osm,
-                                      const float* __restrict__ csm, const float (&cf)[NX], float (&v)[NV],
-                                      float* dap, float* kap, int dstride, int p, int m, int n_obs, int n_curv,
+__device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float4* __restrict__ osm,
+                                      const float* __restrict__ csm, const float2 (&cxy)[NC], float (&v)[NV],
+                                      float* dap, float* kap, int dstride, int p, int m, int npair, int n_curv,
                                       const SceneLim& L, int& conf, bool& ovf) {
 #pragma unroll
     for (int k = 0; k < NV; ++k) v[k] = 0.f;
@@ -125,17 +126,15 @@ __device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float
             const float4 f = wr[q];
             w[4 * q] = f.x; w[4 * q + 1] = f.y; w[4 * q + 2] = f.z; w[4 * q + 3] = f.w;
         }
-        // forward: X = W c_x, ... (pkg/projection.py:295)
-        float X = 0.f, Y = 0.f, XD = 0.f, YD = 0.f, XDD = 0.f, YDD = 0.f;
+        // forward (X, Y) = W c, (Xd, Yd) = Wd c, (Xdd, Ydd) = Wdd c (pkg/projection.py:295)
+        float2 P0 = make_float2(0.f, 0.f), P1 = P0, P2 = P0;
 #pragma unroll
         for (int k = 0; k < NC; ++k) {
-            X = fmaf(w[k], cf[k], X);
-            Y = fmaf(w[k], cf[NC + k], Y);
-            XD = fmaf(w[NC + k], cf[k], XD);
-            YD = fmaf(w[NC + k], cf[NC + k], YD);
-            XDD = fmaf(w[2 * NC + k], cf[k], XDD);
-            YDD = fmaf(w[2 * NC + k], cf[NC + k], YDD);
+            P0 = ffma2(w[k], cxy[k], P0);
+            P1 = ffma2(w[NC + k], cxy[k], P1);
+            P2 = ffma2(w[2 * NC + k], cxy[k], P2);
         }
+        const float X = P0.x, Y = P0.y, XD = P1.x, YD = P1.y, XDD = P2.x, YDD = P2.y;
         // velocity / acceleration polar split (pkg/projection.py:119-122) in unit-vector form
         const float dv2 = fmaf(XD, XD, YD * YD);
         const float da2 = fmaf(XDD, XDD, YDD * YDD);
@@ -166,49 +165,52 @@ __device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float
         const float dac = fminf(fmaxf(da, 0.f), ahi);
         dap[di] = dac;
         // residuals F c - h of the velocity / acceleration blocks (pkg/projection.py:312-315)
-        float rvx, rvy, rax, ray;
-        if (dv2 > 0.f) { const float f = (dv - dvc) * iv; rvx = XD * f; rvy = YD * f; }
-        else { rvx = -dvc; rvy = 0.f; }
-        if (da2 > 0.f) { const float f = (da - dac) * ia; rax = XDD * f; ray = YDD * f; }
-        else { rax = -dac; ray = 0.f; }
+        float2 rv, ra;
+        if (dv2 > 0.f) rv = fmul2(make_float2((dv - dvc) * iv, (dv - dvc) * iv), P1);
+        else rv = make_float2(-dvc, 0.f);
+        if (da2 > 0.f) ra = fmul2(make_float2((da - dac) * ia, (da - dac) * ia), P2);
+        else ra = make_float2(-dac, 0.f);
         // obstacle block (pkg/projection.py:316-322) + clearance violation (pkg/constraints.py:116-120).
-        // Common path: branch-free min of the normalised squared distances over the tile row of
-        // this timestep (obstacles [t][o], two per LDS.128); only a lane inside some ellipse
+        // Common path: branch-free min of the normalised squared distances over this timestep's
+        // tile row, two obstacles per LDS.128 / FADD2 / FFMA2; only a lane inside some ellipse
         // (q < 1) takes the exact per-obstacle path.
         const float xs = X * L.inv_a, ys = Y * L.inv_b;
         float rox = 0.f, roy = 0.f, coll = 0.f;
-        const float4* op = reinterpret_cast<const float4*>(osm + t * n_obs);   // n_obs padded to even
+        const float4* op = osm + t * npair;          // (-x0, -x1, -y0, -y1) / (a, a, b, b)
         float qmin = 3.0e38f;
 #pragma unroll 5
-        for (int o = 0; o < n_obs / 2; ++o) {
+        for (int o = 0; o < npair; ++o) {
             const float4 ob = op[o];
-            const float wc0 = xs - ob.x, ws0 = ys - ob.y, wc1 = xs - ob.z, ws1 = ys - ob.w;
-            qmin = fminf(qmin, fminf(fmaf(wc0, wc0, ws0 * ws0), fmaf(wc1, wc1, ws1 * ws1)));
+            const float2 wc = fadd2(make_float2(xs, xs), make_float2(ob.x, ob.y));
+            const float2 ws = fadd2(make_float2(ys, ys), make_float2(ob.z, ob.w));
+            const float2 q = ffma2(wc, wc, fmul2(ws, ws));
+            qmin = fminf(qmin, fminf(q.x, q.y));
         }
         if (qmin < 1.f) {
-            const float2* o2 = osm + t * n_obs;
-            for (int o = 0; o < n_obs; ++o) {
-                const float2 ob = o2[o];
-                const float wc = xs - ob.x, ws = ys - ob.y;
-                const float q = fmaf(wc, wc, ws * ws);
-                if (q < 1.f) {
-                    coll += 1.f - q;
-                    if (q > 0.f) {
-                        const float f = 1.f - rsqrtf(q);
-                        rox = fmaf(wc, f, rox);
-                        roy = fmaf(ws, f, roy);
-                    } else {
-                        rox -= 1.f;                // atan2(0,0) = 0: h - X = (a, 0)
+            for (int o = 0; o < npair; ++o) {
+                const float4 ob = op[o];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const float wc = xs + (h ? ob.y : ob.x), ws = ys + (h ? ob.w : ob.z);
+                    const float q = fmaf(wc, wc, ws * ws);
+                    if (q < 1.f) {
+                        coll += 1.f - q;
+                        if (q > 0.f) {
+                            const float f = 1.f - rsqrtf(q);
+                            rox = fmaf(wc, f, rox);
+                            roy = fmaf(ws, f, roy);
+                        } else {
+                            rox -= 1.f;            // atan2(0,0) = 0: h - X = (a, 0)
+                        }
                     }
                 }
             }
         }
         // lane slack residual (pkg/projection.py:308-310,323)
         const float up = fmaxf(Y - L.y_ub, 0.f), lo = fmaxf(L.y_lb - Y, 0.f);
-        const float rl = up - lo;
+        const float2 ro = make_float2(L.a * rox, fmaf(L.b, roy, up - lo));
         // back-projection g += Wd^T r_v + Wdd^T r_a + W^T r_o (+ lane); the basis row is re-read
         // from shared memory rather than held across the clip/obstacle section (register budget)
-        const float tox = L.a * rox, toy = fmaf(L.b, roy, rl);
 #pragma unroll
         for (int q = 0; q < WROW / 4; ++q) {
             const float4 f = wr[q];
@@ -216,8 +218,12 @@ __device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float
         }
 #pragma unroll
         for (int k = 0; k < NC; ++k) {
-            v[k] = fmaf(w[k], tox, fmaf(w[2 * NC + k], rax, fmaf(w[NC + k], rvx, v[k])));
-            v[NC + k] = fmaf(w[k], toy, fmaf(w[2 * NC + k], ray, fmaf(w[NC + k], rvy, v[NC + k])));
+            float2 g = make_float2(v[2 * k], v[2 * k + 1]);
+            g = ffma2(w[NC + k], rv, g);
+            g = ffma2(w[2 * NC + k], ra, g);
+            g = ffma2(w[k], ro, g);
+            v[2 * k] = g.x;
+            v[2 * k + 1] = g.y;
         }
         if (!INIT) {
             // direct violations (pkg/constraints.py:124-138) and speed cost (pkg/bilevel.py:125-126)
@@ -250,7 +256,7 @@ __global__ void __launch_bounds__(256, 2) am_kernel(const AmArgs a) {
     const int threads = blockDim.x;
     const AmSmem lay(m, n_obs, neq, a.n_curv, a.s_cta, threads, P, CURV);
     float* wsm = reinterpret_cast<float*>(smem + lay.w);
-    float2* osm = reinterpret_cast<float2*>(smem + lay.obs);
+    float4* osm = reinterpret_cast<float4*>(smem + lay.obs);
     double* ksm = reinterpret_cast<double*>(smem + lay.k);
     double* kbsm = reinterpret_cast<double*>(smem + lay.kb);
     double* asm_ = reinterpret_cast<double*>(smem + lay.a);
@@ -259,8 +265,8 @@ __global__ void __launch_bounds__(256, 2) am_kernel(const AmArgs a) {
     // ---- stage constants and the scene tile once per CTA
     for (int i = threadIdx.x; i < m * WROW / 4; i += threads)
         reinterpret_cast<float4*>(wsm)[i] = reinterpret_cast<const float4*>(a.wrow)[i];
-    const float2* og = a.obs + (size_t)scene * n_obs * m;
-    for (int i = threadIdx.x; i < n_obs * m; i += threads) osm[i] = og[i];
+    const float4* og = reinterpret_cast<const float4*>(a.obs) + (size_t)scene * (n_obs / 2) * m;
+    for (int i = threadIdx.x; i < (n_obs / 2) * m; i += threads) osm[i] = og[i];
     for (int i = threadIdx.x; i < 2 * NC * KROW; i += threads) ksm[i] = a.kblk[i];
     for (int i = threadIdx.x; i < NX * neq; i += threads) { kbsm[i] = a.kb[i]; asm_[i] = a.aeq[i]; }
     if (CURV)
@@ -290,34 +296,33 @@ __global__ void __launch_bounds__(256, 2) am_kernel(const AmArgs a) {
         for (int i = 0; i < NX; ++i) s = fma(-asm_[e * NX + i], su[i], s);
         eb[e] = s;
     }
+    // value index i (0..21) <-> coefficient (axis i&1, kk = i>>1), state index ks = axis*NC + kk
     double c[ROWS];
     double* ell = su + 36;          // l = xi_bar + lambda, owned rows only (no cross-lane traffic)
     double* dl = su + 60;           // K_b (b - A xi_bar), used by the first update only
 #pragma unroll
     for (int r = 0; r < ROWS; ++r) {
-        const int k = p + P * r;
+        const int i = p + P * r;
         c[r] = 0.0;
-        if (k < NX) {
-            c[r] = su[k];
-            ell[k] = c[r];
+        if (i < NX) {
+            const int ks = (i & 1) * NC + (i >> 1);
+            c[r] = su[ks];
+            ell[ks] = c[r];
             double s = 0.0;
-            for (int e = 0; e < neq; ++e) s = fma(kbsm[k * neq + e], eb[e], s);
-            dl[k] = s;
-            sc[k] = static_cast<float>(c[r]);
+            for (int e = 0; e < neq; ++e) s = fma(kbsm[ks * neq + e], eb[e], s);
+            dl[ks] = s;
+            sc[i] = static_cast<float>(c[r]);
         }
     }
     __syncwarp();
-    float cf[NX];
+    float2 cxy[NC];
 #pragma unroll
-    for (int q = 0; q < NX / 2; ++q) {
-        const float2 f = reinterpret_cast<const float2*>(sc)[q];
-        cf[2 * q] = f.x; cf[2 * q + 1] = f.y;
-    }
+    for (int q = 0; q < NC; ++q) cxy[q] = reinterpret_cast<const float2*>(sc)[q];
 
     int conf = 0;
     bool bad = false, ovf = false;
     float v[NV];
-    sweep<P, CURV, true>(wsm, osm, csm, cf, v, dap, kap, threads, p, m, n_obs, a.n_curv, L, conf, ovf);
+    sweep<P, CURV, true>(wsm, osm, csm, cxy, v, dap, kap, threads, p, m, n_obs / 2, a.n_curv, L, conf, ovf);
     group_reduce_scatter<P>(v, lane);
 
     const int r_lane = NX % P, r_slot = (NX / P) * P;
@@ -331,27 +336,27 @@ __global__ void __launch_bounds__(256, 2) am_kernel(const AmArgs a) {
         const bool first = (it == 0);
 #pragma unroll
         for (int r = 0; r < ROWS; ++r) {
-            const int k = p + P * r;
-            if (k < NX) {
+            const int i = p + P * r;
+            if (i < NX) {
+                const int ax = i & 1, kk = i >> 1, ks = ax * NC + kk;
                 const double g = static_cast<double>(v[P * r]);
-                double l = ell[k];
+                double l = ell[ks];
                 if (!first) {
                     l = fma(-0.5 * rho, g, l);
-                    ell[k] = l;
+                    ell[ks] = l;
                 }
-                su[k + (k >= NC ? 1 : 0)] = l - c[r] - rho * g;   // per-axis stride 12 (16-B aligned)
+                su[ax * KROW + kk] = l - c[r] - rho * g;   // per-axis stride 12 (16-B aligned)
             }
         }
         __syncwarp();
 #pragma unroll
         for (int r = 0; r < ROWS; ++r) {
-            const int k = p + P * r;
-            if (k < NX) {
-                const int ax = k >= NC ? 1 : 0;
-                const int kk = k - ax * NC;
+            const int i = p + P * r;
+            if (i < NX) {
+                const int ax = i & 1, kk = i >> 1;
                 const double2* kr = reinterpret_cast<const double2*>(ksm + (ax * NC + kk) * KROW);
                 const double2* ur = reinterpret_cast<const double2*>(su + ax * KROW);
-                double s0 = first ? dl[k] : 0.0, s1 = 0.0;
+                double s0 = first ? dl[ax * NC + kk] : 0.0, s1 = 0.0;
 #pragma unroll
                 for (int q = 0; q < NC / 2; ++q) {
                     const double2 kq = kr[q];
@@ -362,17 +367,14 @@ __global__ void __launch_bounds__(256, 2) am_kernel(const AmArgs a) {
                 s0 = fma(kr[NC / 2].x, su[ax * KROW + NC - 1], s0);
                 c[r] += s0 + s1;
                 bad |= !isfinite(c[r]);
-                sc[k] = static_cast<float>(c[r]);
+                sc[i] = static_cast<float>(c[r]);
             }
         }
         __syncwarp();
 #pragma unroll
-        for (int q = 0; q < NX / 2; ++q) {
-            const float2 f = reinterpret_cast<const float2*>(sc)[q];
-            cf[2 * q] = f.x; cf[2 * q + 1] = f.y;
-        }
+        for (int q = 0; q < NC; ++q) cxy[q] = reinterpret_cast<const float2*>(sc)[q];
         // ---- projections, back-projection, residual at the new iterate
-        sweep<P, CURV, false>(wsm, osm, csm, cf, v, dap, kap, threads, p, m, n_obs, a.n_curv, L, conf, ovf);
+        sweep<P, CURV, false>(wsm, osm, csm, cxy, v, dap, kap, threads, p, m, n_obs / 2, a.n_curv, L, conf, ovf);
         group_reduce_scatter<P>(v, lane);
         resid = v[r_slot];
         cost = v[c_slot];
@@ -396,8 +398,8 @@ __global__ void __launch_bounds__(256, 2) am_kernel(const AmArgs a) {
     if (active) {
 #pragma unroll
         for (int r = 0; r < ROWS; ++r) {
-            const int k = p + P * r;
-            if (k < NX) a.xi_out[row * NX + k] = c[r];
+            const int i = p + P * r;
+            if (i < NX) a.xi_out[row * NX + (i & 1) * NC + (i >> 1)] = c[r];
         }
         if (p == r_lane) a.resid_out[row] = static_cast<double>(resid);
         if (a.cost_out && p == c_lane) a.cost_out[row] = static_cast<double>(cost);

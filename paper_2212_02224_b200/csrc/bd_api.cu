@@ -108,6 +108,31 @@ __global__ void __launch_bounds__(256) ffma_probe_kernel(float* out, int iters, 
     if (s == 12345.f) out[0] = s;
 }
 
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    float2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;"
+        : "=l"(*reinterpret_cast<unsigned long long*>(&r))
+        : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
+          "l"(*reinterpret_cast<unsigned long long*>(&c)));
+    return r;
+}
+
+// Packed FP32x2 variant of the probe (FFMA2, sm_100a).
+__global__ void __launch_bounds__(256) ffma2_probe_kernel(float* out, int iters, float a, float b) {
+    float2 v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = make_float2(threadIdx.x * 1e-3f + k, k * 0.5f);
+    const float2 aa = make_float2(a, a), bb = make_float2(b, b);
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = ffma2(v[k], aa, bb);
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += v[k].x + v[k].y;
+    if (s == 12345.f) out[0] = s;
+}
+
 int fail(bd_ctx* c, int code, const char* fmt, ...) {
     char buf[512];
     va_list ap;
@@ -286,7 +311,7 @@ int run_projection(bd_ctx* ctx, int B, const double* xi_bar, const double* b, in
     a.m = ctx->m; a.neq = ctx->neq; a.n_obs = ctx->obs_pad; a.n_curv = ctx->n_curv; a.B = B; a.max_iters = iters;
     a.rho = ctx->rho;
     a.wrow = ctx->wrow.as<float>(); a.kblk = ctx->kblk.as<double>(); a.kb = ctx->kb.as<double>();
-    a.aeq = ctx->aeq.as<double>(); a.obs = ctx->obs.as<float2>(); a.lim = ctx->lim.as<SceneLim>();
+    a.aeq = ctx->aeq.as<double>(); a.obs = ctx->obs.as<float4>(); a.lim = ctx->lim.as<SceneLim>();
     a.bscene = ctx->bscene.as<double>(); a.curv = ctx->curvf.as<float>();
     a.xi_bar = xi_bar; a.b = b; a.xi_out = xi; a.resid_out = res; a.cost_out = cost; a.hist_out = hist;
     a.itmax = ctx->w_itmax.as<unsigned>(); a.conflicts = conf; a.err = ctx->w_err.as<int>();
@@ -406,7 +431,8 @@ int bd_get_stat(bd_ctx* ctx, const char* key, double* value) {
 
 int bd_probe(bd_ctx* ctx, const char* what, double* value) {
     if (!ctx || !what || !value) return BD_ERR_VALUE;
-    if (strcmp(what, "fp32_tflops")) return fail(ctx, BD_ERR_VALUE, "unknown probe %s", what);
+    const bool x2 = !strcmp(what, "fp32x2_tflops");
+    if (strcmp(what, "fp32_tflops") && !x2) return fail(ctx, BD_ERR_VALUE, "unknown probe %s", what);
     cudaSetDevice(ctx->device);
     int sms = 0;
     CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
@@ -416,16 +442,17 @@ int bd_probe(bd_ctx* ctx, const char* what, double* value) {
     cudaEvent_t e0, e1;
     CU(cudaEventCreate(&e0));
     CU(cudaEventCreate(&e1));
-    ffma_probe_kernel<<<blocks, threads, 0, ctx->stream>>>(out.as<float>(), iters / 16, 0.999f, 1e-3f);  // warm
+    auto kern = x2 ? ffma2_probe_kernel : ffma_probe_kernel;
+    kern<<<blocks, threads, 0, ctx->stream>>>(out.as<float>(), iters / 16, 0.999f, 1e-3f);  // warm
     CU(cudaEventRecord(e0, ctx->stream));
-    ffma_probe_kernel<<<blocks, threads, 0, ctx->stream>>>(out.as<float>(), iters, 0.999f, 1e-3f);
+    kern<<<blocks, threads, 0, ctx->stream>>>(out.as<float>(), iters, 0.999f, 1e-3f);
     CU(cudaEventRecord(e1, ctx->stream));
     CU(cudaEventSynchronize(e1));
     float ms = 0.f;
     CU(cudaEventElapsedTime(&ms, e0, e1));
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    *value = 2.0 * 8.0 * (double)iters * blocks * threads / (ms * 1e-3) / 1e12;
+    *value = (x2 ? 2.0 : 1.0) * 2.0 * 8.0 * (double)iters * blocks * threads / (ms * 1e-3) / 1e12;
     return 0;
 }
 
@@ -531,7 +558,7 @@ int bd_set_scenes(bd_ctx* ctx, int S, int n_obs, int m, const double* ox, const 
     const int neq = ctx->neq ? ctx->neq : 6;
     const size_t no = (size_t)S * n_obs * m;
     const int nop = (n_obs + 1) / 2 * 2;                         // even: two obstacles per LDS.128
-    std::vector<float2> obs((size_t)S * nop * m + 1, make_float2(1e18f, 1e18f));
+    std::vector<float> obs((size_t)S * nop * m * 2 + 4, -1e18f);   // [s][t][pair] (-x0,-x1,-y0,-y1)
     std::vector<SceneLim> lim(S);
     std::vector<double> bs((size_t)S * neq, 0.0), l64((size_t)S * 9);
     for (int s = 0; s < S; ++s) {
@@ -551,14 +578,16 @@ int bd_set_scenes(bd_ctx* ctx, int S, int n_obs, int m, const double* ox, const 
         for (int o = 0; o < n_obs; ++o)
             for (int t = 0; t < m; ++t) {
                 const size_t g = ((size_t)s * n_obs + o) * m + t;
-                obs[((size_t)s * m + t) * nop + o] = make_float2((float)(ox[g] / l.ellipse_a), (float)(oy[g] / l.ellipse_b));
+                const size_t base = (((size_t)s * m + t) * (nop / 2) + o / 2) * 4 + (o & 1);
+                obs[base] = (float)(-ox[g] / l.ellipse_a);
+                obs[base + 2] = (float)(-oy[g] / l.ellipse_b);
             }
     }
-    CU(ctx->obs.ensure(obs.size() * sizeof(float2)));
+    CU(ctx->obs.ensure(obs.size() * sizeof(float)));
     CU(ctx->lim.ensure(lim.size() * sizeof(SceneLim)));
     CU(ctx->bscene.ensure(bs.size() * 8));
     CU(ctx->lim64.ensure(l64.size() * 8));
-    CU(cudaMemcpy(ctx->obs.p, obs.data(), obs.size() * sizeof(float2), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(ctx->obs.p, obs.data(), obs.size() * sizeof(float), cudaMemcpyHostToDevice));
     CU(cudaMemcpy(ctx->lim.p, lim.data(), lim.size() * sizeof(SceneLim), cudaMemcpyHostToDevice));
     CU(cudaMemcpy(ctx->bscene.p, bs.data(), bs.size() * 8, cudaMemcpyHostToDevice));
     CU(cudaMemcpy(ctx->lim64.p, l64.data(), l64.size() * 8, cudaMemcpyHostToDevice));
