@@ -231,10 +231,11 @@ void raise_smem(K kernel, size_t bytes) {
 
 int pick_lanes(bd_ctx* ctx, long total) {
     if (ctx->opt_lanes) return ctx->opt_lanes;
+    // measured on B200 (profiles/r01): latency-bound small batches want a warp per sample,
+    // throughput batches 8 lanes per sample (P=4 loses to its longer serial sweep)
     if (total <= 2500) return 32;
     if (total <= 5000) return 16;
-    if (total <= 12000) return 8;
-    return 4;
+    return 8;
 }
 
 template <int P, bool CURV>
