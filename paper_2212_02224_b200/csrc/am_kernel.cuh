@@ -51,7 +51,34 @@ struct AmArgs {
     unsigned long long* conflicts;  // S
     int* err;
     const int* replay;          // nullptr, or per-scene iteration count of a replay launch (0 = skip)
+    // full pass only (replay == nullptr): the last CTA of each scene runs the batch-global exit scan
+    double tol;
+    int* iters_used;            // S (nullptr: no in-kernel scan)
+    int* replay_out;            // S
+    unsigned* done_ctr;         // S, zero before the launch, re-armed to zero by the last CTA
 };
+
+__device__ __forceinline__ void exit_scan_block(const unsigned* base, int max_iters, double tol, int scene,
+                                                int* iters_used, int* replay, unsigned long long* conflicts) {
+    __shared__ int red[32];
+    int first = max_iters;
+    for (int it = threadIdx.x; it < max_iters; it += blockDim.x) {
+        unsigned mx = 0;
+        for (int s = 0; s < ITMAX_SLOTS; ++s) mx = max(mx, __ldcg(base + (size_t)it * ITMAX_SLOTS + s));
+        if (static_cast<double>(__uint_as_float(mx)) <= tol && it < first) first = it;
+    }
+    for (int o = 16; o >= 1; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = first;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x + 31) / 32; ++w) first = min(first, red[w]);
+        const int used = first < max_iters ? first + 1 : max_iters;
+        iters_used[scene] = used;
+        const int rep = used < max_iters ? used : 0;
+        if (replay) replay[scene] = rep;
+        if (rep && conflicts) conflicts[scene] = 0ull;
+    }
+}
 
 // Shared-memory carve-up, identical on host and device.
 struct AmSmem {
@@ -417,6 +444,22 @@ __global__ void __launch_bounds__(256, 2) am_kernel(const AmArgs a) {
         if (anybad) atomicOr(a.err + scene, ERR_NONFINITE);
         if (anyovf) atomicOr(a.err + scene, ERR_RANGE);
     }
+    // ---- batch-global early exit folded into the last CTA of the scene (no extra launch)
+    if (a.replay == nullptr && a.done_ctr != nullptr) {
+        __shared__ bool last;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            last = atomicAdd(a.done_ctr + scene, 1u) == gridDim.x - 1;
+        }
+        __syncthreads();
+        if (last) {
+            __threadfence();
+            exit_scan_block(a.itmax + (size_t)scene * a.max_iters * ITMAX_SLOTS, a.max_iters, a.tol, scene,
+                            a.iters_used, a.replay_out, a.conflicts);
+            if (threadIdx.x == 0) a.done_ctr[scene] = 0u;
+        }
+    }
 }
 
 // Batch-global early exit (pkg/projection.py:329): first iteration whose batch max
@@ -426,26 +469,8 @@ __global__ void __launch_bounds__(256, 2) am_kernel(const AmArgs a) {
 __global__ void exit_scan_kernel(const unsigned* itmax, int max_iters, double tol, int* iters_used, int* replay,
                                  unsigned long long* conflicts) {
     const int scene = blockIdx.x;
-    const unsigned* base = itmax + (size_t)scene * max_iters * ITMAX_SLOTS;
-    int first = max_iters;
-    for (int it = threadIdx.x; it < max_iters; it += blockDim.x) {
-        unsigned mx = 0;
-        for (int s = 0; s < ITMAX_SLOTS; ++s) mx = max(mx, base[(size_t)it * ITMAX_SLOTS + s]);
-        const float f = __uint_as_float(mx);
-        if (static_cast<double>(f) <= tol && it < first) first = it;
-    }
-    for (int o = 16; o >= 1; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
-    __shared__ int red[32];
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = first;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int w = 1; w < (int)(blockDim.x + 31) / 32; ++w) first = min(first, red[w]);
-        const int used = first < max_iters ? first + 1 : max_iters;
-        iters_used[scene] = used;
-        const int rep = used < max_iters ? used : 0;
-        if (replay) replay[scene] = rep;
-        if (rep && conflicts) conflicts[scene] = 0ull;
-    }
+    exit_scan_block(itmax + (size_t)scene * max_iters * ITMAX_SLOTS, max_iters, tol, scene, iters_used, replay,
+                    conflicts);
 }
 
 }  // namespace bd

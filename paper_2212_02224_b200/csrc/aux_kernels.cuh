@@ -25,26 +25,23 @@ struct S1Args {
     int* err;
 };
 
-__global__ void __launch_bounds__(256) stage1_kernel(const S1Args a) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    double* kinv = reinterpret_cast<double*>(smem);
-    double* kkt = kinv + a.nr * a.nr;
-    double* qm = kkt + a.nr * a.nr;                       // qmx | qmy
+__device__ __forceinline__ void stage1_load(const S1Args& a, double* kinv, double* kkt, double* qm) {
     const int nn = a.nr * a.nr;
     for (int i = threadIdx.x; i < nn; i += blockDim.x) { kinv[i] = a.kinv[i]; kkt[i] = a.kkt[i]; }
     if (!a.rhs_in)
         for (int i = threadIdx.x; i < NC * a.m_seg; i += blockDim.x) { qm[i] = a.qmx[i]; qm[NC * a.m_seg + i] = a.qmy[i]; }
-    __syncthreads();
+}
+
+// One sample per warp; pr points at its behaviour vector (global or shared memory).
+__device__ __forceinline__ void stage1_body(const S1Args& a, int row, const double* pr, const double* kinv,
+                                            const double* kkt, const double* qm) {
     const int lane = threadIdx.x & 31;
-    const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (row >= a.total) return;
     const int i = lane;
     double rhs = 0.0;
     if (a.rhs_in) {
         if (i < a.nr) rhs = a.rhs_in[(size_t)row * a.nr + i];
     } else {
     const int scene = row / a.B;
-    const double* pr = a.params + (size_t)row * a.dim;
     const int ms = a.m_seg;
     if (i < NC) {
         double s = 0.0;
@@ -90,6 +87,58 @@ __global__ void __launch_bounds__(256) stage1_kernel(const S1Args a) {
         if (a.mu) a.mu[(size_t)row * a.neq + e] = sol;
         if (a.b_out) a.b_out[(size_t)row * a.neq + e] = rhs;
     }
+}
+
+__global__ void __launch_bounds__(256) stage1_kernel(const S1Args a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double* kinv = reinterpret_cast<double*>(smem);
+    double* kkt = kinv + a.nr * a.nr;
+    double* qm = kkt + a.nr * a.nr;                       // qmx | qmy
+    stage1_load(a, kinv, kkt, qm);
+    __syncthreads();
+    const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (row >= a.total) return;
+    stage1_body(a, row, a.rhs_in ? nullptr : a.params + (size_t)row * a.dim, kinv, kkt, qm);
+}
+
+// K4 + K1 fused for the CEM cycle: p = mean + z L^T (pkg/bilevel.py:51-57; z from the caller
+// or device Philox; the warm-start tile on iteration 1) written to params, then stage 1.
+__global__ void __launch_bounds__(256) sample_stage1_kernel(CemState cs, int it, const double* z, const double* warm,
+                                                           uint64_t seed, int scene_offset, double* params,
+                                                           const S1Args a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double* kinv = reinterpret_cast<double*>(smem);
+    double* kkt = kinv + a.nr * a.nr;
+    double* qm = kkt + a.nr * a.nr;
+    double* pw = qm + 2 * NC * a.m_seg;                  // one behaviour vector per warp
+    stage1_load(a, kinv, kkt, qm);
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int row = blockIdx.x * (blockDim.x >> 5) + wid;
+    if (row >= a.total) return;
+    const int scene = row / a.B, j = row % a.B;
+    if (cs.err[scene]) return;                          // failed scene: frozen until the cycle ends
+    const int d = cs.dim;
+    double* pr = pw + wid * MAX_DIM;
+    if (warm != nullptr) {
+        if (lane < d) pr[lane] = warm[(size_t)row * d + lane];
+    } else {
+        double zz[MAX_DIM];
+        if (z != nullptr) {
+            for (int q = 0; q < d; ++q) zz[q] = z[(size_t)row * d + q];
+        } else {
+            philox_normals(seed, scene + scene_offset, it, j, zz, d);
+        }
+        if (lane < d) {
+            const double* L = cs.L + scene * d * d;
+            double acc = 0.0;
+            for (int q = 0; q < d; ++q) acc = fma(zz[q], L[lane * d + q], acc);
+            pr[lane] = cs.mean[scene * d + lane] + acc;
+        }
+    }
+    __syncwarp();
+    if (lane < d) params[(size_t)row * d + lane] = pr[lane];
+    stage1_body(a, row, pr, kinv, kkt, qm);
 }
 
 // SamplingDistribution.sample (pkg/bilevel.py:51-57) for one distribution: the factor is

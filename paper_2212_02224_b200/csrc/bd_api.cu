@@ -72,7 +72,7 @@ struct bd_ctx {
     int S = 0, scene_obs = 0, obs_pad = 0, n_curv = 0;
     DevBuf obs, lim, bscene, curvf, ox64, oy64, lim64, curv64;
     // workspace
-    DevBuf w_xibar, w_b, w_mu, w_xi, w_res, w_cost, w_hist, w_itmax, w_iters, w_replay, w_conf, w_err, w_params;
+    DevBuf w_xibar, w_b, w_mu, w_xi, w_res, w_cost, w_hist, w_itmax, w_iters, w_replay, w_conf, w_err, w_params, w_done;
     DevBuf stage[8];
     int n_stage = 0;
     std::vector<PendingCopy> pending;
@@ -306,6 +306,10 @@ int run_projection(bd_ctx* ctx, int B, const double* xi_bar, const double* b, in
     const int S = ctx->S;
     CU(ctx->w_itmax.ensure((size_t)S * iters * ITMAX_SLOTS * 4));
     CU(ctx->w_replay.ensure((size_t)S * 4));
+    if (ctx->w_done.bytes < (size_t)S * 4) {
+        CU(ctx->w_done.ensure((size_t)S * 4));
+        CU(cudaMemsetAsync(ctx->w_done.p, 0, (size_t)S * 4, ctx->stream));
+    }
     CU(cudaMemsetAsync(ctx->w_itmax.p, 0, (size_t)S * iters * ITMAX_SLOTS * 4, ctx->stream));
     CU(cudaMemsetAsync(conf, 0, (size_t)S * 8, ctx->stream));
     AmArgs a{};
@@ -317,11 +321,11 @@ int run_projection(bd_ctx* ctx, int B, const double* xi_bar, const double* b, in
     a.xi_bar = xi_bar; a.b = b; a.xi_out = xi; a.resid_out = res; a.cost_out = cost; a.hist_out = hist;
     a.itmax = ctx->w_itmax.as<unsigned>(); a.conflicts = conf; a.err = ctx->w_err.as<int>();
     a.replay = ctx->w_replay.as<int>();
-    int rc = launch_am(ctx, a, false);
+    a.tol = tol; a.iters_used = iters_used; a.replay_out = ctx->w_replay.as<int>();
+    a.done_ctr = ctx->w_done.as<unsigned>();
+    int rc = launch_am(ctx, a, false);     // its last CTA per scene runs the exit scan
     if (rc) return rc;
-    exit_scan_kernel<<<S, 128, 0, ctx->stream>>>(a.itmax, iters, tol, iters_used, ctx->w_replay.as<int>(), conf);
-    ctx->launches++;
-    return launch_am(ctx, a, true);
+    return launch_am(ctx, a, true);        // replay guard: exits at once unless an early exit fired
 }
 
 int run_stage1(bd_ctx* ctx, int B, const double* params, double* xi_bar, double* mu, double* b_out) {
@@ -801,7 +805,7 @@ int bd_rank_refit(bd_ctx* ctx, int S, int B, int dim, const double* resid, const
         return fail(ctx, BD_ERR_VALUE, "bad rank_refit call");
     if (!(n_elite <= n_cons && n_cons <= B) || n_elite < 1 || n_cons > 1024)
         return fail(ctx, BD_ERR_VALUE, "need 1 <= elites <= constraint_elites <= min(batch, 1024)");
-    if (B > 8192) return fail(ctx, BD_ERR_VALUE, "rank_refit supports at most 8192 samples per scene");
+    if (B > 16384) return fail(ctx, BD_ERR_VALUE, "rank_refit supports at most 16384 samples per scene");
     begin_call(ctx);
     int rc;
     const size_t tot = (size_t)S * B;
@@ -841,7 +845,7 @@ int bd_rank_refit(bd_ctx* ctx, int S, int B, int dim, const double* resid, const
     s.best_xi = ctx->c_best_xi.as<double>(); s.best_scal = ctx->c_best_s.as<double>();
     int np2 = 1;
     while (np2 < B) np2 <<= 1;
-    const size_t smem = (size_t)np2 * 12;
+    const size_t smem = rank_refit_smem(np2, n_cons, n_elite, dim);
     raise_smem(rank_refit_kernel, smem);
     rank_refit_kernel<<<S, 1024, smem, ctx->stream>>>(s, 0, np2);
     ctx->launches++;
@@ -864,7 +868,7 @@ int bd_cem_cycle(bd_ctx* ctx, int S, const bd_cem_config* cfg, const double* ini
     if (!(cfg->n_elite <= cfg->n_cons && cfg->n_cons <= B) || cfg->n_elite < 1 || cfg->n_cons > 1024)
         return fail(ctx, BD_ERR_VALUE, "need elites <= constraint_elites <= batch_size (<= 1024 constraint elites)");
     if (!(cfg->eta > 0 && cfg->eta <= 1) || !(cfg->gamma > 0)) return fail(ctx, BD_ERR_VALUE, "bad eta / gamma");
-    if (B > 8192) return fail(ctx, BD_ERR_VALUE, "CEM batch above 8192 per scene is not supported by this build");
+    if (B > 16384) return fail(ctx, BD_ERR_VALUE, "CEM batch above 16384 per scene is not supported by this build");
     begin_call(ctx);
     const size_t tot = (size_t)S * B;
     const double *dz = nullptr, *dwarm = nullptr, *dm0, *dc0;
@@ -906,14 +910,21 @@ int bd_cem_cycle(bd_ctx* ctx, int S, const bd_cem_config* cfg, const double* ini
     ctx->launches++;
     int np2 = 1;
     while (np2 < B) np2 <<= 1;
-    const size_t rsmem = (size_t)np2 * 12;
+    const size_t rsmem = rank_refit_smem(np2, cfg->n_cons, cfg->n_elite, dim);
     raise_smem(rank_refit_kernel, rsmem);
+    S1Args s1{};
+    s1.total = S * B; s1.B = B; s1.dim = dim; s1.neq = ctx->neq1; s1.m_seg = ctx->m_seg;
+    s1.with_goal = ctx->with_goal; s1.nr = NX + ctx->neq1; s1.nvar = NX;
+    s1.qmx = ctx->qmx.as<double>(); s1.qmy = ctx->qmy.as<double>(); s1.kkt = ctx->kkt1.as<double>();
+    s1.kinv = ctx->kinv1.as<double>(); s1.params = ctx->w_params.as<double>(); s1.bscene = ctx->bscene.as<double>();
+    s1.xi_bar = ctx->w_xibar.as<double>(); s1.mu = nullptr; s1.b_out = db; s1.err = ctx->w_err.as<int>();
+    const size_t s1smem = (size_t)(2 * s1.nr * s1.nr + 2 * NC * s1.m_seg + 8 * MAX_DIM) * 8;
+    raise_smem(sample_stage1_kernel, s1smem);
     for (int it = 0; it < N; ++it) {
         const double* zi = dz ? dz + (size_t)it * tot * dim : nullptr;
-        sample_kernel<<<(unsigned)((tot + 127) / 128), 128, 0, ctx->stream>>>(
-            s, it, zi, it == 0 ? dwarm : nullptr, cfg->seed, cfg->scene_offset, ctx->w_params.as<double>());
+        sample_stage1_kernel<<<(unsigned)((tot + 7) / 8), 256, s1smem, ctx->stream>>>(
+            s, it, zi, it == 0 ? dwarm : nullptr, cfg->seed, cfg->scene_offset, ctx->w_params.as<double>(), s1);
         ctx->launches++;
-        if ((rc = run_stage1(ctx, B, ctx->w_params.as<double>(), ctx->w_xibar.as<double>(), nullptr, db))) return rc;
         if ((rc = run_projection(ctx, B, ctx->w_xibar.as<double>(), db, cfg->am_iters, cfg->tol,
                                  ctx->w_xi.as<double>(), ctx->w_res.as<double>(), ctx->w_cost.as<double>(), nullptr,
                                  ctx->w_iters.as<int>(), ctx->w_conf.as<unsigned long long>())))

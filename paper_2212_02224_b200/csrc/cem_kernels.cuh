@@ -164,8 +164,30 @@ __global__ void sample_kernel(CemState s, int it, const double* z, const double*
     }
 }
 
+// Block-wide sum of one double per thread (result valid in every thread).
+__device__ __forceinline__ double block_sum(double v, double* red) {
+    for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+    return t;
+}
+
+// Dynamic shared memory of rank_refit_kernel (bytes); npow2 >= B and both powers of two.
+__host__ __device__ inline size_t rank_refit_smem(int npow2, int n_cons, int n_elite, int dim) {
+    int np2 = 1;
+    while (np2 < n_cons) np2 <<= 1;
+    const int staged = n_elite <= 128 ? n_elite : 0;
+    return (size_t)npow2 * 12 + (size_t)np2 * 20 + (size_t)staged * dim * 8;
+}
+
 // rank_samples + update_distribution + IterationStats + best record for one CEM
-// iteration, one CTA per scene.  Requires B <= 8192 (shared-memory sort).
+// iteration, one CTA (1024 threads) per scene.  The residual keys of the whole batch are
+// bitonic-sorted in shared memory (B <= 16384: 196 KB), the constraint elites re-sorted by
+// augmented cost, the q elite set-point vectors staged in shared memory and the weighted
+// mean / covariance reduced warp-parallel in fp64.
 __global__ void __launch_bounds__(1024) rank_refit_kernel(CemState s, int it, int npow2) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int scene = blockIdx.x;
@@ -174,13 +196,19 @@ __global__ void __launch_bounds__(1024) rank_refit_kernel(CemState s, int it, in
         if (threadIdx.x == 0 && s.done[scene] == it) s.done[scene] = (it == 0) ? -1 : it;
         return;
     }
+    const int n = s.n_cons, q = s.n_elite;
+    int np2 = 1;
+    while (np2 < n) np2 <<= 1;
+    // dynamic layout (rank_refit_smem): key | idx | key2 | idx2 | w | staged elite set-points
     unsigned long long* key = reinterpret_cast<unsigned long long*>(smem);
     int* idx = reinterpret_cast<int*>(key + npow2);
-    __shared__ unsigned long long key2[1024];
-    __shared__ int idx2[1024];
-    __shared__ double w[1024];
+    unsigned long long* key2 = reinterpret_cast<unsigned long long*>(idx + npow2);
+    int* idx2 = reinterpret_cast<int*>(key2 + np2);
+    double* w = reinterpret_cast<double*>(idx2 + np2);
+    double* pe = w + np2;                  // q <= 128 staged; larger q read from global
     __shared__ double red[32];
     __shared__ double mu_new[MAX_DIM];
+    __shared__ double cnew[MAX_DIM * MAX_DIM];
     const size_t base = (size_t)scene * s.B;
     for (int i = threadIdx.x; i < npow2; i += blockDim.x) {
         key[i] = i < s.B ? ordered_bits(s.resid[base + i]) : ~0ull;
@@ -189,15 +217,13 @@ __global__ void __launch_bounds__(1024) rank_refit_kernel(CemState s, int it, in
     __syncthreads();
     block_bitonic_sort(key, idx, npow2);
     // constraint elites: first n of the stable residual order; aug = cost + w r
-    const int n = s.n_cons, q = s.n_elite;
-    int np2 = 1;
-    while (np2 < n) np2 <<= 1;
     for (int i = threadIdx.x; i < np2; i += blockDim.x) {
         if (i < n) {
             const int j = idx[i];
             const double aug = s.cost[base + j] + s.w_res * s.resid[base + j];
             key2[i] = ordered_bits(aug);
             idx2[i] = j;
+            w[i] = aug;
             if (s.cons_idx) s.cons_idx[(size_t)scene * n + i] = j;
         } else {
             key2[i] = ~0ull;
@@ -207,48 +233,49 @@ __global__ void __launch_bounds__(1024) rank_refit_kernel(CemState s, int it, in
     __syncthreads();
     block_bitonic_sort(key2, idx2, np2);
     // elite weights exp(-(aug - min aug)/gamma), uniform fallback (pkg/bilevel.py:163-172)
-    const double amin = s.cost[base + idx2[0]] + s.w_res * s.resid[base + idx2[0]];
-    double part = 0.0;
+    const int j0 = idx2[0];
+    const double amin = s.cost[base + j0] + s.w_res * s.resid[base + j0];
+    double part = 0.0, cpart = 0.0;
+    const bool staged = q <= 128;
+    __syncthreads();
     for (int i = threadIdx.x; i < q; i += blockDim.x) {
         const int j = idx2[i];
         const double aug = s.cost[base + j] + s.w_res * s.resid[base + j];
-        w[i] = exp(-(aug - amin) / s.gamma);
-        part += w[i];
+        const double wi = exp(-(aug - amin) / s.gamma);
+        w[i] = wi;
+        part += wi;
+        cpart += s.cost[base + j];
         if (s.elite_idx) s.elite_idx[(size_t)scene * q + i] = j;
         if (s.elite_aug) s.elite_aug[(size_t)scene * q + i] = aug;
     }
-    for (int o = 16; o >= 1; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
-    __syncthreads();
-    __shared__ double total;
-    if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
-        total = t;
-    }
-    __syncthreads();
+    if (staged)
+        for (int e = threadIdx.x; e < q * d; e += blockDim.x) pe[e] = s.params[(base + idx2[e / d]) * d + e % d];
+    const double total = block_sum(part, red);
+    const double csum = block_sum(cpart, red);
     const bool uniform = !(isfinite(total) && total > 0.0);
     for (int i = threadIdx.x; i < q; i += blockDim.x) w[i] = uniform ? 1.0 / q : w[i] / total;
     __syncthreads();
-    // weighted mean / covariance refit (pkg/bilevel.py:175-194), fp64, one thread per entry
+    // weighted mean / covariance refit (pkg/bilevel.py:175-194): warp per output entry
     const double eta = s.eta;
     double* mean = s.mean + scene * d;
     double* cov = s.cov + scene * d * d;
-    if (threadIdx.x < d) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
+    auto P = [&](int i, int r) -> double {
+        return staged ? pe[i * d + r] : s.params[(base + idx2[i]) * d + r];
+    };
+    for (int r = warp; r < d; r += nwarp) {
         double acc = 0.0;
-        for (int i = 0; i < q; ++i) acc = fma(w[i], s.params[(base + idx2[i]) * d + threadIdx.x], acc);
-        mu_new[threadIdx.x] = (1.0 - eta) * mean[threadIdx.x] + eta * acc;
+        for (int i = lane; i < q; i += 32) acc = fma(w[i], P(i, r), acc);
+        for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) mu_new[r] = (1.0 - eta) * mean[r] + eta * acc;
     }
     __syncthreads();
-    __shared__ double cnew[MAX_DIM * MAX_DIM];
-    if (threadIdx.x < d * d) {
-        const int r = threadIdx.x / d, c = threadIdx.x % d;
+    for (int e = warp; e < d * d; e += nwarp) {
+        const int r = e / d, c = e % d;
         double acc = 0.0;
-        for (int i = 0; i < q; ++i) {
-            const double* pi = s.params + (base + idx2[i]) * d;
-            acc = fma(w[i] * (pi[r] - mu_new[r]), pi[c] - mu_new[c], acc);
-        }
-        cnew[threadIdx.x] = (1.0 - eta) * cov[threadIdx.x] + eta * acc + (r == c ? 1e-6 : 0.0);
+        for (int i = lane; i < q; i += 32) acc = fma(w[i] * (P(i, r) - mu_new[r]), P(i, c) - mu_new[c], acc);
+        for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) cnew[e] = (1.0 - eta) * cov[e] + eta * acc + (r == c ? 1e-6 : 0.0);
     }
     __syncthreads();
     if (threadIdx.x < d * d) {
@@ -256,16 +283,8 @@ __global__ void __launch_bounds__(1024) rank_refit_kernel(CemState s, int it, in
         cov[threadIdx.x] = 0.5 * (cnew[r * d + c] + cnew[c * d + r]);
     }
     if (threadIdx.x < d) mean[threadIdx.x] = mu_new[threadIdx.x];
-    // elite-mean upper cost
-    double cs = 0.0;
-    for (int i = threadIdx.x; i < q; i += blockDim.x) cs += s.cost[base + idx2[i]];
-    for (int o = 16; o >= 1; o >>= 1) cs += __shfl_xor_sync(0xffffffffu, cs, o);
-    __syncthreads();
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cs;
     __syncthreads();
     if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
         sampling_factor(cov, s.L + scene * d * d, d);
         // IterationStats (pkg/bilevel.py:282-292)
         const int B = s.B;
@@ -276,18 +295,17 @@ __global__ void __launch_bounds__(1024) rank_refit_kernel(CemState s, int it, in
         for (int i = 0; i < d; ++i) tr += cov[i * d + i];
         if (s.stats) {
             double* st = s.stats + ((size_t)scene * s.iters + it) * 6;
-            st[0] = t / q; st[1] = amin; st[2] = tr; st[3] = rmin; st[4] = rmed; st[5] = rmax;
+            st[0] = csum / q; st[1] = amin; st[2] = tr; st[3] = rmin; st[4] = rmed; st[5] = rmax;
         }
         // best EliteRecord = elite[0] (pkg/bilevel.py:272-280)
-        const int jb = idx2[0];
-        s.best_index[scene] = jb;
-        for (int k = 0; k < d; ++k) s.best_params[scene * d + k] = s.params[(base + jb) * d + k];
-        for (int k = 0; k < NX; ++k) s.best_xi[scene * NX + k] = s.xi[(base + jb) * NX + k];
-        s.best_scal[scene * 3 + 0] = s.cost[base + jb];
-        s.best_scal[scene * 3 + 1] = s.resid[base + jb];
+        s.best_index[scene] = j0;
+        s.best_scal[scene * 3 + 0] = s.cost[base + j0];
+        s.best_scal[scene * 3 + 1] = s.resid[base + j0];
         s.best_scal[scene * 3 + 2] = amin;
         s.done[scene] = it + 1;
     }
+    if (threadIdx.x < d) s.best_params[scene * d + threadIdx.x] = s.params[(base + j0) * d + threadIdx.x];
+    if (threadIdx.x < NX && s.xi) s.best_xi[scene * NX + threadIdx.x] = s.xi[(base + j0) * NX + threadIdx.x];
 }
 
 }  // namespace bd
