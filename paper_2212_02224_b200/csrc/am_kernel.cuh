@@ -267,10 +267,20 @@ __device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float
     }
 }
 
+// Pair barrier of the two warps that share a sample when P == 64 (named barriers 1..4).
+__device__ __forceinline__ void pair_sync() {
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + (int)(threadIdx.x >> 6)) : "memory");
+}
+
 template <int P, bool CURV>
 __global__ void __launch_bounds__(256, 2) am_kernel(const AmArgs a) {
-    constexpr int NV = ((NX + 2 + P - 1) / P) * P;   // 22 back-projections + residual + cost, padded
-    constexpr int ROWS = (NX + P - 1) / P;           // coefficient rows owned per lane
+    // P <= 32: a sample is a group of P lanes of one warp.  P == 64: a sample spans two warps
+    // (latency mapping for small batches); each warp reduce-scatters its partial sums, the second
+    // warp hands them to the first through shared memory and the first warp owns the update.
+    constexpr bool PAIR = (P == 64);
+    constexpr int RP = PAIR ? 32 : P;                // reduction width / ownership stride
+    constexpr int NV = ((NX + 2 + RP - 1) / RP) * RP;   // 22 back-projections + residual + cost, padded
+    constexpr int ROWS = (NX + RP - 1) / RP;         // coefficient rows owned per lane
     extern __shared__ __align__(16) unsigned char smem[];
 
     const int scene = blockIdx.y;
@@ -301,7 +311,9 @@ __global__ void __launch_bounds__(256, 2) am_kernel(const AmArgs a) {
     __syncthreads();
 
     const int lane = threadIdx.x & 31;
-    const int p = lane % P;
+    const int p = PAIR ? (int)(threadIdx.x % 64) : lane % P;        // timestep lane within the sample
+    const int own = PAIR ? ((threadIdx.x & 32) ? 64 : lane) : p;     // ownership index (>= NX: none)
+    auto gsync = [&]() { if (PAIR) pair_sync(); else __syncwarp(); };
     const int slot = threadIdx.x / P;
     const int local = blockIdx.x * a.s_cta + slot;
     const bool active = local < a.B;
@@ -315,7 +327,7 @@ __global__ void __launch_bounds__(256, 2) am_kernel(const AmArgs a) {
 
     // ---- prologue: xi_bar, equality residual correction delta = K_b (b - A xi_bar)
     for (int k = p; k < NX; k += P) su[k] = a.xi_bar[row * NX + k];
-    __syncwarp();
+    gsync();
     double eb[MAX_NEQ];
     const double* brow = a.b ? a.b + row * neq : a.bscene + (size_t)scene * neq;
     for (int e = 0; e < neq; ++e) {
@@ -329,7 +341,7 @@ __global__ void __launch_bounds__(256, 2) am_kernel(const AmArgs a) {
     double* dl = su + 60;           // K_b (b - A xi_bar), used by the first update only
 #pragma unroll
     for (int r = 0; r < ROWS; ++r) {
-        const int i = p + P * r;
+        const int i = own + RP * r;
         c[r] = 0.0;
         if (i < NX) {
             const int ks = (i & 1) * NC + (i >> 1);
@@ -341,7 +353,7 @@ __global__ void __launch_bounds__(256, 2) am_kernel(const AmArgs a) {
             sc[i] = static_cast<float>(c[r]);
         }
     }
-    __syncwarp();
+    gsync();
     float2 cxy[NC];
 #pragma unroll
     for (int q = 0; q < NC; ++q) cxy[q] = reinterpret_cast<const float2*>(sc)[q];
@@ -349,11 +361,20 @@ __global__ void __launch_bounds__(256, 2) am_kernel(const AmArgs a) {
     int conf = 0;
     bool bad = false, ovf = false;
     float v[NV];
+    float* xbuf = reinterpret_cast<float*>(smem + lay.scr + (size_t)slot * AmSmem::SCR_BYTES + 672);
+    auto reduce = [&]() {
+        group_reduce_scatter<RP>(v, lane);
+        if (PAIR) {                                   // second warp -> first warp partial sums
+            if ((threadIdx.x & 32) && lane < NX + 2) xbuf[lane] = v[0];
+            pair_sync();
+            if (!(threadIdx.x & 32) && lane < NX + 2) v[0] += xbuf[lane];
+        }
+    };
     sweep<P, CURV, true>(wsm, osm, csm, cxy, v, dap, kap, threads, p, m, n_obs / 2, a.n_curv, L, conf, ovf);
-    group_reduce_scatter<P>(v, lane);
+    reduce();
 
-    const int r_lane = NX % P, r_slot = (NX / P) * P;
-    const int c_lane = (NX + 1) % P, c_slot = ((NX + 1) / P) * P;
+    const int r_lane = NX % RP, r_slot = (NX / RP) * RP;
+    const int c_lane = (NX + 1) % RP, c_slot = ((NX + 1) / RP) * RP;
     float resid = 0.f, cost = 0.f;
     const int warp_global = blockIdx.x * (threads / 32) + (threadIdx.x >> 5);
     unsigned* itm = a.itmax + (size_t)scene * a.max_iters * ITMAX_SLOTS + (warp_global % ITMAX_SLOTS);
@@ -363,7 +384,7 @@ __global__ void __launch_bounds__(256, 2) am_kernel(const AmArgs a) {
         const bool first = (it == 0);
 #pragma unroll
         for (int r = 0; r < ROWS; ++r) {
-            const int i = p + P * r;
+            const int i = own + RP * r;
             if (i < NX) {
                 const int ax = i & 1, kk = i >> 1, ks = ax * NC + kk;
                 const double g = static_cast<double>(v[P * r]);
@@ -375,10 +396,10 @@ __global__ void __launch_bounds__(256, 2) am_kernel(const AmArgs a) {
                 su[ax * KROW + kk] = l - c[r] - rho * g;   // per-axis stride 12 (16-B aligned)
             }
         }
-        __syncwarp();
+        gsync();
 #pragma unroll
         for (int r = 0; r < ROWS; ++r) {
-            const int i = p + P * r;
+            const int i = own + RP * r;
             if (i < NX) {
                 const int ax = i & 1, kk = i >> 1;
                 const double2* kr = reinterpret_cast<const double2*>(ksm + (ax * NC + kk) * KROW);
@@ -397,16 +418,16 @@ __global__ void __launch_bounds__(256, 2) am_kernel(const AmArgs a) {
                 sc[i] = static_cast<float>(c[r]);
             }
         }
-        __syncwarp();
+        gsync();
 #pragma unroll
         for (int q = 0; q < NC; ++q) cxy[q] = reinterpret_cast<const float2*>(sc)[q];
         // ---- projections, back-projection, residual at the new iterate
         sweep<P, CURV, false>(wsm, osm, csm, cxy, v, dap, kap, threads, p, m, n_obs / 2, a.n_curv, L, conf, ovf);
-        group_reduce_scatter<P>(v, lane);
+        reduce();
         resid = v[r_slot];
         cost = v[c_slot];
         // ---- residual history + batch max for the batch-global early exit (pkg/projection.py:327-330)
-        const bool owner = (p == r_lane);
+        const bool owner = (own == r_lane);
         if (a.hist_out && owner && active)
             a.hist_out[((size_t)scene * a.max_iters + it) * a.B + local] = resid;
         if (a.replay == nullptr) {
@@ -425,11 +446,11 @@ __global__ void __launch_bounds__(256, 2) am_kernel(const AmArgs a) {
     if (active) {
 #pragma unroll
         for (int r = 0; r < ROWS; ++r) {
-            const int i = p + P * r;
+            const int i = own + RP * r;
             if (i < NX) a.xi_out[row * NX + (i & 1) * NC + (i >> 1)] = c[r];
         }
-        if (p == r_lane) a.resid_out[row] = static_cast<double>(resid);
-        if (a.cost_out && p == c_lane) a.cost_out[row] = static_cast<double>(cost);
+        if (own == r_lane) a.resid_out[row] = static_cast<double>(resid);
+        if (a.cost_out && own == c_lane) a.cost_out[row] = static_cast<double>(cost);
     } else {
         conf = 0;
         bad = false;

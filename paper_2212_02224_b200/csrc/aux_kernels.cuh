@@ -142,15 +142,15 @@ __global__ void __launch_bounds__(256) sample_stage1_kernel(CemState cs, int it,
 }
 
 // SamplingDistribution.sample (pkg/bilevel.py:51-57) for one distribution: the factor is
-// computed by thread 0 (chol, 1e-5 I fallback), then p = mean + z L^T per sample.
-__device__ void sampling_factor(const double* cov, double* L, int d);
-
+// computed by warp 0 (chol, 1e-5 I fallback), then p = mean + z L^T per sample.
 __global__ void sample_one_kernel(int d, int count, const double* mean, const double* cov, const double* z,
                                   double* out) {
-    __shared__ double L[MAX_DIM * MAX_DIM];
+    __shared__ double L[MAX_DIM * MAX_DIM], csh[MAX_DIM * MAX_DIM], lsh[MAX_DIM * MAX_DIM];
     __shared__ double mu[MAX_DIM];
-    if (threadIdx.x == 0) sampling_factor(cov, L, d);
+    for (int i = threadIdx.x; i < d * d; i += blockDim.x) csh[i] = cov[i];
     if (threadIdx.x < d) mu[threadIdx.x] = mean[threadIdx.x];
+    __syncthreads();
+    if (threadIdx.x < 32) warp_sampling_factor(csh, lsh, L, d, threadIdx.x);
     __syncthreads();
     for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < count; s += gridDim.x * blockDim.x) {
         for (int r = 0; r < d; ++r) {

@@ -272,6 +272,7 @@ int launch_am(bd_ctx* ctx, AmArgs a, bool replay_pass) {
     const long total = (long)a.B * ctx->S;
     const int P = pick_lanes(ctx, total);
     int threads = ctx->opt_spc ? ctx->opt_spc * P : (P == 32 ? 64 : 128);
+    if (P == 64 && threads % 64) threads = 128;
     if (threads % 32 || threads > 256 || threads < 32) return fail(ctx, BD_ERR_VALUE, "bad samples_per_cta");
     a.s_cta = threads / P;
     const bool curv = a.n_curv > 0;
@@ -284,7 +285,8 @@ int launch_am(bd_ctx* ctx, AmArgs a, bool replay_pass) {
         AM_CASE(8)
         AM_CASE(16)
         AM_CASE(32)
-        default: return fail(ctx, BD_ERR_VALUE, "lanes_per_sample must be 4, 8, 16 or 32");
+        AM_CASE(64)
+        default: return fail(ctx, BD_ERR_VALUE, "lanes_per_sample must be 4, 8, 16, 32 or 64");
     }
 #undef AM_CASE
 }
@@ -397,8 +399,8 @@ int bd_synchronize(bd_ctx* ctx) {
 int bd_set_option(bd_ctx* ctx, const char* key, int value) {
     if (!ctx || !key) return BD_ERR_VALUE;
     if (!strcmp(key, "lanes_per_sample")) {
-        if (value != 0 && value != 4 && value != 8 && value != 16 && value != 32)
-            return fail(ctx, BD_ERR_VALUE, "lanes_per_sample must be 0, 4, 8, 16 or 32");
+        if (value != 0 && value != 4 && value != 8 && value != 16 && value != 32 && value != 64)
+            return fail(ctx, BD_ERR_VALUE, "lanes_per_sample must be 0, 4, 8, 16, 32 or 64");
         ctx->opt_lanes = value;
         return 0;
     }

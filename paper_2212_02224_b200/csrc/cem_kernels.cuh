@@ -36,32 +36,48 @@ __device__ void block_bitonic_sort(unsigned long long* key, int* idx, int n_pow2
     }
 }
 
-// Cholesky of a dim x dim SPD matrix (row-major, fp64) by one thread; false if not PD.
-__device__ bool chol_small(const double* A, double* L, int d) {
-    for (int i = 0; i < d * d; ++i) L[i] = 0.0;
+// Warp-cooperative Cholesky of a dim x dim SPD matrix held in shared memory (row-major, fp64):
+// column j: lane 0 forms the pivot, lanes i > j the sub-diagonal entries.  Returns false (in
+// every lane) if the matrix is not positive definite.
+__device__ bool warp_chol(const double* A, double* L, int d, int lane) {
+    for (int i = lane; i < d * d; i += 32) L[i] = 0.0;
+    __syncwarp();
+    bool ok = true;
     for (int j = 0; j < d; ++j) {
-        double s = A[j * d + j];
-        for (int k = 0; k < j; ++k) s -= L[j * d + k] * L[j * d + k];
-        if (!(s > 0.0)) return false;
-        const double ljj = sqrt(s);
-        L[j * d + j] = ljj;
-        for (int i = j + 1; i < d; ++i) {
+        double piv = 0.0;
+        if (lane == 0) {
+            double s = A[j * d + j];
+            for (int k = 0; k < j; ++k) s -= L[j * d + k] * L[j * d + k];
+            piv = s;
+            L[j * d + j] = s > 0.0 ? sqrt(s) : 0.0;
+        }
+        piv = __shfl_sync(0xffffffffu, piv, 0);
+        __syncwarp();
+        if (!(piv > 0.0)) { ok = false; break; }
+        const double ljj = L[j * d + j];
+        const int i = j + 1 + lane;
+        if (i < d) {
             double t = A[i * d + j];
             for (int k = 0; k < j; ++k) t -= L[i * d + k] * L[j * d + k];
             L[i * d + j] = t / ljj;
         }
+        __syncwarp();
     }
-    return true;
+    return ok;
 }
 
-// SamplingDistribution.sample's factor: chol(cov), falling back to chol(cov + 1e-5 I) (pkg/bilevel.py:52-55).
-__device__ void sampling_factor(const double* cov, double* L, int d) {
-    if (chol_small(cov, L, d)) return;
-    double tmp[MAX_DIM * MAX_DIM];
-    for (int i = 0; i < d * d; ++i) tmp[i] = cov[i];
-    for (int i = 0; i < d; ++i) tmp[i * d + i] += 1e-5;
-    if (!chol_small(tmp, L, d))
-        for (int i = 0; i < d * d; ++i) L[i] = __longlong_as_double(0x7ff8000000000000ll);  // NaN: numpy would raise
+// SamplingDistribution.sample's factor (pkg/bilevel.py:52-55): chol(cov), falling back to
+// chol(cov + 1e-5 I); a failing fallback leaves NaN (numpy would raise).  One warp; cov_sh and
+// L_sh are shared-memory scratch (cov_sh is modified by the fallback); Lout receives the factor.
+__device__ void warp_sampling_factor(double* cov_sh, double* L_sh, double* Lout, int d, int lane) {
+    if (!warp_chol(cov_sh, L_sh, d, lane)) {
+        if (lane < d) cov_sh[lane * d + lane] += 1e-5;
+        __syncwarp();
+        if (!warp_chol(cov_sh, L_sh, d, lane))
+            for (int i = lane; i < d * d; i += 32) L_sh[i] = __longlong_as_double(0x7ff8000000000000ll);
+        __syncwarp();
+    }
+    for (int i = lane; i < d * d; i += 32) Lout[i] = L_sh[i];
 }
 
 // ---------------------------------------------------------------- Philox4x32-10 normals
@@ -126,11 +142,16 @@ struct CemState {
 __global__ void cem_init_kernel(CemState s, const double* mean0, const double* cov0) {
     const int scene = blockIdx.x;
     const int d = s.dim;
+    __shared__ double csh[MAX_DIM * MAX_DIM], lsh[MAX_DIM * MAX_DIM];
     for (int i = threadIdx.x; i < d; i += blockDim.x) s.mean[scene * d + i] = mean0[scene * d + i];
-    for (int i = threadIdx.x; i < d * d; i += blockDim.x) s.cov[scene * d * d + i] = cov0[scene * d * d + i];
+    for (int i = threadIdx.x; i < d * d; i += blockDim.x) {
+        const double v = cov0[scene * d * d + i];
+        s.cov[scene * d * d + i] = v;
+        csh[i] = v;
+    }
     __syncthreads();
+    if (threadIdx.x < 32) warp_sampling_factor(csh, lsh, s.L + scene * d * d, d, threadIdx.x);
     if (threadIdx.x == 0) {
-        sampling_factor(s.cov + scene * d * d, s.L + scene * d * d, d);
         s.err[scene] = 0;
         s.done[scene] = 0;
     }
@@ -278,21 +299,25 @@ __global__ void __launch_bounds__(1024) rank_refit_kernel(CemState s, int it, in
         if (lane == 0) cnew[e] = (1.0 - eta) * cov[e] + eta * acc + (r == c ? 1e-6 : 0.0);
     }
     __syncthreads();
+    __shared__ double csym[MAX_DIM * MAX_DIM], lsh[MAX_DIM * MAX_DIM];
     if (threadIdx.x < d * d) {
         const int r = threadIdx.x / d, c = threadIdx.x % d;
-        cov[threadIdx.x] = 0.5 * (cnew[r * d + c] + cnew[c * d + r]);
+        const double v = 0.5 * (cnew[r * d + c] + cnew[c * d + r]);
+        cov[threadIdx.x] = v;
+        csym[threadIdx.x] = v;
     }
     if (threadIdx.x < d) mean[threadIdx.x] = mu_new[threadIdx.x];
     __syncthreads();
+    if (threadIdx.x < 32) warp_sampling_factor(csym, lsh, s.L + scene * d * d, d, threadIdx.x);
+    __syncthreads();
     if (threadIdx.x == 0) {
-        sampling_factor(cov, s.L + scene * d * d, d);
         // IterationStats (pkg/bilevel.py:282-292)
         const int B = s.B;
         const double rmin = s.resid[base + idx[0]], rmax = s.resid[base + idx[B - 1]];
         const double rmed = (B & 1) ? s.resid[base + idx[B / 2]]
                                     : 0.5 * (s.resid[base + idx[B / 2 - 1]] + s.resid[base + idx[B / 2]]);
         double tr = 0.0;
-        for (int i = 0; i < d; ++i) tr += cov[i * d + i];
+        for (int i = 0; i < d; ++i) tr += cnew[i * d + i];   // symmetrisation keeps the diagonal
         if (s.stats) {
             double* st = s.stats + ((size_t)scene * s.iters + it) * 6;
             st[0] = csum / q; st[1] = amin; st[2] = tr; st[3] = rmin; st[4] = rmed; st[5] = rmax;

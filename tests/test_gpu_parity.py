@@ -65,7 +65,7 @@ def test_lower_level_solve_matches_reference(case):
     _check_lower(g, sol, proj, solver.last_costs)
 
 
-@pytest.mark.parametrize("lanes", [4, 8, 16, 32])
+@pytest.mark.parametrize("lanes", [4, 8, 16, 32, 64])
 @pytest.mark.parametrize("case", ["c1_s0", "canon", "dense50", "curve"])
 def test_every_lane_mapping_matches_reference(case, lanes):
     g = load("lower_" + case)
