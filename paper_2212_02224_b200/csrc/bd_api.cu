@@ -233,6 +233,7 @@ int pick_lanes(bd_ctx* ctx, long total) {
     if (ctx->opt_lanes) return ctx->opt_lanes;
     // measured on B200 (profiles/r01): latency-bound small batches want a warp per sample,
     // throughput batches 8 lanes per sample (P=4 loses to its longer serial sweep)
+    if (total <= 1200) return 64;   // one wave of two-warp samples on 148 SMs
     if (total <= 2500) return 32;
     if (total <= 5000) return 16;
     return 8;
