@@ -24,15 +24,17 @@ def main():
     ap.add_argument("rep")
     ap.add_argument("out")
     ap.add_argument("--samples", type=float, default=None, help="sample-iterations executed by the launch")
+    ap.add_argument("--kernel", default=None, help="regex of the kernel to summarise (first matching launch)")
     a = ap.parse_args()
-    det = ncu_csv(a.rep, "--page", "details")
+    sel = ["-k", "regex:" + a.kernel, "-c", "1"] if a.kernel else []
+    det = ncu_csv(a.rep, *sel, "--page", "details")
     hdr = det[0]
     metrics = {}
     for row in det[1:]:
         d = dict(zip(hdr, row))
         if d.get("Metric Name"):
             metrics[d["Metric Name"]] = (d["Metric Value"], d.get("Metric Unit", ""))
-    raw = ncu_csv(a.rep, "--page", "raw")
+    raw = ncu_csv(a.rep, *sel, "--page", "raw")
     rh, ru, rv = raw[0], raw[1], raw[2]
     rawd = {h: (v, u) for h, u, v in zip(rh, ru, rv)}
 
@@ -49,13 +51,15 @@ def main():
     dram_bytes = dram * scale.get(unit_r, 1) + dram_w * scale.get(rawd.get("dram__bytes_write.sum", ("", ""))[1], 1)
     pipes = {k: num(v[0]) for k, v in rawd.items()
              if k.startswith("sm__inst_executed_pipe_") and k.endswith("avg.pct_of_peak_sustained_active")}
-    sass = ncu_csv(a.rep, "--page", "source", "--print-source", "sass")
+    sass = ncu_csv(a.rep, *sel, "--page", "source", "--print-source", "sass")
     sh = sass[1]
     idx = {h: i for i, h in enumerate(sh)}
     stalls = collections.Counter()
     ops = collections.Counter()
     total = 0.0
     for r in sass[2:]:
+        if len(r) < len(sh):
+            break
         for h in sh:
             if h.startswith("stall_") and "Not Issued" not in h:
                 stalls[h[6:]] += num(r[idx[h]]) or 0.0
