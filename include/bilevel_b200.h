@@ -145,7 +145,23 @@ int bd_residuals(bd_ctx* ctx, int n_scenes, int batch, const double* xi, double*
 int bd_kkt_solve(bd_ctx* ctx, int nvar, int neq, const double* kkt, const double* kkt_inv, int count,
                  const double* rhs, double* sol);
 
+/* Sharded single-scene batch (multi-GPU, BASELINE config 4).  Stage 1 + AM projection of this
+ * rank's contiguous shard WITHOUT the batch-global exit decision: iter_max (max_iters floats)
+ * receives the shard's per-iteration maximum residual, which the caller all-reduces (MAX) over
+ * ranks to apply pkg/projection.py:329 globally; bd_replay_shard then re-runs the shard for
+ * exactly the global iteration count when the exit fired earlier.  One scene (S = 1). */
+int bd_solve_lower_shard(bd_ctx* ctx, int batch, const double* params, int max_iters, double* xi_bar, double* xi,
+                         double* residuals, double* cost, float* iter_max);
+int bd_replay_shard(bd_ctx* ctx, int batch, const double* xi_bar, int iterations, double* xi, double* residuals,
+                    double* cost);
+
 /* ------------------------------------------------------------------ upper level */
+
+/* Device-RNG sampling: p = mean + z chol(cov)^T with z = Philox4x32-10 normals keyed by
+ * (seed, scene, iteration, first_index + i) -- the same stream bd_cem_cycle draws, so any
+ * shard of a batch can be regenerated on any rank. */
+int bd_sample_philox(bd_ctx* ctx, int dim, int count, const double* mean, const double* cov, uint64_t seed,
+                     int scene, int iteration, int first_index, double* params);
 
 /* SamplingDistribution.sample (pkg/bilevel.py:51-57): p = mean + z chol(cov)^T, with the
  * reference's 1e-5 I fallback; z count x dim (e.g. from the caller's numpy Generator). */

@@ -41,6 +41,9 @@ SIGNATURES = {
     "bd_eval": (c_int, [_P, c_int, _P, _P, _P, _P, _P, _P, _P]),
     "bd_residuals": (c_int, [_P, c_int, c_int, _P, _P]),
     "bd_kkt_solve": (c_int, [_P, c_int, c_int, _P, _P, c_int, _P, _P]),
+    "bd_solve_lower_shard": (c_int, [_P, c_int, _P, c_int, _P, _P, _P, _P, _P]),
+    "bd_replay_shard": (c_int, [_P, c_int, _P, c_int, _P, _P, _P]),
+    "bd_sample_philox": (c_int, [_P, c_int, c_int, _P, _P, c_uint64, c_int, c_int, c_int, _P]),
     "bd_sample": (c_int, [_P, c_int, c_int, _P, _P, _P, _P]),
     "bd_rank_refit": (c_int, [_P, c_int, c_int, c_int, _P, _P, _P, c_int, c_int, c_double, c_double, c_double, _P, _P,
                               _P, _P, _P, _P]),
@@ -152,6 +155,10 @@ class Context:
         self.call("bd_set_option", key.encode(), int(value))
 
     def set_stream(self, stream_ptr: int | None):
+        """Run on an external cudaStream_t; 0 (torch's legacy default stream) maps to cudaStreamLegacy,
+        None restores the library's own stream."""
+        if stream_ptr == 0:
+            stream_ptr = 1   # cudaStreamLegacy
         self.call("bd_set_stream", stream_ptr)
 
     def synchronize(self):

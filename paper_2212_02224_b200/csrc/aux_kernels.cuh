@@ -161,6 +161,36 @@ __global__ void sample_one_kernel(int d, int count, const double* mean, const do
     }
 }
 
+// Philox-keyed variant of the above (bd_sample_philox).
+__global__ void sample_philox_kernel(int d, int count, const double* mean, const double* cov, uint64_t seed,
+                                     int scene, int iteration, int first_index, double* out) {
+    __shared__ double L[MAX_DIM * MAX_DIM], csh[MAX_DIM * MAX_DIM], lsh[MAX_DIM * MAX_DIM];
+    __shared__ double mu[MAX_DIM];
+    for (int i = threadIdx.x; i < d * d; i += blockDim.x) csh[i] = cov[i];
+    if (threadIdx.x < d) mu[threadIdx.x] = mean[threadIdx.x];
+    __syncthreads();
+    if (threadIdx.x < 32) warp_sampling_factor(csh, lsh, L, d, threadIdx.x);
+    __syncthreads();
+    for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < count; s += gridDim.x * blockDim.x) {
+        double z[MAX_DIM];
+        philox_normals(seed, scene, iteration, first_index + s, z, d);
+        for (int r = 0; r < d; ++r) {
+            double acc = 0.0;
+            for (int q = 0; q < d; ++q) acc = fma(z[q], L[r * d + q], acc);
+            out[(size_t)s * d + r] = mu[r] + acc;
+        }
+    }
+}
+
+// Per-iteration maximum over the spread slots of the early-exit buffer (one scene).
+__global__ void itmax_reduce_kernel(const unsigned* itmax, int iters, float* out) {
+    for (int it = blockIdx.x * blockDim.x + threadIdx.x; it < iters; it += gridDim.x * blockDim.x) {
+        unsigned mx = 0;
+        for (int s = 0; s < ITMAX_SLOTS; ++s) mx = max(mx, itmax[(size_t)it * ITMAX_SLOTS + s]);
+        out[it] = __uint_as_float(mx);
+    }
+}
+
 // ---------------------------------------------------------------- trajectory evaluation
 // eval_trajectory (pkg/basis.py:182-195) in fp64: one thread per (sample, timestep).
 __global__ void eval_kernel(int count, int m, const double* __restrict__ W, const double* __restrict__ Wd,

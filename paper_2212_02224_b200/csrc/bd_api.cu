@@ -305,7 +305,8 @@ int require_solver(bd_ctx* ctx, bool need_stage1) {
 
 // Projection core: xi_bar, b device pointers -> outputs in device buffers.
 int run_projection(bd_ctx* ctx, int B, const double* xi_bar, const double* b, int iters, double tol, double* xi,
-                   double* res, double* cost, float* hist, int* iters_used, unsigned long long* conf) {
+                   double* res, double* cost, float* hist, int* iters_used, unsigned long long* conf,
+                   bool external_exit = false) {
     const int S = ctx->S;
     CU(ctx->w_itmax.ensure((size_t)S * iters * ITMAX_SLOTS * 4));
     CU(ctx->w_replay.ensure((size_t)S * 4));
@@ -326,9 +327,24 @@ int run_projection(bd_ctx* ctx, int B, const double* xi_bar, const double* b, in
     a.replay = ctx->w_replay.as<int>();
     a.tol = tol; a.iters_used = iters_used; a.replay_out = ctx->w_replay.as<int>();
     a.done_ctr = ctx->w_done.as<unsigned>();
+    if (external_exit) a.done_ctr = nullptr;   // sharded batch: the exit is decided across ranks
     int rc = launch_am(ctx, a, false);     // its last CTA per scene runs the exit scan
-    if (rc) return rc;
+    if (rc || external_exit) return rc;
     return launch_am(ctx, a, true);        // replay guard: exits at once unless an early exit fired
+}
+
+AmArgs projection_args(bd_ctx* ctx, int B, const double* xi_bar, int iters, double* xi, double* res,
+                       double* cost) {
+    AmArgs a{};
+    a.m = ctx->m; a.neq = ctx->neq; a.n_obs = ctx->obs_pad; a.n_curv = ctx->n_curv; a.B = B; a.max_iters = iters;
+    a.rho = ctx->rho;
+    a.wrow = ctx->wrow.as<float>(); a.kblk = ctx->kblk.as<double>(); a.kb = ctx->kb.as<double>();
+    a.aeq = ctx->aeq.as<double>(); a.obs = ctx->obs.as<float4>(); a.lim = ctx->lim.as<SceneLim>();
+    a.bscene = ctx->bscene.as<double>(); a.curv = ctx->curvf.as<float>();
+    a.xi_bar = xi_bar; a.xi_out = xi; a.resid_out = res; a.cost_out = cost;
+    a.itmax = ctx->w_itmax.as<unsigned>(); a.conflicts = ctx->w_conf.as<unsigned long long>();
+    a.err = ctx->w_err.as<int>(); a.replay = ctx->w_replay.as<int>();
+    return a;
 }
 
 int run_stage1(bd_ctx* ctx, int B, const double* params, double* xi_bar, double* mu, double* b_out) {
@@ -751,6 +767,75 @@ int bd_residuals(bd_ctx* ctx, int S, int B, const double* xi, double* out) {
     r.ox = ctx->ox64.as<double>(); r.oy = ctx->oy64.as<double>(); r.lim = ctx->lim64.as<double>();
     r.curv = ctx->curv64.as<double>(); r.xi = dxi; r.out = dout;
     residual_kernel<<<(unsigned)((tot + 7) / 8), 256, 0, ctx->stream>>>(r);
+    ctx->launches++;
+    return finish_call(ctx, false, 0);
+}
+
+int bd_solve_lower_shard(bd_ctx* ctx, int B, const double* params, int iters, double* xi_bar, double* xi,
+                         double* res, double* cost, float* iter_max) {
+    if (!ctx) return BD_ERR_VALUE;
+    int rc = require_solver(ctx, true);
+    if (rc) return rc;
+    if (ctx->S != 1 || ctx->with_goal || B < 1 || !params || !xi_bar || !xi || !res || !iter_max || iters < 1)
+        return fail(ctx, BD_ERR_VALUE, "bad shard call (one scene, non-goal layout)");
+    begin_call(ctx);
+    const double* dp;
+    double *dxb, *dxi, *dres, *dcost;
+    float* dmax;
+    if ((rc = stage_in(ctx, params, (size_t)B * ctx->dim, &dp))) return rc;
+    if ((rc = stage_out_req(ctx, xi_bar, (size_t)B * NX, ctx->w_xibar, &dxb))) return rc;
+    if ((rc = stage_out(ctx, xi, (size_t)B * NX, ctx->w_xi, &dxi))) return rc;
+    if ((rc = stage_out(ctx, res, (size_t)B, ctx->w_res, &dres))) return rc;
+    if ((rc = stage_out(ctx, cost, (size_t)B, ctx->w_cost, &dcost))) return rc;
+    if ((rc = stage_out(ctx, iter_max, (size_t)iters, ctx->stage[7], &dmax))) return rc;
+    CU(ctx->w_iters.ensure(4));
+    CU(ctx->w_conf.ensure(8));
+    CU(cudaMemsetAsync(ctx->w_err.p, 0, 4, ctx->stream));
+    if ((rc = run_stage1(ctx, B, dp, dxb, nullptr, nullptr))) return rc;
+    if ((rc = run_projection(ctx, B, dxb, nullptr, iters, 1.0, dxi, dres, dcost, nullptr, ctx->w_iters.as<int>(),
+                             ctx->w_conf.as<unsigned long long>(), true)))
+        return rc;
+    itmax_reduce_kernel<<<1, 128, 0, ctx->stream>>>(ctx->w_itmax.as<unsigned>(), iters, dmax);
+    ctx->launches++;
+    return finish_call(ctx, ctx->host_out, 1);
+}
+
+int bd_replay_shard(bd_ctx* ctx, int B, const double* xi_bar, int iters, double* xi, double* res, double* cost) {
+    if (!ctx) return BD_ERR_VALUE;
+    int rc = require_solver(ctx, false);
+    if (rc) return rc;
+    if (ctx->S != 1 || B < 1 || !xi_bar || !xi || !res || iters < 1) return fail(ctx, BD_ERR_VALUE, "bad replay");
+    begin_call(ctx);
+    const double* dxb;
+    double *dxi, *dres, *dcost;
+    if ((rc = stage_in(ctx, xi_bar, (size_t)B * NX, &dxb))) return rc;
+    if ((rc = stage_out(ctx, xi, (size_t)B * NX, ctx->w_xi, &dxi))) return rc;
+    if ((rc = stage_out(ctx, res, (size_t)B, ctx->w_res, &dres))) return rc;
+    if ((rc = stage_out(ctx, cost, (size_t)B, ctx->w_cost, &dcost))) return rc;
+    CU(ctx->w_itmax.ensure((size_t)iters * ITMAX_SLOTS * 4));
+    CU(ctx->w_replay.ensure(4));
+    CU(ctx->w_conf.ensure(8));
+    CU(cudaMemsetAsync(ctx->w_err.p, 0, 4, ctx->stream));
+    CU(cudaMemcpyAsync(ctx->w_replay.p, &iters, 4, cudaMemcpyHostToDevice, ctx->stream));
+    AmArgs a = projection_args(ctx, B, dxb, iters, dxi, dres, dcost);
+    if ((rc = launch_am(ctx, a, true))) return rc;
+    return finish_call(ctx, true, 1);
+}
+
+int bd_sample_philox(bd_ctx* ctx, int dim, int count, const double* mean, const double* cov, uint64_t seed,
+                     int scene, int iteration, int first_index, double* params) {
+    if (!ctx) return BD_ERR_VALUE;
+    if (dim < 1 || dim > MAX_DIM || count < 1 || !mean || !cov || !params || first_index < 0)
+        return fail(ctx, BD_ERR_VALUE, "bad sample call");
+    begin_call(ctx);
+    int rc;
+    const double *dm, *dc;
+    double* dp;
+    if ((rc = stage_in(ctx, mean, (size_t)dim, &dm))) return rc;
+    if ((rc = stage_in(ctx, cov, (size_t)dim * dim, &dc))) return rc;
+    if ((rc = stage_out(ctx, params, (size_t)count * dim, ctx->w_params, &dp))) return rc;
+    const int blocks = count / 256 + 1 < 148 ? count / 256 + 1 : 148;
+    sample_philox_kernel<<<blocks, 256, 0, ctx->stream>>>(dim, count, dm, dc, seed, scene, iteration, first_index, dp);
     ctx->launches++;
     return finish_call(ctx, false, 0);
 }

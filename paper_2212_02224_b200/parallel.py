@@ -1,0 +1,191 @@
+"""Multi-GPU drivers: one process per GPU, torch.distributed (NCCL over NVLink) for the plumbing.
+
+Two ways the path shards:
+
+* **Fleet** (BASELINE config 5) — independent scenes, contiguous blocks of global scene ids per
+  rank, each planned with :class:`~paper_2212_02224_b200.fleet.FleetPlanner`.  No collective on
+  the data path; the per-scene best records are gathered once at the end (C4).
+
+* **Sharded batch** (BASELINE config 4) — one scene whose B samples are split contiguously over
+  ranks by global sample index.  Per CEM iteration (pkg/bilevel.py:249-292):
+
+  1. every rank regenerates the *full* batch of set-points from the device Philox stream keyed
+     by global sample index (bit-identical on every rank, independent of the rank count);
+  2. stage 1 + AM projection on the local shard only, without the batch-global exit;
+  3. C1: all-reduce(MAX) of the per-iteration shard maxima -> the reference's batch-global
+     early exit (pkg/projection.py:329) decided for the whole batch; ranks replay their shard
+     for exactly that many iterations if it fired;
+  4. C2: all-gather of the shard (residual, cost) pairs -> full arrays on every rank;
+  5. rank + refit on the full arrays, identically on every rank (C3 needs no sufficient-statistic
+     exchange: every rank already holds the elite set-points), then the owner of the best sample
+     broadcasts its 22 coefficients.
+
+The protocol is written against a small backend interface so the same code runs the CUDA path
+(:class:`CudaShardBackend`) and, in the CPU test-suite, an oracle stand-in over gloo.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+__all__ = ["shard_range", "ShardedCEM", "ShardedResult", "CudaShardBackend", "plan_fleet_distributed"]
+
+
+def _world(group=None):
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_rank(group), dist.get_world_size(group)
+    return 0, 1
+
+
+def shard_range(total: int, rank: int, world: int) -> tuple[int, int, int]:
+    """(lo, hi, shard) of the contiguous block of `total` items owned by `rank` (shard = ceil)."""
+    shard = math.ceil(total / world)
+    lo = min(total, rank * shard)
+    return lo, min(total, lo + shard), shard
+
+
+@dataclass
+class ShardedResult:
+    best_index: int
+    best_xi: np.ndarray
+    best_cost: float
+    best_residual: float
+    best_aug: float
+    stats: np.ndarray          # N x 6 IterationStats fields
+    mean: np.ndarray
+    cov: np.ndarray
+    iterations_used: list      # AM iterations actually run per CEM iteration
+
+
+class ShardedCEM:
+    """solve_bilevel over one scene with the batch sharded across the process group."""
+
+    def __init__(self, backend, batch: int, n_cons: int, n_elite: int, iterations: int, eta: float, gamma: float,
+                 residual_weight: float, am_iters: int, tol: float, seed: int, group=None):
+        self.b = backend
+        self.B, self.n, self.q, self.N = batch, n_cons, n_elite, iterations
+        self.eta, self.gamma, self.w = eta, gamma, residual_weight
+        self.am_iters, self.tol, self.seed = am_iters, tol, seed
+        self.group = group
+        self.rank, self.world = _world(group)
+        self.lo, self.hi, self.shard = shard_range(batch, self.rank, self.world)
+
+    def _all_reduce_max(self, t: torch.Tensor) -> torch.Tensor:
+        if self.world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        return t
+
+    def _all_gather(self, t: torch.Tensor) -> torch.Tensor:
+        """Gather equal-size (padded) shards; returns the concatenation trimmed to the batch."""
+        if self.world == 1:
+            return t
+        pad = torch.full((self.shard,) + tuple(t.shape[1:]), float("inf"), dtype=t.dtype, device=t.device)
+        pad[: t.shape[0]] = t
+        parts = [torch.empty_like(pad) for _ in range(self.world)]
+        dist.all_gather(parts, pad, group=self.group)
+        return torch.cat(parts)[: self.B]
+
+    def run(self, init_mean, init_cov) -> ShardedResult:
+        mean = self.b.tensor(init_mean)
+        cov = self.b.tensor(init_cov)
+        stats, used_log = [], []
+        best = None
+        for it in range(self.N):
+            P = self.b.sample(mean, cov, self.seed, it, self.B)                 # full batch, every rank
+            shard = self.b.solve_shard(P[self.lo:self.hi], self.am_iters)         # no exit decision
+            itmax = self._all_reduce_max(shard["iter_max"].clone())              # C1
+            hit = torch.nonzero(itmax.double() <= self.tol)
+            used = int(hit[0, 0]) + 1 if hit.numel() else self.am_iters
+            if used < self.am_iters:                                              # batch-global exit fired
+                shard = dict(shard, **self.b.replay_shard(used))
+            used_log.append(used)
+            rc = torch.stack([shard["residuals"], shard["cost"]], dim=1)
+            full = self._all_gather(rc)                                           # C2
+            out = self.b.rank_refit(full[:, 0].contiguous(), full[:, 1].contiguous(), P, mean, cov, self.n, self.q,
+                                    self.w, self.eta, self.gamma)
+            mean, cov = out["mean"], out["cov"]
+            j = int(out["elite_idx"][0])
+            owner = min(j // self.shard, self.world - 1)
+            xi = torch.zeros(22, dtype=torch.float64, device=mean.device)
+            if self.rank == owner:
+                xi.copy_(shard["xi"][j - self.lo])
+            if self.world > 1:
+                dist.broadcast(xi, src=owner, group=self.group)
+            best = (j, xi.cpu().numpy(), float(full[j, 1]), float(full[j, 0]), float(out["elite_aug"][0]))
+            stats.append(np.asarray(out["stats"].cpu(), dtype=np.float64))
+        return ShardedResult(best[0], best[1], best[2], best[3], best[4], np.array(stats),
+                             mean.cpu().numpy(), cov.cpu().numpy(), used_log)
+
+
+class CudaShardBackend:
+    """ShardedCEM backend on the CUDA library (device tensors, C-ABI on the torch stream)."""
+
+    def __init__(self, solver, scene, device: int | None = None):
+        self.solver = solver
+        self.ctx = solver.context
+        self.dev = torch.device("cuda", device if device is not None else torch.cuda.current_device())
+        solver.projector._check_spec(scene.spec)
+        solver.projector._ensure_scene(scene)
+        self.ctx.set_stream(torch.cuda.current_stream(self.dev).cuda_stream)
+        self.dim = solver.layout.dim
+
+    def tensor(self, x):
+        return torch.as_tensor(np.asarray(x, dtype=np.float64), device=self.dev).contiguous()
+
+    def sample(self, mean, cov, seed, it, count):
+        P = torch.empty((count, self.dim), dtype=torch.float64, device=self.dev)
+        self.ctx.call("bd_sample_philox", self.dim, count, mean, cov, int(seed), 0, int(it), 0, P)
+        return P
+
+    def solve_shard(self, P, iters):
+        n = P.shape[0]
+        self._xb = torch.empty((n, 22), dtype=torch.float64, device=self.dev)
+        xi = torch.empty_like(self._xb)
+        res = torch.empty(n, dtype=torch.float64, device=self.dev)
+        cost = torch.empty_like(res)
+        mx = torch.empty(iters, dtype=torch.float32, device=self.dev)
+        self.ctx.call("bd_solve_lower_shard", n, P.contiguous(), iters, self._xb, xi, res, cost, mx)
+        return {"xi": xi, "residuals": res, "cost": cost, "iter_max": mx}
+
+    def replay_shard(self, iters):
+        n = self._xb.shape[0]
+        xi = torch.empty_like(self._xb)
+        res = torch.empty(n, dtype=torch.float64, device=self.dev)
+        cost = torch.empty_like(res)
+        self.ctx.call("bd_replay_shard", n, self._xb, iters, xi, res, cost)
+        return {"xi": xi, "residuals": res, "cost": cost}
+
+    def rank_refit(self, resid, cost, P, mean, cov, n, q, w, eta, gamma):
+        B = resid.shape[0]
+        mean, cov = mean.clone(), cov.clone()
+        el = torch.empty(q, dtype=torch.int64, device=self.dev)
+        ea = torch.empty(q, dtype=torch.float64, device=self.dev)
+        st = torch.empty(6, dtype=torch.float64, device=self.dev)
+        self.ctx.call("bd_rank_refit", 1, B, self.dim, resid, cost, P.contiguous(), n, q, float(w), float(eta),
+                      float(gamma), mean, cov, None, el, ea, st)
+        return {"mean": mean, "cov": cov, "elite_idx": el, "elite_aug": ea, "stats": st}
+
+
+def plan_fleet_distributed(planner, scene_factory, n_scenes: int, seed: int = 0, group=None):
+    """Config 5: each rank plans its contiguous block of global scene ids; the best records are
+    all-gathered at the end (C4).  Returns the full FleetResult arrays on every rank."""
+    rank, world = _world(group)
+    lo, hi, shard = shard_range(n_scenes, rank, world)
+    scenes = [scene_factory(g) for g in range(lo, hi)]
+    res = planner.plan(scenes, seed=seed, scene_offset=lo)
+    cols = np.concatenate([res.best_index[:, None].astype(np.float64), res.best_cost[:, None],
+                           res.best_residual[:, None], res.best_aug[:, None], res.best_xi,
+                           res.iterations_done[:, None].astype(np.float64)], axis=1)
+    if world == 1:
+        return cols
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    t = torch.full((shard, cols.shape[1]), float("nan"), dtype=torch.float64, device=dev)
+    t[: cols.shape[0]] = torch.as_tensor(cols, device=dev)
+    parts = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(parts, t, group=group)
+    return torch.cat(parts)[:n_scenes].cpu().numpy()
