@@ -137,11 +137,16 @@ __device__ __forceinline__ void group_reduce_scatter(float (&v)[NV], int lane) {
 // forward evaluation, polar split + coupled clips, back-projection of the residuals
 // (v[2k] = g_x[k], v[2k+1] = g_y[k]), the direct residual (v[22]) and the upper cost (v[23]).
 // The x/y pairs run as packed fp32x2 (FFMA2 with the basis value broadcast).
-template <int P, bool CURV, bool INIT, int NV>
+template <int P, bool CURV, bool INIT, int NV, int MT, int NPT, int TPB>
 __device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float4* __restrict__ osm,
                                       const float* __restrict__ csm, const float2 (&cxy)[NC], float (&v)[NV],
-                                      float* dap, float* kap, int dstride, int p, int m, int npair, int n_curv,
-                                      const SceneLim& L, int& conf, bool& ovf) {
+                                      float* dap, float* kap, int dstride_rt, int p, int m_rt, int npair_rt,
+                                      int n_curv, const SceneLim& L, int& conf, bool& ovf) {
+    // MT / NPT / TPB > 0: timesteps, obstacle pairs and CTA size fixed at compile time (the
+    // BASELINE shapes), so the tile addressing folds into immediates and the pair loop unrolls.
+    const int m = MT ? MT : m_rt;
+    const int npair = NPT ? NPT : npair_rt;
+    const int dstride = TPB ? TPB : dstride_rt;
 #pragma unroll
     for (int k = 0; k < NV; ++k) v[k] = 0.f;
     int j = 0;
@@ -272,7 +277,7 @@ __device__ __forceinline__ void pair_sync() {
     asm volatile("bar.sync %0, 64;" ::"r"(1 + (int)(threadIdx.x >> 6)) : "memory");
 }
 
-template <int P, bool CURV>
+template <int P, bool CURV, int MT = 0, int NPT = 0, int TPB = 0>
 __global__ void __launch_bounds__(256, 2) am_kernel(const AmArgs a) {
     // P <= 32: a sample is a group of P lanes of one warp.  P == 64: a sample spans two warps
     // (latency mapping for small batches); each warp reduce-scatters its partial sums, the second
@@ -370,7 +375,8 @@ __global__ void __launch_bounds__(256, 2) am_kernel(const AmArgs a) {
             if (!(threadIdx.x & 32) && lane < NX + 2) v[0] += xbuf[lane];
         }
     };
-    sweep<P, CURV, true>(wsm, osm, csm, cxy, v, dap, kap, threads, p, m, n_obs / 2, a.n_curv, L, conf, ovf);
+    sweep<P, CURV, true, NV, MT, NPT, TPB>(wsm, osm, csm, cxy, v, dap, kap, threads, p, m, n_obs / 2, a.n_curv, L,
+                                           conf, ovf);
     reduce();
 
     const int r_lane = NX % RP, r_slot = (NX / RP) * RP;
@@ -422,7 +428,8 @@ __global__ void __launch_bounds__(256, 2) am_kernel(const AmArgs a) {
 #pragma unroll
         for (int q = 0; q < NC; ++q) cxy[q] = reinterpret_cast<const float2*>(sc)[q];
         // ---- projections, back-projection, residual at the new iterate
-        sweep<P, CURV, false>(wsm, osm, csm, cxy, v, dap, kap, threads, p, m, n_obs / 2, a.n_curv, L, conf, ovf);
+        sweep<P, CURV, false, NV, MT, NPT, TPB>(wsm, osm, csm, cxy, v, dap, kap, threads, p, m, n_obs / 2, a.n_curv,
+                                                L, conf, ovf);
         reduce();
         resid = v[r_slot];
         cost = v[c_slot];

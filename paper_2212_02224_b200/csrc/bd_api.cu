@@ -239,11 +239,11 @@ int pick_lanes(bd_ctx* ctx, long total) {
     return 8;
 }
 
-template <int P, bool CURV>
+template <int P, bool CURV, int MT = 0, int NPT = 0, int TPB = 0>
 int launch_am_t(bd_ctx* ctx, AmArgs a, int threads, bool replay_pass) {
     const AmSmem lay(a.m, a.n_obs, a.neq, a.n_curv, a.s_cta, threads, P, CURV);
     if (lay.total > 227 * 1024) return fail(ctx, BD_ERR_VALUE, "AM kernel needs %zu B of shared memory", lay.total);
-    raise_smem(am_kernel<P, CURV>, lay.total);
+    raise_smem(am_kernel<P, CURV, MT, NPT, TPB>, lay.total);
     dim3 grid((a.B + a.s_cta - 1) / a.s_cta, ctx->S);
     if (!replay_pass) a.replay = nullptr;
     std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
@@ -258,7 +258,7 @@ int launch_am_t(bd_ctx* ctx, AmArgs a, int threads, bool replay_pass) {
         }
         cudaEventRecord(ev.first, ctx->stream);
     }
-    am_kernel<P, CURV><<<grid, threads, lay.total, ctx->stream>>>(a);
+    am_kernel<P, CURV, MT, NPT, TPB><<<grid, threads, lay.total, ctx->stream>>>(a);
     ctx->launches++;
     if (timed) {
         cudaEventRecord(ev.second, ctx->stream);
@@ -277,9 +277,14 @@ int launch_am(bd_ctx* ctx, AmArgs a, bool replay_pass) {
     if (threads % 32 || threads > 256 || threads < 32) return fail(ctx, BD_ERR_VALUE, "bad samples_per_cta");
     a.s_cta = threads / P;
     const bool curv = a.n_curv > 0;
-#define AM_CASE(PP)                                                                       \
-    case PP:                                                                              \
-        return curv ? launch_am_t<PP, true>(ctx, a, threads, replay_pass)                 \
+    const int dflt = P == 32 ? 64 : 128;
+    // compile-time shapes of the BASELINE configs (m = 100; 10 or 50 obstacles), default CTA size
+    const bool fixed = !curv && a.m == 100 && threads == dflt;
+#define AM_CASE(PP)                                                                                      \
+    case PP:                                                                                             \
+        if (fixed && a.n_obs == 10) return launch_am_t<PP, false, 100, 5, (PP == 32 ? 64 : 128)>(ctx, a, threads, replay_pass); \
+        if (fixed && a.n_obs == 50) return launch_am_t<PP, false, 100, 25, (PP == 32 ? 64 : 128)>(ctx, a, threads, replay_pass); \
+        return curv ? launch_am_t<PP, true>(ctx, a, threads, replay_pass)                                \
                     : launch_am_t<PP, false>(ctx, a, threads, replay_pass);
     switch (P) {
         AM_CASE(4)
