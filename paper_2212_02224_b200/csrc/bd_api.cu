@@ -229,21 +229,19 @@ void raise_smem(K kernel, size_t bytes) {
     if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
-int pick_lanes(bd_ctx* ctx, long total) {
-    if (ctx->opt_lanes) return ctx->opt_lanes;
-    // measured on B200 (profiles/r01): latency-bound small batches want a warp per sample,
-    // throughput batches 8 lanes per sample (P=4 loses to its longer serial sweep)
-    if (total <= 1200) return 64;   // one wave of two-warp samples on 148 SMs
-    if (total <= 2500) return 32;
-    if (total <= 5000) return 16;
-    return 8;
-}
-
 template <int P, bool CURV, int MT = 0, int NPT = 0, int TPB = 0>
-int launch_am_t(bd_ctx* ctx, AmArgs a, int threads, bool replay_pass) {
+int launch_am_t(bd_ctx* ctx, AmArgs a, int threads, bool replay_pass, int* occ = nullptr) {
     const AmSmem lay(a.m, a.n_obs, a.neq, a.n_curv, a.s_cta, threads, P, CURV);
     if (lay.total > 227 * 1024) return fail(ctx, BD_ERR_VALUE, "AM kernel needs %zu B of shared memory", lay.total);
     raise_smem(am_kernel<P, CURV, MT, NPT, TPB>, lay.total);
+    if (occ) {   // occupancy query only (lane-mapping choice)
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, am_kernel<P, CURV, MT, NPT, TPB>, threads, lay.total) !=
+            cudaSuccess) {
+            cudaGetLastError();
+            *occ = 0;
+        }
+        return 0;
+    }
     dim3 grid((a.B + a.s_cta - 1) / a.s_cta, ctx->S);
     if (!replay_pass) a.replay = nullptr;
     std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
@@ -269,23 +267,20 @@ int launch_am_t(bd_ctx* ctx, AmArgs a, int threads, bool replay_pass) {
     return 0;
 }
 
-int launch_am(bd_ctx* ctx, AmArgs a, bool replay_pass) {
-    const long total = (long)a.B * ctx->S;
-    const int P = pick_lanes(ctx, total);
-    int threads = ctx->opt_spc ? ctx->opt_spc * P : (P == 32 ? 64 : 128);
-    if (P == 64 && threads % 64) threads = 128;
-    if (threads % 32 || threads > 256 || threads < 32) return fail(ctx, BD_ERR_VALUE, "bad samples_per_cta");
+int dispatch_am(bd_ctx* ctx, AmArgs a, int P, int threads, bool replay_pass, int* occ) {
     a.s_cta = threads / P;
     const bool curv = a.n_curv > 0;
     const int dflt = P == 32 ? 64 : 128;
     // compile-time shapes of the BASELINE configs (m = 100; 10 or 50 obstacles), default CTA size
     const bool fixed = !curv && a.m == 100 && threads == dflt;
-#define AM_CASE(PP)                                                                                      \
-    case PP:                                                                                             \
-        if (fixed && a.n_obs == 10) return launch_am_t<PP, false, 100, 5, (PP == 32 ? 64 : 128)>(ctx, a, threads, replay_pass); \
-        if (fixed && a.n_obs == 50) return launch_am_t<PP, false, 100, 25, (PP == 32 ? 64 : 128)>(ctx, a, threads, replay_pass); \
-        return curv ? launch_am_t<PP, true>(ctx, a, threads, replay_pass)                                \
-                    : launch_am_t<PP, false>(ctx, a, threads, replay_pass);
+#define AM_CASE(PP)                                                                                          \
+    case PP:                                                                                                 \
+        if (fixed && a.n_obs == 10)                                                                          \
+            return launch_am_t<PP, false, 100, 5, (PP == 32 ? 64 : 128)>(ctx, a, threads, replay_pass, occ);  \
+        if (fixed && a.n_obs == 50)                                                                          \
+            return launch_am_t<PP, false, 100, 25, (PP == 32 ? 64 : 128)>(ctx, a, threads, replay_pass, occ); \
+        return curv ? launch_am_t<PP, true>(ctx, a, threads, replay_pass, occ)                               \
+                    : launch_am_t<PP, false>(ctx, a, threads, replay_pass, occ);
     switch (P) {
         AM_CASE(4)
         AM_CASE(8)
@@ -295,6 +290,47 @@ int launch_am(bd_ctx* ctx, AmArgs a, bool replay_pass) {
         default: return fail(ctx, BD_ERR_VALUE, "lanes_per_sample must be 4, 8, 16, 32 or 64");
     }
 #undef AM_CASE
+}
+
+int default_threads(bd_ctx* ctx, int P) {
+    int threads = ctx->opt_spc ? ctx->opt_spc * P : (P == 32 ? 64 : 128);
+    if (P == 64 && threads % 64) threads = 128;
+    return threads;
+}
+
+// Lane mapping from a wave model: for each mapping, rounds = ceil(warps / resident warp slots)
+// (slots from the occupancy API for the exact kernel instance and its shared memory) times the
+// per-round cost of one sample group -- its serial timestep sweep plus reduction overhead, in
+// units of one timestep (calibrated on B200, profiles/r01).  Small single-scene batches pick
+// the two-warp mapping, fleets P = 8, the 10 000 x 50-obstacle batch P = 16.
+int pick_lanes(bd_ctx* ctx, const AmArgs& a) {
+    if (ctx->opt_lanes) return ctx->opt_lanes;
+    const double total = (double)a.B * ctx->S;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+    const int cands[4] = {8, 16, 32, 64};
+    const double overhead[4] = {0.5, 0.7, 0.9, 1.0};
+    int best = 8;
+    double best_cost = 1e300;
+    for (int i = 0; i < 4; ++i) {
+        const int P = cands[i];
+        const int threads = default_threads(ctx, P);
+        int occ = 0;
+        if (dispatch_am(ctx, a, P, threads, false, &occ) != 0 || occ <= 0) continue;
+        const double slots = (double)occ * sms * (threads / 32);
+        const double warps = total * P / 32.0;
+        const double rounds = std::ceil(warps / slots);
+        const double cost = rounds * (std::ceil((double)a.m / P) + overhead[i]);
+        if (cost < best_cost) { best_cost = cost; best = P; }
+    }
+    return best;
+}
+
+int launch_am(bd_ctx* ctx, AmArgs a, bool replay_pass) {
+    const int P = pick_lanes(ctx, a);
+    const int threads = default_threads(ctx, P);
+    if (threads % 32 || threads > 256 || threads < 32) return fail(ctx, BD_ERR_VALUE, "bad samples_per_cta");
+    return dispatch_am(ctx, a, P, threads, replay_pass, nullptr);
 }
 
 int require_solver(bd_ctx* ctx, bool need_stage1) {
