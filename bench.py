@@ -169,6 +169,40 @@ def cem_latency(device: int, cycles: int = 30):
                       "host-visible best xi via solve_bilevel (numpy Generator draws, H2D+D2H included)"}
 
 
+def dense_config4(device: int, steps: int = 3):
+    """BASELINE config 4 on one GPU: one scene, B = 10 000 samples x 50 obstacles, one full CEM
+    cycle (4 iterations, 100 AM iterations) per step, device Philox draws."""
+    import torch
+    import paper_2212_02224_b200 as bd
+    from paper_2212_02224_b200.fleet import FleetPlanner, initial_distribution
+    from paper_2212_02224_b200.scenes import HighwayRecipe, highway_scene
+    basis = bd.build_basis(10, M, T, "bernstein")
+    cfg = bd.BiLevelConfig(10_000, N_CONS, N_ELITE, N_CEM, 0.7, 0.9, 1.0)
+    fp = FleetPlanner(basis, bd.TrackingWeights(), bd.ParamLayout(4), bd.ProjectionConfig(1.0, AM_ITERS, 1e-3), 50,
+                      cfg, device=device)
+    sc = highway_scene(0, HighwayRecipe(density=3.0, vehicle_count=80, n_obs=50, obstacle_range=250.0))
+    fp.set_scenes([sc])
+    mean, cov = initial_distribution(sc)
+    m_t = torch.tensor(mean[None], dtype=torch.float64, device=device)
+    c_t = torch.tensor(cov[None], dtype=torch.float64, device=device)
+    stream = torch.cuda.current_stream(device)
+    fp.context.set_stream(stream.cuda_stream)
+    outs = {"best_cost": torch.zeros(1, dtype=torch.float64, device=device),
+            "iterations_done": torch.zeros(1, dtype=torch.int32, device=device)}
+    fp.plan_device(1, 0, m_t, c_t, outs)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for k in range(steps):
+        fp.plan_device(1, 1 + k, m_t, c_t, outs)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    assert int(outs["iterations_done"][0]) == N_CEM
+    return {"value": 10_000 * N_CEM / (ms / 1e3), "unit": "trajectories/s", "cycle_ms": ms,
+            "config": "1 scene, B=10000, 50 obstacles, 4 CEM iterations, 100 AM iterations (1 GPU)"}
+
+
 def run_b200(args, rank: int, world: int, dist):
     import torch
 
@@ -284,6 +318,7 @@ def run_b200(args, rank: int, world: int, dist):
     }
     if world == 1:
         line["cem_cycle_latency"] = cem_latency(dev)
+        line["dense_config4"] = dense_config4(dev)
         ref, _ = cpu_reference(steps=2, warmup=1)
         line["cpu_baseline"] = ref
     print(json.dumps(line), flush=True)
