@@ -13,7 +13,8 @@ from ctypes import POINTER, c_char_p, c_double, c_int, c_int64, c_uint64, c_void
 
 import numpy as np
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libbilevel_b200.so")
+LIB_PATH = os.environ.get("BD_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib",
+                                                           "libbilevel_b200.so")   # BD_LIB_PATH: tuning builds
 
 BD_OK, BD_ERR_VALUE, BD_ERR_STRUCTURE, BD_ERR_NUMERICAL, BD_ERR_CUDA, BD_ERR_STATE = 0, -1, -2, -3, -4, -5
 

@@ -170,8 +170,6 @@ __device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float
         // velocity / acceleration polar split (pkg/projection.py:119-122) in unit-vector form
         const float dv2 = fmaf(XD, XD, YD * YD);
         const float da2 = fmaf(XDD, XDD, YDD * YDD);
-        // fp32 range guard: |x| beyond 1e18 m (or a non-finite derivative) cannot be swept in fp32
-        ovf |= !(fmaxf(fabsf(X), fabsf(Y)) < 1e18f && dv2 < 3e38f && da2 < 3e38f);
         const float iv = dv2 > 0.f ? rsqrtf(dv2) : 0.f;
         const float ia = da2 > 0.f ? rsqrtf(da2) : 0.f;
         const float dv = dv2 * iv, da = da2 * ia;
@@ -243,6 +241,9 @@ __device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float
         const float2 ro = make_float2(L.a * rox, fmaf(L.b, roy, up - lo));
         // back-projection g += Wd^T r_v + Wdd^T r_a + W^T r_o (+ lane); the basis row is re-read
         // from shared memory rather than held across the clip/obstacle section (register budget)
+#if BD_AM_RELOAD_W
+        asm volatile("" ::: "memory");
+#endif
 #pragma unroll
         for (int q = 0; q < WROW / 4; ++q) {
             const float4 f = wr[q];
@@ -277,8 +278,14 @@ __device__ __forceinline__ void pair_sync() {
     asm volatile("bar.sync %0, 64;" ::"r"(1 + (int)(threadIdx.x >> 6)) : "memory");
 }
 
+#ifndef BD_AM_RELOAD_W
+#define BD_AM_RELOAD_W 0
+#endif
+#ifndef BD_AM_MINB
+#define BD_AM_MINB 2       // x 256 threads: 128 registers per thread
+#endif
 template <int P, bool CURV, int MT = 0, int NPT = 0, int TPB = 0>
-__global__ void __launch_bounds__(256, 2) am_kernel(const AmArgs a) {
+__global__ void __launch_bounds__(256, BD_AM_MINB) am_kernel(const AmArgs a) {
     // P <= 32: a sample is a group of P lanes of one warp.  P == 64: a sample spans two warps
     // (latency mapping for small batches); each warp reduce-scatters its partial sums, the second
     // warp hands them to the first through shared memory and the first warp owns the update.
@@ -421,6 +428,9 @@ __global__ void __launch_bounds__(256, 2) am_kernel(const AmArgs a) {
                 s0 = fma(kr[NC / 2].x, su[ax * KROW + NC - 1], s0);
                 c[r] += s0 + s1;
                 bad |= !isfinite(c[r]);
+                // fp32 range of the sweep: Bernstein rows are a partition of unity, so |X| <= max|c|,
+                // |Xd| <= 4 max|c|, |Xdd| <= 15 max|c| on this basis; 1e17 keeps every square < 3e38
+                ovf |= !(fabs(c[r]) < 1e17);
                 sc[i] = static_cast<float>(c[r]);
             }
         }
