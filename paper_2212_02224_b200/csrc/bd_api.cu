@@ -72,7 +72,8 @@ struct bd_ctx {
     int S = 0, scene_obs = 0, obs_pad = 0, n_curv = 0;
     DevBuf obs, lim, bscene, curvf, ox64, oy64, lim64, curv64;
     // workspace
-    DevBuf w_xibar, w_b, w_mu, w_xi, w_res, w_cost, w_hist, w_itmax, w_iters, w_replay, w_conf, w_err, w_params, w_done;
+    DevBuf w_xibar, w_b, w_mu, w_xi, w_res, w_cost, w_hist, w_itmax, w_iters, w_replay, w_conf, w_err, w_params, w_done,
+        w_order;
     DevBuf stage[8];
     int n_stage = 0;
     std::vector<PendingCopy> pending;
@@ -934,7 +935,7 @@ int bd_rank_refit(bd_ctx* ctx, int S, int B, int dim, const double* resid, const
         return fail(ctx, BD_ERR_VALUE, "bad rank_refit call");
     if (!(n_elite <= n_cons && n_cons <= B) || n_elite < 1 || n_cons > 1024)
         return fail(ctx, BD_ERR_VALUE, "need 1 <= elites <= constraint_elites <= min(batch, 1024)");
-    if (B > 16384) return fail(ctx, BD_ERR_VALUE, "rank_refit supports at most 16384 samples per scene");
+    if (B > (1 << 24)) return fail(ctx, BD_ERR_VALUE, "batch too large");
     begin_call(ctx);
     int rc;
     const size_t tot = (size_t)S * B;
@@ -972,11 +973,12 @@ int bd_rank_refit(bd_ctx* ctx, int S, int B, int dim, const double* resid, const
     s.elite_aug = dea; s.stats = dst;
     s.best_index = ctx->c_best_idx.as<long long>(); s.best_params = ctx->c_best_p.as<double>();
     s.best_xi = ctx->c_best_xi.as<double>(); s.best_scal = ctx->c_best_s.as<double>();
-    int np2 = 1;
-    while (np2 < B) np2 <<= 1;
-    const size_t smem = rank_refit_smem(np2, n_cons, n_elite, dim);
+    CU(ctx->w_order.ensure(tot * 4));
+    rank_count_kernel<<<(unsigned)((tot + 7) / 8), 256, 0, ctx->stream>>>(dr, nullptr, S, B, ctx->w_order.as<int>());
+    ctx->launches++;
+    const size_t smem = rank_refit_smem(n_cons, n_elite, dim);
     raise_smem(rank_refit_kernel, smem);
-    rank_refit_kernel<<<S, 1024, smem, ctx->stream>>>(s, 0, np2);
+    rank_refit_kernel<<<S, 1024, smem, ctx->stream>>>(s, 0, ctx->w_order.as<int>());
     ctx->launches++;
     CU(cudaMemcpyAsync(mean, ctx->c_mean.p, (size_t)S * dim * 8, cudaMemcpyDefault, ctx->stream));
     CU(cudaMemcpyAsync(cov, ctx->c_cov.p, (size_t)S * dim * dim * 8, cudaMemcpyDefault, ctx->stream));
@@ -997,7 +999,7 @@ int bd_cem_cycle(bd_ctx* ctx, int S, const bd_cem_config* cfg, const double* ini
     if (!(cfg->n_elite <= cfg->n_cons && cfg->n_cons <= B) || cfg->n_elite < 1 || cfg->n_cons > 1024)
         return fail(ctx, BD_ERR_VALUE, "need elites <= constraint_elites <= batch_size (<= 1024 constraint elites)");
     if (!(cfg->eta > 0 && cfg->eta <= 1) || !(cfg->gamma > 0)) return fail(ctx, BD_ERR_VALUE, "bad eta / gamma");
-    if (B > 16384) return fail(ctx, BD_ERR_VALUE, "CEM batch above 16384 per scene is not supported by this build");
+    if (B > (1 << 24)) return fail(ctx, BD_ERR_VALUE, "batch too large");
     begin_call(ctx);
     const size_t tot = (size_t)S * B;
     const double *dz = nullptr, *dwarm = nullptr, *dm0, *dc0;
@@ -1037,9 +1039,8 @@ int bd_cem_cycle(bd_ctx* ctx, int S, const bd_cem_config* cfg, const double* ini
     s.best_xi = ctx->c_best_xi.as<double>(); s.best_scal = ctx->c_best_s.as<double>();
     cem_init_kernel<<<S, 64, 0, ctx->stream>>>(s, dm0, dc0);
     ctx->launches++;
-    int np2 = 1;
-    while (np2 < B) np2 <<= 1;
-    const size_t rsmem = rank_refit_smem(np2, cfg->n_cons, cfg->n_elite, dim);
+    CU(ctx->w_order.ensure(tot * 4));
+    const size_t rsmem = rank_refit_smem(cfg->n_cons, cfg->n_elite, dim);
     raise_smem(rank_refit_kernel, rsmem);
     S1Args s1{};
     s1.total = S * B; s1.B = B; s1.dim = dim; s1.neq = ctx->neq1; s1.m_seg = ctx->m_seg;
@@ -1058,8 +1059,10 @@ int bd_cem_cycle(bd_ctx* ctx, int S, const bd_cem_config* cfg, const double* ini
                                  ctx->w_xi.as<double>(), ctx->w_res.as<double>(), ctx->w_cost.as<double>(), nullptr,
                                  ctx->w_iters.as<int>(), ctx->w_conf.as<unsigned long long>())))
             return rc;
-        rank_refit_kernel<<<S, 1024, rsmem, ctx->stream>>>(s, it, np2);
-        ctx->launches++;
+        rank_count_kernel<<<(unsigned)((tot + 7) / 8), 256, 0, ctx->stream>>>(s.resid, s.err, S, B,
+                                                                             ctx->w_order.as<int>());
+        rank_refit_kernel<<<S, 1024, rsmem, ctx->stream>>>(s, it, ctx->w_order.as<int>());
+        ctx->launches += 2;
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(ctx, BD_ERR_CUDA, "CEM launch: %s", cudaGetErrorString(e));

@@ -196,20 +196,39 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
     return t;
 }
 
-// Dynamic shared memory of rank_refit_kernel (bytes); npow2 >= B and both powers of two.
-__host__ __device__ inline size_t rank_refit_smem(int npow2, int n_cons, int n_elite, int dim) {
-    int np2 = 1;
-    while (np2 < n_cons) np2 <<= 1;
+// Stable residual order by counting (np.argsort(kind="stable"), pkg/bilevel.py:131): one warp per
+// sample counts the keys that precede it, (key, index) lexicographic, and scatters the sample to
+// its rank.  O(B^2) comparisons, but spread over the whole GPU instead of a single CTA's sort.
+__global__ void __launch_bounds__(256) rank_count_kernel(const double* resid, const int* err, int S, int B,
+                                                         int* order) {
+    const int lane = threadIdx.x & 31;
+    const long gi = (long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (gi >= (long)S * B) return;
+    const int scene = (int)(gi / B), i = (int)(gi % B);
+    if (err && err[scene]) return;
+    const double* r = resid + (size_t)scene * B;
+    const unsigned long long ki = ordered_bits(r[i]);
+    int cnt = 0;
+    for (int j = lane; j < B; j += 32) {
+        const unsigned long long kj = ordered_bits(__ldg(r + j));
+        cnt += (kj < ki) || (kj == ki && j < i);
+    }
+    for (int o = 16; o >= 1; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane == 0) order[(size_t)scene * B + cnt] = i;
+}
+
+// Dynamic shared memory of rank_refit_kernel (bytes).
+__host__ __device__ inline size_t rank_refit_smem(int n_cons, int n_elite, int dim) {
     const int staged = n_elite <= 128 ? n_elite : 0;
-    return (size_t)npow2 * 12 + (size_t)np2 * 20 + (size_t)staged * dim * 8;
+    return (size_t)n_cons * (8 + 4 + 4 + 8) + (size_t)staged * dim * 8;
 }
 
 // rank_samples + update_distribution + IterationStats + best record for one CEM
-// iteration, one CTA (1024 threads) per scene.  The residual keys of the whole batch are
-// bitonic-sorted in shared memory (B <= 16384: 196 KB), the constraint elites re-sorted by
-// augmented cost, the q elite set-point vectors staged in shared memory and the weighted
-// mean / covariance reduced warp-parallel in fp64.
-__global__ void __launch_bounds__(1024) rank_refit_kernel(CemState s, int it, int npow2) {
+// iteration, one CTA (1024 threads) per scene, on the residual order produced by
+// rank_count_kernel.  The n constraint elites are ranked by augmented cost (ties by sample
+// index, np.lexsort((idx, aug))) by counting in shared memory, the q elite set-point vectors
+// staged in shared memory and the weighted mean / covariance reduced warp-parallel in fp64.
+__global__ void __launch_bounds__(1024) rank_refit_kernel(CemState s, int it, const int* order) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int scene = blockIdx.x;
     const int d = s.dim;
@@ -218,41 +237,34 @@ __global__ void __launch_bounds__(1024) rank_refit_kernel(CemState s, int it, in
         return;
     }
     const int n = s.n_cons, q = s.n_elite;
-    int np2 = 1;
-    while (np2 < n) np2 <<= 1;
-    // dynamic layout (rank_refit_smem): key | idx | key2 | idx2 | w | staged elite set-points
-    unsigned long long* key = reinterpret_cast<unsigned long long*>(smem);
-    int* idx = reinterpret_cast<int*>(key + npow2);
-    unsigned long long* key2 = reinterpret_cast<unsigned long long*>(idx + npow2);
-    int* idx2 = reinterpret_cast<int*>(key2 + np2);
-    double* w = reinterpret_cast<double*>(idx2 + np2);
-    double* pe = w + np2;                  // q <= 128 staged; larger q read from global
+    // dynamic layout (rank_refit_smem): key2 | cidx | idx2 | w | staged elite set-points
+    unsigned long long* key2 = reinterpret_cast<unsigned long long*>(smem);
+    int* cidx = reinterpret_cast<int*>(key2 + n);
+    int* idx2 = cidx + n;
+    double* w = reinterpret_cast<double*>(idx2 + n);
+    double* pe = w + n;                    // q <= 128 staged; larger q read from global
     __shared__ double red[32];
     __shared__ double mu_new[MAX_DIM];
     __shared__ double cnew[MAX_DIM * MAX_DIM];
     const size_t base = (size_t)scene * s.B;
-    for (int i = threadIdx.x; i < npow2; i += blockDim.x) {
-        key[i] = i < s.B ? ordered_bits(s.resid[base + i]) : ~0ull;
-        idx[i] = i < s.B ? i : 0x7fffffff;
-    }
-    __syncthreads();
-    block_bitonic_sort(key, idx, npow2);
+    const int* ord = order + base;
     // constraint elites: first n of the stable residual order; aug = cost + w r
-    for (int i = threadIdx.x; i < np2; i += blockDim.x) {
-        if (i < n) {
-            const int j = idx[i];
-            const double aug = s.cost[base + j] + s.w_res * s.resid[base + j];
-            key2[i] = ordered_bits(aug);
-            idx2[i] = j;
-            w[i] = aug;
-            if (s.cons_idx) s.cons_idx[(size_t)scene * n + i] = j;
-        } else {
-            key2[i] = ~0ull;
-            idx2[i] = 0x7fffffff;
-        }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int j = ord[i];
+        key2[i] = ordered_bits(s.cost[base + j] + s.w_res * s.resid[base + j]);
+        cidx[i] = j;
+        if (s.cons_idx) s.cons_idx[(size_t)scene * n + i] = j;
     }
     __syncthreads();
-    block_bitonic_sort(key2, idx2, np2);
+    // rank among the constraint elites by (aug, sample index), scatter
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const unsigned long long ki = key2[i];
+        const int ji = cidx[i];
+        int rk = 0;
+        for (int k = 0; k < n; ++k) rk += (key2[k] < ki) || (key2[k] == ki && cidx[k] < ji);
+        idx2[rk] = ji;
+    }
+    __syncthreads();
     // elite weights exp(-(aug - min aug)/gamma), uniform fallback (pkg/bilevel.py:163-172)
     const int j0 = idx2[0];
     const double amin = s.cost[base + j0] + s.w_res * s.resid[base + j0];
@@ -313,9 +325,9 @@ __global__ void __launch_bounds__(1024) rank_refit_kernel(CemState s, int it, in
     if (threadIdx.x == 0) {
         // IterationStats (pkg/bilevel.py:282-292)
         const int B = s.B;
-        const double rmin = s.resid[base + idx[0]], rmax = s.resid[base + idx[B - 1]];
-        const double rmed = (B & 1) ? s.resid[base + idx[B / 2]]
-                                    : 0.5 * (s.resid[base + idx[B / 2 - 1]] + s.resid[base + idx[B / 2]]);
+        const double rmin = s.resid[base + ord[0]], rmax = s.resid[base + ord[B - 1]];
+        const double rmed = (B & 1) ? s.resid[base + ord[B / 2]]
+                                    : 0.5 * (s.resid[base + ord[B / 2 - 1]] + s.resid[base + ord[B / 2]]);
         double tr = 0.0;
         for (int i = 0; i < d; ++i) tr += cnew[i * d + i];   // symmetrisation keeps the diagonal
         if (s.stats) {
