@@ -189,6 +189,35 @@ int bd_cem_cycle(bd_ctx* ctx, int n_scenes, const bd_cem_config* cfg, const doub
                  double* best_params, double* best_xi, double* best_cost, double* best_residual,
                  double* best_aug, double* stats, double* final_mean, double* final_cov, int* iterations_done);
 
+/* ------------------------------------------------------------------ scene construction / control emission
+ * the steps either side of the path, on the device.                          */
+
+/* Planner-side constants of build_scene (PlannerEnvConfig, pkg/planners.py:40-87). */
+typedef struct bd_env {
+    int max_obstacles;          /* obstacle rows per scene (must equal the projection's n_obs)      */
+    double obstacle_range;      /* longitudinal neighbour filter [m]                                */
+    double wheelbase;           /* ego_flat_state yaw rate                                          */
+    double v_max, a_max, kappa_max, c_max, v_min;
+    double other_length, other_width;   /* neighbour footprint for combined_ellipse (5 x 2 m)      */
+} bd_env;
+
+/* build_scene + ego_flat_state (pkg/planners.py:99-160) and observe (pkg/highway.py:208-246) for S
+ * worlds, writing the scenes straight into the context (replaces bd_set_scenes).
+ * ego S x 8 (x, y, psi, v, accel, steer, length, width); veh S x n_veh_max x 5 (x, y, psi, v,
+ * lateral_rate) in world.neighbors order; n_veh S; road S x 2 (lane_count, lane_width);
+ * times m (basis.times).  Optional outputs: obstacles S x n_obs x m (x, y), initial states S x 6,
+ * limits S x 9 (a b v_min v_max a_max kappa_max c_max y_lb y_ub), observations S x 55. */
+int bd_build_scenes(bd_ctx* ctx, int n_scenes, int n_veh_max, const double* ego, const double* veh,
+                    const int* n_veh, const double* road, const bd_env* env, const double* times, double* ox_out,
+                    double* oy_out, double* b0_out, double* limits_out, double* observations);
+
+/* controls_on_grid -> flat_to_controls (pkg/planners.py:209-216, pkg/basis.py:206-234): the basis
+ * derivative rows at the n_ctrl control instants (matrices_at), then per trajectory the clipped
+ * (accel, steer) sequence; singular[i] = 1 where the speed drops to eps_v (SpeedSingularity). */
+int bd_set_control_grid(bd_ctx* ctx, int n_ctrl, const double* Wd_ctrl, const double* Wdd_ctrl, double wheelbase,
+                        double a_max, double steer_limit, double eps_v);
+int bd_controls(bd_ctx* ctx, int count, const double* xi, double* accel, double* steer, int* singular);
+
 /* ------------------------------------------------------------------ CVAE warm start
  * Decoder MLP of the paper (not in the reference package):
  * (obs 55 + z 2) -> 1024 -> 1024 -> 1024 -> 1024 -> 256 -> dim, BatchNorm folded

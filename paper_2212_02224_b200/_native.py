@@ -49,6 +49,9 @@ SIGNATURES = {
     "bd_rank_refit": (c_int, [_P, c_int, c_int, c_int, _P, _P, _P, c_int, c_int, c_double, c_double, c_double, _P, _P,
                               _P, _P, _P, _P]),
     "bd_cem_cycle": (c_int, [_P, c_int, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "bd_build_scenes": (c_int, [_P, c_int, c_int, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "bd_set_control_grid": (c_int, [_P, c_int, _P, _P, c_double, c_double, c_double, c_double]),
+    "bd_controls": (c_int, [_P, c_int, _P, _P, _P, _P]),
     "bd_cvae_set_weights": (c_int, [_P, c_int, _P, _P, _P]),
     "bd_cvae_decode": (c_int, [_P, c_int, _P, _P, _P]),
 }
@@ -65,6 +68,13 @@ class CemConfig(ctypes.Structure):
     _fields_ = [("batch", c_int), ("n_cons", c_int), ("n_elite", c_int), ("iterations", c_int),
                 ("am_iters", c_int), ("eta", c_double), ("gamma", c_double), ("residual_weight", c_double),
                 ("tol", c_double), ("seed", c_uint64), ("scene_offset", c_int)]
+
+
+class Env(ctypes.Structure):
+    """bd_env: PlannerEnvConfig fields used by build_scene (pkg/planners.py:40-87)."""
+    _fields_ = [("max_obstacles", c_int), ("obstacle_range", c_double), ("wheelbase", c_double),
+                ("v_max", c_double), ("a_max", c_double), ("kappa_max", c_double), ("c_max", c_double),
+                ("v_min", c_double), ("other_length", c_double), ("other_width", c_double)]
 
 
 _lib = None

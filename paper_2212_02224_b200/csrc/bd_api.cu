@@ -15,6 +15,7 @@
 #include "cem_kernels.cuh"
 #include "aux_kernels.cuh"
 #include "cvae_kernel.cuh"
+#include "scene_kernels.cuh"
 
 using namespace bd;
 
@@ -80,6 +81,10 @@ struct bd_ctx {
     bool host_out = false;
     // CEM state
     DevBuf c_mean, c_cov, c_L, c_done, c_best_idx, c_best_p, c_best_xi, c_best_s, c_stats, c_cons, c_elite, c_eaug;
+    // control grid
+    int n_ctrl = 0;
+    double ctrl_wb = 0, ctrl_amax = 0, ctrl_steer = 0, ctrl_eps = 0;
+    DevBuf ctrl_wd, ctrl_wdd, w_sing, w_accel, w_steer;
     // CVAE
     std::vector<int> cvae_dims;
     std::vector<DevBuf*> cvae_w, cvae_b;
@@ -1091,6 +1096,112 @@ int bd_cem_cycle(bd_ctx* ctx, int S, const bd_cem_config* cfg, const double* ini
         }
     if (any_host) CU(cudaStreamSynchronize(ctx->stream));
     return 0;
+}
+
+// ------------------------------------------------------------------ scenes from worlds, controls
+int bd_build_scenes(bd_ctx* ctx, int S, int n_veh_max, const double* ego, const double* veh, const int* n_veh,
+                    const double* road, const bd_env* env, const double* times, double* ox_out, double* oy_out,
+                    double* b0_out, double* limits_out, double* observations) {
+    if (!ctx || !env) return BD_ERR_VALUE;
+    if (!ctx->m) return fail(ctx, BD_ERR_STATE, "basis not set");
+    const int m = ctx->m, n_obs = env->max_obstacles;
+    if (S < 1 || n_veh_max < 0 || n_obs < 0 || !ego || !n_veh || !road || !times || (n_veh_max > 0 && !veh))
+        return fail(ctx, BD_ERR_VALUE, "bad build_scenes arguments");
+    if (n_veh_max > 4096) return fail(ctx, BD_ERR_VALUE, "at most 4096 neighbours per world");
+    begin_call(ctx);
+    int rc;
+    const double *de, *dv, *dr, *dt;
+    const int* dn;
+    if ((rc = stage_in(ctx, ego, (size_t)S * 8, &de))) return rc;
+    if ((rc = stage_in(ctx, veh, (size_t)S * n_veh_max * 5, &dv))) return rc;
+    if ((rc = stage_in(ctx, n_veh, (size_t)S, &dn))) return rc;
+    if ((rc = stage_in(ctx, road, (size_t)S * 2, &dr))) return rc;
+    if ((rc = stage_in(ctx, times, (size_t)m, &dt))) return rc;
+    const int neq = ctx->neq ? ctx->neq : 6;
+    const int nop = (n_obs + 1) / 2 * 2;
+    const size_t no = (size_t)S * n_obs * m;
+    CU(ctx->obs.ensure(((size_t)S * nop * m * 2 + 4) * sizeof(float)));
+    CU(ctx->lim.ensure((size_t)S * sizeof(SceneLim)));
+    CU(ctx->bscene.ensure((size_t)S * neq * 8));
+    CU(ctx->lim64.ensure((size_t)S * 9 * 8));
+    CU(ctx->ox64.ensure(no ? no * 8 : 8));
+    CU(ctx->oy64.ensure(no ? no * 8 : 8));
+    CU(ctx->w_err.ensure((size_t)S * 4));
+    CU(cudaMemsetAsync(ctx->w_err.p, 0, (size_t)S * 4, ctx->stream));
+    double *db0, *dobs;
+    if ((rc = stage_out(ctx, b0_out, (size_t)S * 6, ctx->stage[6], &db0))) return rc;
+    if ((rc = stage_out(ctx, observations, (size_t)S * OBS_DIM, ctx->stage[7], &dobs))) return rc;
+    SceneBuildArgs a{};
+    a.S = S; a.n_veh_max = n_veh_max; a.n_obs = n_obs; a.n_pad = nop; a.m = m; a.neq = neq;
+    a.range = env->obstacle_range; a.wheelbase = env->wheelbase; a.v_max = env->v_max; a.a_max = env->a_max;
+    a.k_max = env->kappa_max; a.c_max = env->c_max; a.v_min = env->v_min; a.other_len = env->other_length;
+    a.other_wid = env->other_width;
+    a.ego = de; a.veh = dv; a.n_veh = dn; a.road = dr; a.times = dt;
+    a.tile = ctx->obs.as<float>(); a.lim = ctx->lim.as<SceneLim>(); a.bscene = ctx->bscene.as<double>();
+    a.ox64 = ctx->ox64.as<double>(); a.oy64 = ctx->oy64.as<double>(); a.lim64 = ctx->lim64.as<double>();
+    a.b0_out = db0; a.observation = dobs;
+    const size_t smem = (size_t)n_veh_max * 8 + (size_t)(n_obs + OBS_NEIGHBORS) * 4 + (size_t)n_veh_max * 2 + 16;
+    raise_smem(build_scene_kernel, smem);
+    build_scene_kernel<<<S, 128, smem, ctx->stream>>>(a);
+    ctx->launches++;
+    // optional host-facing copies of the fp64 scene
+    struct Out { void* dst; const void* src; size_t bytes; };
+    const Out outs[] = {{ox_out, ctx->ox64.p, no * 8}, {oy_out, ctx->oy64.p, no * 8},
+                        {limits_out, ctx->lim64.p, (size_t)S * 9 * 8}};
+    for (const Out& o : outs)
+        if (o.dst && o.bytes) {
+            if (is_device_ptr(o.dst)) {
+                CU(cudaMemcpyAsync(o.dst, o.src, o.bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+            } else {
+                ctx->pending.push_back({o.dst, o.src, o.bytes});
+                ctx->host_out = true;
+            }
+        }
+    ctx->S = S;
+    ctx->scene_obs = n_obs;
+    ctx->obs_pad = nop;
+    ctx->n_curv = 0;
+    return finish_call(ctx, false, 0);
+}
+
+int bd_set_control_grid(bd_ctx* ctx, int n_ctrl, const double* wd, const double* wdd, double wheelbase,
+                        double a_max, double steer_limit, double eps_v) {
+    if (!ctx || n_ctrl < 1 || !wd || !wdd) return BD_ERR_VALUE;
+    begin_call(ctx);
+    CU(ctx->ctrl_wd.ensure((size_t)n_ctrl * NC * 8));
+    CU(ctx->ctrl_wdd.ensure((size_t)n_ctrl * NC * 8));
+    CU(cudaMemcpy(ctx->ctrl_wd.p, wd, (size_t)n_ctrl * NC * 8, cudaMemcpyDefault));
+    CU(cudaMemcpy(ctx->ctrl_wdd.p, wdd, (size_t)n_ctrl * NC * 8, cudaMemcpyDefault));
+    ctx->n_ctrl = n_ctrl;
+    ctx->ctrl_wb = wheelbase;
+    ctx->ctrl_amax = a_max;
+    ctx->ctrl_steer = steer_limit;
+    ctx->ctrl_eps = eps_v;
+    return 0;
+}
+
+int bd_controls(bd_ctx* ctx, int count, const double* xi, double* accel, double* steer, int* singular) {
+    if (!ctx) return BD_ERR_VALUE;
+    if (!ctx->n_ctrl) return fail(ctx, BD_ERR_STATE, "control grid not set");
+    if (count < 1 || !xi || !accel || !steer || !singular) return fail(ctx, BD_ERR_VALUE, "bad controls call");
+    begin_call(ctx);
+    int rc;
+    const size_t n = (size_t)count * ctx->n_ctrl;
+    const double* dxi;
+    double *da, *ds;
+    int* dsg;
+    if ((rc = stage_in(ctx, xi, (size_t)count * NX, &dxi))) return rc;
+    if ((rc = stage_out(ctx, accel, n, ctx->w_accel, &da))) return rc;
+    if ((rc = stage_out(ctx, steer, n, ctx->w_steer, &ds))) return rc;
+    if ((rc = stage_out_req(ctx, singular, (size_t)count, ctx->w_sing, &dsg))) return rc;
+    CU(cudaMemsetAsync(dsg, 0, (size_t)count * 4, ctx->stream));
+    ControlArgs c{};
+    c.count = count; c.n_ctrl = ctx->n_ctrl; c.wd = ctx->ctrl_wd.as<double>(); c.wdd = ctx->ctrl_wdd.as<double>();
+    c.xi = dxi; c.wheelbase = ctx->ctrl_wb; c.a_max = ctx->ctrl_amax; c.steer_limit = ctx->ctrl_steer;
+    c.eps_v = ctx->ctrl_eps; c.accel = da; c.steer = ds; c.singular = dsg;
+    controls_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(c);
+    ctx->launches++;
+    return finish_call(ctx, false, 0);
 }
 
 // ------------------------------------------------------------------ CVAE decoder

@@ -265,13 +265,68 @@ def gen_scenes():
     print("scenes written")
 
 
+def gen_worlds():
+    """World snapshots after a few simulator steps (nonzero heading / steer / lane changes) with the
+    reference's build_scene (pkg/planners.py:116-160), ego_flat_state (:99-113) and observe
+    (pkg/highway.py:208-246) outputs, plus controls_on_grid (pkg/planners.py:209-216) of the
+    projected trajectories of lower_c1_s0."""
+    from bilevel_drive.basis import flat_to_controls, SpeedSingularity
+    from bilevel_drive.highway import observe, step
+    from bilevel_drive.planners import ego_flat_state
+    out = {}
+    k = 0
+    for lanes, dens, veh, seed, nsteps, nobs, rng_ in ((4, 2.0, 24, 0, 0, 10, 120.0), (4, 2.0, 24, 1, 17, 10, 120.0),
+                                                       (2, 1.0, 12, 2, 25, 10, 120.0), (4, 3.0, 80, 3, 9, 50, 250.0),
+                                                       (3, 1.5, 30, 4, 31, 10, 60.0), (2, 0.4, 3, 5, 5, 10, 120.0)):
+        world = spawn_world(ScenarioConfig(RoadSpec(lane_count=lanes), density=dens, vehicle_count=veh, seed=seed))
+        for t in range(nsteps):
+            step(world, 0.8 * np.sin(0.3 * t), 0.03 * np.cos(0.2 * t))
+        env = env_for(n_obs=nobs, obstacle_range=rng_)
+        basis = build_basis(10, 100, 5.0, "bernstein")
+        sc = build_scene(world, env, basis.times)
+        e = world.ego
+        out[f"w{k}_ego"] = np.array([e.x, e.y, e.psi, e.v, e.accel, e.steer, e.length, e.width])
+        out[f"w{k}_veh"] = np.array([[v.x, v.y, v.psi, v.v, v.lateral_rate] for v in world.neighbors])
+        out[f"w{k}_road"] = np.array([world.road.lane_count, world.road.lane_width])
+        out[f"w{k}_env"] = np.array([nobs, rng_, env.wheelbase])
+        out[f"w{k}_ox"], out[f"w{k}_oy"] = sc.spec.obstacles_x, sc.spec.obstacles_y
+        out[f"w{k}_b0"] = sc.initial_state
+        assert np.array_equal(sc.initial_state, ego_flat_state(world, env.wheelbase))
+        out[f"w{k}_lim"] = scene_arrays(sc)["limits"]
+        out[f"w{k}_obs"] = observe(world)
+        k += 1
+    out["n_worlds"] = k
+    # control emission on the simulator grid (dt = 0.1 s over the 5 s horizon, wheelbase 2.5)
+    g = np.load(os.path.join(OUT, "lower_c1_s0.npz"))
+    basis = build_basis(10, 100, 5.0, "bernstein")
+    times = np.arange(int(5.0 / 0.1)) * 0.1
+    env = env_for()
+    acc, ste, sing = [], [], []
+    from bilevel_drive.basis import TrajectoryCoeffs
+    xis = np.concatenate([g["xi"], g["xi_bar"], np.zeros((22, 1))], axis=1)
+    for j in range(xis.shape[1]):
+        try:
+            c = flat_to_controls(basis, TrajectoryCoeffs.from_stacked(xis[:, j]), env.wheelbase, times=times)
+            acc.append(np.clip(c.accel, -env.a_max, env.a_max))
+            ste.append(np.clip(c.delta, -env.steer_limit, env.steer_limit))
+            sing.append(0)
+        except SpeedSingularity:
+            acc.append(np.full(len(times), np.nan))
+            ste.append(np.full(len(times), np.nan))
+            sing.append(1)
+    out.update(ctrl_xi=xis.T.copy(), ctrl_accel=np.array(acc), ctrl_steer=np.array(ste), ctrl_singular=np.array(sing),
+               ctrl_times=times, ctrl_limits=np.array([env.wheelbase, env.a_max, env.steer_limit]))
+    np.savez_compressed(os.path.join(OUT, "worlds.npz"), **out)
+    print(f"worlds written ({k} worlds, {xis.shape[1]} control sets, {sum(sing)} singular)")
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", nargs="*", default=None)
     a = ap.parse_args()
     os.makedirs(OUT, exist_ok=True)
     jobs = {"basis": gen_basis, "lower": gen_lower, "scenes": gen_scenes, "cem_small": gen_cem_small,
-            "cem_c2": gen_cem_c2}
+            "cem_c2": gen_cem_c2, "worlds": gen_worlds}
     for name, fn in jobs.items():
         if a.only is None or name in a.only:
             fn()
