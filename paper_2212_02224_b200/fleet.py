@@ -94,6 +94,35 @@ class FleetPlanner:
                           out.best_aug, out.stats, out.final_mean, out.final_cov, out.iterations_done)
         return out
 
+    def plan_cycle(self, worlds, env, emitter, seed: int = 0, scene_offset: int = 0, sigma_offset: float = 1.5,
+                   sigma_speed: float = 3.0):
+        """MPCBiLevelPlanner.plan_cycle for a batch of worlds (pkg/planners.py:200-216, 276-306):
+        device scene build -> device CEM cycle -> device control emission of each best trajectory.
+        Returns (accels, steers, singular, FleetResult); world arrays in, controls out."""
+        from .worlds import build_scenes
+        build_scenes(self.context, self.solver.basis, worlds, env)
+        self._scenes_key = ("worlds", id(worlds))
+        self.solver.projector._scene_key = None
+        ms = self.layout.m_seg
+        # BasePlanner.initial_distribution (pkg/planners.py:218-231): nearest lane centre, current speed
+        y0, v0 = worlds.ego[:, 1], worlds.ego[:, 3]
+        lanes, lw = worlds.road[:, 0].astype(int), worlds.road[:, 1]
+        lane_y = np.array([(np.arange(n) * w)[np.argmin(np.abs(np.arange(n) * w - y))] for n, w, y in zip(lanes, lw, y0)])
+        S = worlds.size
+        mean = np.concatenate([np.repeat(lane_y[:, None], ms, 1), np.repeat(np.abs(v0)[:, None], ms, 1)], axis=1)
+        cov = np.repeat(np.diag(np.concatenate([np.full(ms, sigma_offset ** 2), np.full(ms, sigma_speed ** 2)]))[None],
+                        S, axis=0)
+        dim, N, n2 = self.layout.dim, self.config.iterations, 2 * self.solver.basis.num_coeffs
+        out = FleetResult(np.zeros(S, np.int64), np.zeros((S, dim)), np.zeros((S, n2)), np.zeros(S), np.zeros(S),
+                          np.zeros(S), np.zeros((S, N, 6)), np.zeros((S, dim)), np.zeros((S, dim, dim)),
+                          np.zeros(S, np.int32))
+        cfg = self.cem_config(seed, scene_offset)
+        self.context.call("bd_cem_cycle", S, ctypes.byref(cfg), f64(mean), f64(cov), None, None, out.best_index,
+                          out.best_params, out.best_xi, out.best_cost, out.best_residual, out.best_aug, out.stats,
+                          out.final_mean, out.final_cov, out.iterations_done)
+        acc, ste, sing = emitter.emit(out.best_xi)
+        return acc, ste, sing, out
+
     def plan_device(self, S: int, seed: int, init_mean, init_cov, outputs: dict, scene_offset: int = 0):
         """Asynchronous variant on device buffers (torch tensors): scenes must already be set."""
         cfg = self.cem_config(seed, scene_offset)

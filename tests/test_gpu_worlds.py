@@ -70,3 +70,31 @@ def test_control_emission_matches_reference():
     ok = ~sing
     np.testing.assert_allclose(acc[ok], g["ctrl_accel"][ok], rtol=1e-10, atol=1e-10)
     np.testing.assert_allclose(ste[ok], g["ctrl_steer"][ok], rtol=1e-10, atol=1e-12)
+
+
+def test_fleet_plan_cycle_from_worlds():
+    import paper_2212_02224_b200 as bd
+    from paper_2212_02224_b200.fleet import FleetPlanner
+    from paper_2212_02224_b200.worlds import ControlEmitter, PlannerEnv, WorldBatch
+    g = load("worlds")
+    ks = [0, 1, 2, 4, 5]                     # the 10-obstacle worlds
+    n_max = max(g[f"w{k}_veh"].shape[0] for k in ks)
+    veh = np.zeros((len(ks), n_max, 5))
+    for i, k in enumerate(ks):
+        veh[i, : g[f"w{k}_veh"].shape[0]] = g[f"w{k}_veh"]
+    worlds = WorldBatch(np.stack([g[f"w{k}_ego"] for k in ks]), veh,
+                        np.array([g[f"w{k}_veh"].shape[0] for k in ks], np.int32),
+                        np.stack([g[f"w{k}_road"] for k in ks]))
+    basis = bd.build_basis(10, 100, 5.0, "bernstein")
+    fp = FleetPlanner(basis, bd.TrackingWeights(), bd.ParamLayout(4), bd.ProjectionConfig(1.0, 50, 1e-3), 10,
+                      bd.BiLevelConfig(500, 100, 50, 3, 0.7, 0.9, 1.0))
+    em = ControlEmitter(fp.context, basis, 5.0, 0.1, PlannerEnv())
+    acc, ste, sing, res = fp.plan_cycle(worlds, PlannerEnv(), em, seed=3)
+    assert acc.shape == (5, 50) and np.all(res.iterations_done == 3)
+    assert not sing.any() and np.all(np.abs(acc) <= 6.0) and np.all(np.isfinite(ste))
+    # same as planning each world alone (scene_offset keeps the Philox stream per world)
+    for i in range(5):
+        one = WorldBatch(worlds.ego[i:i + 1], worlds.veh[i:i + 1], worlds.n_veh[i:i + 1], worlds.road[i:i + 1])
+        a1, s1, _, r1 = fp.plan_cycle(one, PlannerEnv(), em, seed=3, scene_offset=i)
+        assert r1.best_index[0] == res.best_index[i]
+        np.testing.assert_array_equal(a1[0], acc[i])
