@@ -266,23 +266,30 @@ def run_b200(args, rank: int, world: int, dist):
     traj = S * world * N_CEM * B_CEM * args.steps
     value = traj / (t_max / 1e3)
 
-    # end to end through the public API: host scenes in, host results out, every step
-    e2e_scenes = [highway_scene(10_000 + rank * S + j) for j in range(S)]
-    planner.plan(e2e_scenes, seed=1)       # warm the host path
+    # end to end through the public API: the planning cycle of MPCBiLevelPlanner.plan_cycle for
+    # S worlds -- host world state in (H2D), device scene build, CEM cycle, control emission,
+    # host controls + best records out (D2H), every step
+    from paper_2212_02224_b200.scenes import spawn_worlds
+    from paper_2212_02224_b200.worlds import ControlEmitter, PlannerEnv
+    worlds = spawn_worlds(range(10_000 + rank * S, 10_000 + (rank + 1) * S))
+    emitter = ControlEmitter(ctx, planner.solver.basis, T, 0.1, PlannerEnv())
+    ctx.set_stream(None)
+    planner.plan_cycle(worlds, PlannerEnv(), emitter, seed=1)      # warm the host path
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for k in range(max(1, min(args.steps, 5))):
-        planner._scenes_key = None          # force the scene upload (H2D) every step
-        res = planner.plan(e2e_scenes, seed=2 + k, scene_offset=10_000 + rank * S)
     e2e_steps = max(1, min(args.steps, 5))
+    t0 = time.perf_counter()
+    for k in range(e2e_steps):
+        acc, ste, sing, res = planner.plan_cycle(worlds, PlannerEnv(), emitter, seed=2 + k,
+                                                 scene_offset=10_000 + rank * S)
     e2e_s = (time.perf_counter() - t0) / e2e_steps
+    assert np.all(res.iterations_done == N_CEM)
     if dist is not None:
         t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    h2d = S * (2 * N_OBS * M * 8 + 9 * 8 + 6 * 8) + S * (8 + 64) * 8
+    h2d = worlds.ego.nbytes + worlds.veh.nbytes + worlds.n_veh.nbytes + worlds.road.nbytes + M * 8 + S * (8 + 64) * 8
     d2h = res.best_index.nbytes + res.best_params.nbytes + res.best_xi.nbytes + 3 * S * 8 + res.stats.nbytes + \
-        res.final_mean.nbytes + res.final_cov.nbytes + res.iterations_done.nbytes
+        res.final_mean.nbytes + res.final_cov.nbytes + res.iterations_done.nbytes + acc.nbytes + ste.nbytes + S * 4
 
     if rank != 0:
         return
@@ -306,7 +313,8 @@ def run_b200(args, rank: int, world: int, dist):
                    "l2": "flushed (256 MB write) between timed steps"},
         "e2e": {"value": S * world * N_CEM * B_CEM / e2e_s, "unit": "trajectories/s",
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "api": "FleetPlanner.plan (host scenes -> bd_set_scenes + bd_cem_cycle -> host results)"},
+                "api": "FleetPlanner.plan_cycle (host world state -> device scene build -> CEM cycle -> control "
+                       "emission -> host controls + best records)"},
         "gpu_launches": int(launches),
         "roofline": {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
                      "frac": achieved / fp32_peak, "traffic": traffic,

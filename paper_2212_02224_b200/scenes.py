@@ -17,7 +17,7 @@ import numpy as np
 
 from .constraints import ConstraintSpec, PlanningScene
 
-__all__ = ["HighwayRecipe", "highway_scene", "SENTINEL_DISTANCE"]
+__all__ = ["HighwayRecipe", "highway_scene", "spawn_worlds", "SENTINEL_DISTANCE"]
 
 SENTINEL_DISTANCE = 1e4
 
@@ -44,10 +44,9 @@ class HighwayRecipe:
     v_min: float = 0.5
 
 
-def highway_scene(seed: int, recipe: HighwayRecipe = HighwayRecipe()) -> PlanningScene:
-    r = recipe
+def _spawn(seed: int, r: HighwayRecipe):
+    """Neighbour (x, y, v) list of spawn_world (pkg/highway.py:168-205)."""
     rng = np.random.default_rng(seed)
-    ego_x, ego_y = 0.0, r.ego_lane * r.lane_width
     spacing = r.spawn_base_spacing / r.density
     cursor = [(25.0 if lane == r.ego_lane else -15.0) + spacing * 0.5 * rng.uniform(0.0, 1.0)
               for lane in range(r.lanes)]
@@ -59,6 +58,31 @@ def highway_scene(seed: int, recipe: HighwayRecipe = HighwayRecipe()) -> Plannin
         v = r.neighbor_speed * (1.0 + 0.15 * rng.uniform(-1.0, 1.0))
         rng.uniform(0.0, 2.0)   # lane-change cooldown draw of the simulator; keeps the stream aligned
         cars.append((float(x), lane * r.lane_width, float(v)))
+    return cars
+
+
+def spawn_worlds(seeds, recipe: HighwayRecipe = HighwayRecipe()):
+    """WorldBatch of freshly spawned worlds (ego at rest on its lane, heading 0) for the device
+    scene build (`worlds.build_scenes`)."""
+    from .worlds import WorldBatch
+    seeds = list(seeds)
+    r = recipe
+    S = len(seeds)
+    ego = np.zeros((S, 8))
+    veh = np.zeros((S, max(1, r.vehicle_count), 5))
+    ego[:, 1] = r.ego_lane * r.lane_width
+    ego[:, 3] = r.ego_speed
+    ego[:, 6], ego[:, 7] = 5.0, 2.0
+    for s, seed in enumerate(seeds):
+        for j, (x, y, v) in enumerate(_spawn(seed, r)):
+            veh[s, j] = (x, y, 0.0, v, 0.0)
+    return WorldBatch(ego, veh, np.full(S, r.vehicle_count, np.int32), np.tile([r.lanes, r.lane_width], (S, 1)))
+
+
+def highway_scene(seed: int, recipe: HighwayRecipe = HighwayRecipe()) -> PlanningScene:
+    r = recipe
+    ego_x, ego_y = 0.0, r.ego_lane * r.lane_width
+    cars = _spawn(seed, r)
     near = sorted((c for c in cars if abs(c[0] - ego_x) <= r.obstacle_range),
                   key=lambda c: (c[0] - ego_x) ** 2 + (c[1] - ego_y) ** 2)[: r.n_obs]
     times = np.linspace(0.0, r.horizon, r.num_samples)
