@@ -31,7 +31,7 @@ from .projection import ProjectionBatchResult, ProjectionConfig, ProjectionOpera
 __all__ = [
     "SamplingDistribution", "EliteRecord", "BiLevelConfig", "IterationStats", "BiLevelResult", "upper_cost",
     "upper_cost_batch", "rank_samples", "select_elites", "DegenerateWeights", "update_distribution",
-    "LowerLevelSolver", "solve_bilevel",
+    "LowerLevelSolver", "solve_bilevel", "evaluate_batch",
 ]
 
 log = logging.getLogger(__name__)
@@ -239,6 +239,32 @@ class LowerLevelSolver:
         yd = np.empty((B, m))
         self._ctx.call("bd_eval", B, ptr(X), None, None, ptr(xd), ptr(yd), None, None)
         return xd, yd
+
+
+def evaluate_batch(solver: LowerLevelSolver, scene: PlanningScene, params: np.ndarray, constraint_elites: int,
+                   elites: int, residual_weight: float = 1.0) -> tuple[EliteRecord, dict]:
+    """One lower-level sweep over a set-point batch and its best record by augmented cost —
+    the baseline planners' path (BasePlanner.evaluate_batch, pkg/planners.py:233-258: Random,
+    Grid, Vanilla and the goal-layout planner) on the same device kernels (solve + K3 ranking)."""
+    P = solver._params(params)
+    _, proj = solver.solve(P, scene)
+    costs = solver.last_costs
+    B = P.shape[0]
+    n = min(constraint_elites, B)
+    q = min(elites, n)
+    dim = solver.layout.dim
+    el = np.empty(q, np.int64)
+    ea = np.empty(q)
+    mean, cov = np.zeros(dim), np.eye(dim)       # the refit K3 also performs is discarded here
+    solver.context.call("bd_rank_refit", 1, B, dim, f64(proj.residuals), f64(costs), P, n, q,
+                        float(residual_weight), 0.5, 1.0, mean, cov, None, el, ea, None)
+    j = int(el[0])
+    record = EliteRecord(index=j, params=BehaviorParams.from_vector(P[j], solver.layout),
+                         coeffs=TrajectoryCoeffs.from_stacked(proj.xi[:, j]), upper_cost=float(costs[j]),
+                         residual=float(proj.residuals[j]), augmented_cost=float(ea[0]))
+    diag = {"residual": record.residual, "upper_cost": record.upper_cost, "proj_iterations": proj.iterations_used,
+            "batch": int(B)}
+    return record, diag
 
 
 # ----------------------------------------------------------------------------- upper level

@@ -150,3 +150,21 @@ def test_device_rng_cycle_is_deterministic_and_contracts():
     assert outs[0][1] == outs[1][1]
     assert outs[0][0][-1, 2] < outs[0][0][0, 2]      # covariance trace shrinks
     assert np.all(np.isfinite(outs[0][0]))
+
+
+@pytest.mark.parametrize("case", ["c1_s0", "goal", "dense50"])
+def test_evaluate_batch_baseline_planners(case):
+    """BasePlanner.evaluate_batch (pkg/planners.py:233-258) on the device: best record equals the
+    reference ranking of the reference's own residuals/costs (outside the tie band)."""
+    import paper_2212_02224_b200 as bd
+    from paper_2212_02224_b200.bilevel import evaluate_batch
+    from tests.test_gpu_parity import _solver
+    g = load("lower_" + case)
+    solver = _solver(g)
+    n, q = 150, 50
+    rec, diag = evaluate_batch(solver, _scene(g), g["params"], n, q, 1.0)
+    B = g["params"].shape[0]
+    _, el, ea = O.rank_two_stage(g["residuals"], g["costs"], min(n, B), min(q, min(n, B)), 1.0)
+    assert rec.index == int(el[0])
+    assert abs(rec.augmented_cost - ea[0]) <= 1e-3 * (1 + abs(ea[0]))
+    assert diag["batch"] == B and diag["proj_iterations"] == int(g["iterations_used"])
