@@ -15,6 +15,8 @@
 #include "cem_kernels.cuh"
 #include "aux_kernels.cuh"
 #include "cvae_kernel.cuh"
+#include "cvae_tc.cuh"
+#include <cudaTypedefs.h>
 #include "scene_kernels.cuh"
 
 using namespace bd;
@@ -87,13 +89,15 @@ struct bd_ctx {
     DevBuf ctrl_wd, ctrl_wdd, w_sing, w_accel, w_steer;
     // CVAE
     std::vector<int> cvae_dims;
-    std::vector<DevBuf*> cvae_w, cvae_b;
-    DevBuf cvae_h0, cvae_h1, cvae_obs, cvae_z;
+    std::vector<DevBuf*> cvae_w, cvae_b, cvae_w16;
+    DevBuf cvae_h0, cvae_h1, cvae_obs, cvae_z, cvae_a0, cvae_a1;
+    int cvae_tc = 1;            // option "cvae_tensor_cores": bf16 tcgen05 hidden layers (1) or fp32 SIMT (0)
     ~bd_ctx() {
         for (auto& e : ev_used) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
         for (auto& e : ev_free) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
         for (auto* b : cvae_w) delete b;
         for (auto* b : cvae_b) delete b;
+        for (auto* b : cvae_w16) delete b;
     }
 };
 
@@ -466,6 +470,10 @@ int bd_set_option(bd_ctx* ctx, const char* key, int value) {
         if (value != 0 && value != 4 && value != 8 && value != 16 && value != 32 && value != 64)
             return fail(ctx, BD_ERR_VALUE, "lanes_per_sample must be 0, 4, 8, 16, 32 or 64");
         ctx->opt_lanes = value;
+        return 0;
+    }
+    if (!strcmp(key, "cvae_tensor_cores")) {
+        ctx->cvae_tc = value != 0;
         return 0;
     }
     if (!strcmp(key, "timing")) {
@@ -1210,8 +1218,10 @@ int bd_cvae_set_weights(bd_ctx* ctx, int n_layers, const int* dims, const float*
     begin_call(ctx);
     for (auto* p : ctx->cvae_w) delete p;
     for (auto* p : ctx->cvae_b) delete p;
+    for (auto* p : ctx->cvae_w16) delete p;
     ctx->cvae_w.clear();
     ctx->cvae_b.clear();
+    ctx->cvae_w16.clear();
     ctx->cvae_dims.assign(dims, dims + n_layers + 1);
     for (int l = 0; l < n_layers; ++l) {
         const size_t nw = (size_t)dims[l] * dims[l + 1], nb = dims[l + 1];
@@ -1224,9 +1234,45 @@ int bd_cvae_set_weights(bd_ctx* ctx, int n_layers, const int* dims, const float*
         CU(bb->ensure(nb * 4));
         CU(cudaMemcpy(wb->p, W[l], nw * 4, cudaMemcpyDefault));
         CU(cudaMemcpy(bb->p, b[l], nb * 4, cudaMemcpyDefault));
+        // bf16 copy for the tensor-core layers
+        std::vector<float> hw(nw);
+        CU(cudaMemcpy(hw.data(), W[l], nw * 4, cudaMemcpyDefault));
+        std::vector<__nv_bfloat16> h16(nw);
+        for (size_t i = 0; i < nw; ++i) h16[i] = __float2bfloat16_rn(hw[i]);
+        auto* w16 = new DevBuf();
+        ctx->cvae_w16.push_back(w16);
+        CU(w16->ensure(nw * 2));
+        CU(cudaMemcpy(w16->p, h16.data(), nw * 2, cudaMemcpyHostToDevice));
     }
     return 0;
 }
+
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// 2-D bf16 row-major [rows x cols] tensor map with a 128-row x 64-col box and 128-byte swizzle.
+bool make_map_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols) {
+    auto enc = tensor_map_encoder();
+    if (!enc) return false;
+    const cuuint64_t dims[2] = {cols, rows};
+    const cuuint64_t strides[1] = {cols * 2};
+    const cuuint32_t box[2] = {(cuuint32_t)TC_BK, (cuuint32_t)TC_BM};
+    const cuuint32_t estr[2] = {1, 1};
+    return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+}  // namespace
 
 int bd_cvae_decode(bd_ctx* ctx, int count, const float* obs, const float* z, double* params) {
     if (!ctx || count < 1 || !obs || !z || !params) return BD_ERR_VALUE;
@@ -1242,6 +1288,41 @@ int bd_cvae_decode(bd_ctx* ctx, int count, const float* obs, const float* z, dou
     if ((rc = stage_in(ctx, z, (size_t)count * zdim, &dz))) return rc;
     int widest = 0;
     for (int l = 1; l <= L; ++l) widest = widest > d[l] ? widest : d[l];
+    bool tc_ok = ctx->cvae_tc && L >= 3 && tensor_map_encoder() != nullptr;
+    for (int l = 1; l < L - 1 && tc_ok; ++l) tc_ok = d[l] % TC_BK == 0 && d[l + 1] % TC_BN == 0;
+    if (tc_ok) {
+        const int mpad = (count + TC_BM - 1) / TC_BM * TC_BM;
+        CU(ctx->cvae_a0.ensure((size_t)mpad * widest * 2));
+        CU(ctx->cvae_a1.ensure((size_t)mpad * widest * 2));
+        CU(cudaMemsetAsync(ctx->cvae_a0.p, 0, (size_t)mpad * widest * 2, ctx->stream));
+        double* dout;
+        DevBuf& ws = ctx->stage[7];
+        if ((rc = stage_out(ctx, params, (size_t)count * d[L], ws, &dout))) return rc;
+        auto* cur = ctx->cvae_a0.as<__nv_bfloat16>();
+        auto* nxt = ctx->cvae_a1.as<__nv_bfloat16>();
+        cvae_first_layer_bf16<<<dim3((d[1] + 127) / 128, (count + 31) / 32), dim3(128), 0, ctx->stream>>>(
+            count, d[1], zdim, ctx->cvae_w[0]->as<float>(), ctx->cvae_b[0]->as<float>(), dobs, dz, cur);
+        ctx->launches++;
+        raise_smem(cvae_tc_linear, TC_SMEM);
+        for (int l = 1; l < L - 1; ++l) {
+            CUtensorMap ma, mb;
+            if (!make_map_bf16(&ma, cur, (uint64_t)count, (uint64_t)d[l]) ||
+                !make_map_bf16(&mb, ctx->cvae_w16[l]->p, (uint64_t)d[l + 1], (uint64_t)d[l]))
+                return fail(ctx, BD_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+            dim3 grid(d[l + 1] / TC_BN, mpad / TC_BM);
+            cvae_tc_linear<<<grid, 128, TC_SMEM, ctx->stream>>>(ma, mb, count, d[l + 1], d[l],
+                                                                ctx->cvae_b[l]->as<float>(), nxt, 1);
+            ctx->launches++;
+            auto* t = cur;
+            cur = nxt;
+            nxt = t;
+        }
+        cvae_last_layer_bf16<<<(count + 7) / 8, 256, 0, ctx->stream>>>(count, d[L - 1], d[L], cur,
+                                                                       ctx->cvae_w[L - 1]->as<float>(),
+                                                                       ctx->cvae_b[L - 1]->as<float>(), dout);
+        ctx->launches++;
+        return finish_call(ctx, false, 0);
+    }
     CU(ctx->cvae_h0.ensure((size_t)count * widest * 4));
     CU(ctx->cvae_h1.ensure((size_t)count * widest * 4));
     double* dout;

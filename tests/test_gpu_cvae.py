@@ -9,9 +9,10 @@ from oracle.cvae import decode as decode_ref
 pytestmark = pytest.mark.gpu
 
 
-def test_cvae_decoder_matches_float64_restatement():
+def test_cvae_decoder_fp32_matches_float64_restatement():
     from paper_2212_02224_b200.cvae import CVAEDecoder
     dec = CVAEDecoder.synthetic(7)
+    dec.ctx.set_option("cvae_tensor_cores", 0)
     rng = np.random.default_rng(0)
     obs = rng.standard_normal(55).astype(np.float32)
     z = rng.standard_normal((1000, 2)).astype(np.float32)
@@ -20,6 +21,22 @@ def test_cvae_decoder_matches_float64_restatement():
     assert got.shape == (1000, 8)
     scale = np.abs(ref).max()
     np.testing.assert_allclose(got, ref, rtol=0, atol=1e-4 * scale)
+
+
+@pytest.mark.parametrize("count", [1000, 128, 77])
+def test_cvae_decoder_tcgen05_bf16(count):
+    """Hidden layers on tcgen05 (bf16 operands, fp32 TMEM accumulation): bf16 rounding bound."""
+    from paper_2212_02224_b200.cvae import CVAEDecoder
+    dec = CVAEDecoder.synthetic(7)
+    rng = np.random.default_rng(1)
+    obs = rng.standard_normal(55).astype(np.float32)
+    z = rng.standard_normal((count, 2)).astype(np.float32)
+    got = dec.decode(obs, z)
+    ref = decode_ref(dec.W, dec.b, obs, z)
+    scale = np.abs(ref).max()
+    err = np.abs(got - ref)
+    assert err.max() <= 5e-2 * scale, err.max() / scale
+    assert err.mean() <= 1e-2 * scale, err.mean() / scale
 
 
 def test_cvae_odd_sizes_and_errors():
