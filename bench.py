@@ -169,6 +169,41 @@ def cem_latency(device: int, cycles: int = 30):
                       "host-visible best xi via solve_bilevel (numpy Generator draws, H2D+D2H included)"}
 
 
+def cvae_config3(device: int, cycles: int = 20):
+    """BASELINE config 3: CVAE decoder draws 1000 set-points from a scene embedding (the 55-entry
+    observation), which warm-start iteration 1 of the config-2 CEM cycle; p50 of decode + cycle
+    through the public API (tcgen05 decoder, synthetic seeded weights: the reference ships none)."""
+    import paper_2212_02224_b200 as bd
+    from paper_2212_02224_b200.cvae import CVAEDecoder
+    from paper_2212_02224_b200.fleet import initial_distribution
+    from paper_2212_02224_b200.scenes import highway_scene, spawn_worlds
+    from paper_2212_02224_b200.worlds import PlannerEnv, build_scenes
+    basis = bd.build_basis(10, M, T, "bernstein")
+    solver = bd.LowerLevelSolver(basis, bd.TrackingWeights(), bd.ParamLayout(4),
+                                 bd.ProjectionConfig(1.0, AM_ITERS, 1e-3), N_OBS, device=device)
+    scene = highway_scene(0)
+    mean, cov = initial_distribution(scene)
+    cfg = bd.BiLevelConfig(B_CEM, N_CONS, N_ELITE, N_CEM, 0.7, 0.9, 1.0, mean, cov)
+    dec = CVAEDecoder.synthetic(0, context=solver.context)
+    # the scene embedding: observe() of the world, built on the device
+    *_, obs = build_scenes(solver.context, basis, spawn_worlds([0]), PlannerEnv(), outputs=True)
+    solver.projector._scene_key = None
+    raw = dec.decode(obs[0], np.random.default_rng(0).standard_normal((B_CEM, 2)))
+    shift = mean - raw.mean(axis=0)            # untrained decoder: centre its output on the prior mean
+    ts = []
+    for s in range(cycles + 3):
+        rng = np.random.default_rng(200 + s)
+        t0 = time.perf_counter()
+        ws = dec.warm_start(obs[0], B_CEM, solver.layout, rng, shift=shift)
+        res = bd.solve_bilevel(scene, solver, cfg, rng, warm_start=ws)
+        if s >= 3:
+            ts.append(1e3 * (time.perf_counter() - t0))
+        assert not res.degraded
+    return {"p50_ms": float(np.percentile(ts, 50)), "p99_ms": float(np.percentile(ts, 99)), "cycles": cycles,
+            "config": "CVAE decode of 1000 set-points (tcgen05 bf16 hidden layers) + config-2 CEM cycle warm-started "
+                      "from them; host call to host-visible best xi"}
+
+
 def dense_config4(device: int, steps: int = 3):
     """BASELINE config 4 on one GPU: one scene, B = 10 000 samples x 50 obstacles, one full CEM
     cycle (4 iterations, 100 AM iterations) per step, device Philox draws."""
@@ -327,6 +362,7 @@ def run_b200(args, rank: int, world: int, dist):
     if world == 1:
         line["cem_cycle_latency"] = cem_latency(dev)
         line["dense_config4"] = dense_config4(dev)
+        line["cvae_config3_latency"] = cvae_config3(dev)
         ref, _ = cpu_reference(steps=2, warmup=1)
         line["cpu_baseline"] = ref
     print(json.dumps(line), flush=True)
