@@ -11,8 +11,12 @@ pytestmark = pytest.mark.gpu
 
 def test_batch_serial_equivalence():
     """Projecting a batch equals projecting each sample alone — per-sample results
-    do not depend on the batch (up to the lane mapping's rounding order)."""
-    g = load("lower_c1_s0")
+    do not depend on the batch.  The reference's batch-global early exit (pkg/projection.py:329)
+    couples the samples of a batch (a lone sample may stop early), so the tolerance is set below
+    any residual here."""
+    import paper_2212_02224_b200 as bd
+    g = dict(load("lower_c1_s0"))
+    g["tol"] = 1e-30
     solver = _solver(g)
     sc = _scene(g)
     _, full = solver.solve(g["params"], sc)
