@@ -82,7 +82,7 @@ __device__ __forceinline__ void exit_scan_block(const unsigned* base, int max_it
 
 // Shared-memory carve-up, identical on host and device.
 struct AmSmem {
-    size_t w, obs, k, kb, a, curv, box, scr, dap, kap, total;
+    size_t w, obs, k, kb, a, curv, scr, dap, kap, total;
     __host__ __device__ AmSmem(int m, int n_obs, int neq, int n_curv, int s_cta, int threads, int P, bool curv_on) {
         const int J = (m + P - 1) / P;
         size_t o = 0;
@@ -92,7 +92,6 @@ struct AmSmem {
         kb = o;   o = align_up(o + (size_t)NX * neq * 8, 16);
         a = o;    o = align_up(o + (size_t)neq * NX * 8, 16);
         curv = o; o = align_up(o + (size_t)2 * n_curv * 4, 16);
-        box = o;  o = align_up(o + (size_t)(n_obs / 2) * 16, 16);        // per obstacle pair: scaled bbox
         scr = o;  o = align_up(o + (size_t)s_cta * SCR_BYTES, 16);
         dap = o;  o = align_up(o + (size_t)J * threads * 4, 16);
         kap = o;  o = align_up(o + (curv_on ? (size_t)J * threads * 4 : 0), 16);
@@ -142,7 +141,7 @@ template <int P, bool CURV, bool INIT, int NV, int MT, int NPT, int TPB>
 __device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float4* __restrict__ osm,
                                       const float* __restrict__ csm, const float2 (&cxy)[NC], float (&v)[NV],
                                       float* dap, float* kap, int dstride_rt, int p, int m_rt, int npair_rt,
-                                      int n_curv, const SceneLim& L, int& conf, bool& ovf, unsigned pmask) {
+                                      int n_curv, const SceneLim& L, int& conf, bool& ovf) {
     // MT / NPT / TPB > 0: timesteps, obstacle pairs and CTA size fixed at compile time (the
     // BASELINE shapes), so the tile addressing folds into immediates and the pair loop unrolls.
     const int m = MT ? MT : m_rt;
@@ -211,7 +210,6 @@ __device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float
         float qmin = 3.0e38f;
 #pragma unroll 5
         for (int o = 0; o < npair; ++o) {
-            if (o < 32 && !(pmask & (1u << o))) continue;   // pair culled for every sample of this warp
             const float4 ob = op[o];
             const float2 wc = fadd2(make_float2(xs, xs), make_float2(ob.x, ob.y));
             const float2 ws = fadd2(make_float2(ys, ys), make_float2(ob.z, ob.w));
@@ -220,7 +218,6 @@ __device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float
         }
         if (qmin < 1.f) {
             for (int o = 0; o < npair; ++o) {
-                if (o < 32 && !(pmask & (1u << o))) continue;
                 const float4 ob = op[o];
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
@@ -287,30 +284,6 @@ __device__ __forceinline__ void pair_sync() {
 #ifndef BD_AM_MINB
 #define BD_AM_MINB 2       // x 256 threads: 128 registers per thread
 #endif
-// Obstacle-pair culling mask for the warp: Bernstein rows are non-negative and sum to one, so the
-// sample's positions lie in the box of its control points; pairs whose path box (grown by the
-// ellipse) misses it contribute nothing this iteration.  OR over the warp keeps the loop uniform.
-__device__ __forceinline__ unsigned pair_mask(const float2 (&cxy)[NC], const float4* bsm, int npair, float inv_a,
-                                              float inv_b) {
-    if (npair > 32) return 0xffffffffu;
-    float xl = cxy[0].x, xh = xl, yl = cxy[0].y, yh = yl;
-#pragma unroll
-    for (int k = 1; k < NC; ++k) {
-        xl = fminf(xl, cxy[k].x); xh = fmaxf(xh, cxy[k].x);
-        yl = fminf(yl, cxy[k].y); yh = fmaxf(yh, cxy[k].y);
-    }
-    // scaled, with a relative margin for the fp32 evaluation of the basis products
-    const float mx = 1e-4f * (fabsf(xl) + fabsf(xh)) * inv_a + 1e-4f, my = 1e-4f * (fabsf(yl) + fabsf(yh)) * inv_b + 1e-4f;
-    xl = xl * inv_a - mx; xh = xh * inv_a + mx; yl = yl * inv_b - my; yh = yh * inv_b + my;
-    unsigned msk = 0;
-    for (int j = 0; j < npair; ++j) {
-        const float4 b = bsm[j];
-        const bool hit = !(xh < b.x || xl > b.y || yh < b.z || yl > b.w);
-        msk |= hit ? (1u << j) : 0u;
-    }
-    return __reduce_or_sync(0xffffffffu, msk);
-}
-
 template <int P, bool CURV, int MT = 0, int NPT = 0, int TPB = 0>
 __global__ void __launch_bounds__(256, BD_AM_MINB) am_kernel(const AmArgs a) {
     // P <= 32: a sample is a group of P lanes of one warp.  P == 64: a sample spans two warps
@@ -347,20 +320,6 @@ __global__ void __launch_bounds__(256, BD_AM_MINB) am_kernel(const AmArgs a) {
     for (int i = threadIdx.x; i < NX * neq; i += threads) { kbsm[i] = a.kb[i]; asm_[i] = a.aeq[i]; }
     if (CURV)
         for (int i = threadIdx.x; i < 2 * a.n_curv; i += threads) csm[i] = a.curv[(size_t)scene * 2 * a.n_curv + i];
-    float4* bsm = reinterpret_cast<float4*>(smem + lay.box);
-    __syncthreads();
-    // bounding box of each obstacle pair's predicted path over the horizon (scaled coordinates),
-    // grown by the unit ellipse radius: a sample whose convex-hull box misses it cannot have
-    // q < 1 against either obstacle at any timestep
-    for (int j = threadIdx.x; j < n_obs / 2; j += threads) {
-        float xlo = 3e38f, xhi = -3e38f, ylo = 3e38f, yhi = -3e38f;
-        for (int t = 0; t < m; ++t) {
-            const float4 ob = osm[t * (n_obs / 2) + j];
-            xlo = fminf(xlo, -fmaxf(ob.x, ob.y)); xhi = fmaxf(xhi, -fminf(ob.x, ob.y));
-            ylo = fminf(ylo, -fmaxf(ob.z, ob.w)); yhi = fmaxf(yhi, -fminf(ob.z, ob.w));
-        }
-        bsm[j] = make_float4(xlo - 1.f, xhi + 1.f, ylo - 1.f, yhi + 1.f);
-    }
     __syncthreads();
 
     const int lane = threadIdx.x & 31;
@@ -423,9 +382,8 @@ __global__ void __launch_bounds__(256, BD_AM_MINB) am_kernel(const AmArgs a) {
             if (!(threadIdx.x & 32) && lane < NX + 2) v[0] += xbuf[lane];
         }
     };
-    unsigned pmask = pair_mask(cxy, bsm, n_obs / 2, L.inv_a, L.inv_b);
     sweep<P, CURV, true, NV, MT, NPT, TPB>(wsm, osm, csm, cxy, v, dap, kap, threads, p, m, n_obs / 2, a.n_curv, L,
-                                           conf, ovf, pmask);
+                                           conf, ovf);
     reduce();
 
     const int r_lane = NX % RP, r_slot = (NX / RP) * RP;
@@ -480,9 +438,8 @@ __global__ void __launch_bounds__(256, BD_AM_MINB) am_kernel(const AmArgs a) {
 #pragma unroll
         for (int q = 0; q < NC; ++q) cxy[q] = reinterpret_cast<const float2*>(sc)[q];
         // ---- projections, back-projection, residual at the new iterate
-        pmask = pair_mask(cxy, bsm, n_obs / 2, L.inv_a, L.inv_b);
         sweep<P, CURV, false, NV, MT, NPT, TPB>(wsm, osm, csm, cxy, v, dap, kap, threads, p, m, n_obs / 2, a.n_curv,
-                                                L, conf, ovf, pmask);
+                                                L, conf, ovf);
         reduce();
         resid = v[r_slot];
         cost = v[c_slot];
