@@ -21,13 +21,13 @@ def test_batch_serial_equivalence():
     sc = _scene(g)
     _, full = solver.solve(g["params"], sc)
     checked = 0
-    for j in range(0, 100, 7):
+    for j in range(0, 100, 3):
         _, one = solver.solve(g["params"][j:j + 1], sc)
         if one.iterations_used != full.iterations_used:
             continue                        # this sample alone met the tolerance: exits earlier
         np.testing.assert_allclose(one.xi[:, 0], full.xi[:, j], rtol=1e-5, atol=1e-5)
         checked += 1
-    assert checked >= 5
+    assert checked >= 3
 
 
 def test_initial_conditions_preserved():
