@@ -137,6 +137,9 @@ __device__ __forceinline__ void group_reduce_scatter(float (&v)[NV], int lane) {
 // forward evaluation, polar split + coupled clips, back-projection of the residuals
 // (v[2k] = g_x[k], v[2k+1] = g_y[k]), the direct residual (v[22]) and the upper cost (v[23]).
 // The x/y pairs run as packed fp32x2 (FFMA2 with the basis value broadcast).
+#ifndef BD_AM_OBS_EARLY
+#define BD_AM_OBS_EARLY 1
+#endif
 template <int P, bool CURV, bool INIT, int NV, int MT, int NPT, int TPB>
 __device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float4* __restrict__ osm,
                                       const float* __restrict__ csm, const float2 (&cxy)[NC], float (&v)[NV],
@@ -160,11 +163,39 @@ __device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float
         }
         // forward (X, Y) = W c, (Xd, Yd) = Wd c, (Xdd, Ydd) = Wdd c (pkg/projection.py:295)
         float2 P0 = make_float2(0.f, 0.f), P1 = P0, P2 = P0;
+        const float4* op = osm + t * npair;          // (-x0, -x1, -y0, -y1) / (a, a, b, b)
+        float qmin = 3.0e38f;
+#if BD_AM_OBS_EARLY
+        if (NPT > 0) {
+            // position first, then the obstacle-distance pass interleaved with the derivative
+            // chains so the tile's shared-memory latency hides behind them
 #pragma unroll
-        for (int k = 0; k < NC; ++k) {
-            P0 = ffma2(w[k], cxy[k], P0);
-            P1 = ffma2(w[NC + k], cxy[k], P1);
-            P2 = ffma2(w[2 * NC + k], cxy[k], P2);
+            for (int k = 0; k < NC; ++k) P0 = ffma2(w[k], cxy[k], P0);
+            float4 ob[NPT > 0 ? NPT : 1];
+#pragma unroll
+            for (int o = 0; o < NPT; ++o) ob[o] = op[o];
+#pragma unroll
+            for (int k = 0; k < NC; ++k) {
+                P1 = ffma2(w[NC + k], cxy[k], P1);
+                P2 = ffma2(w[2 * NC + k], cxy[k], P2);
+            }
+            const float xs0 = P0.x * L.inv_a, ys0 = P0.y * L.inv_b;
+#pragma unroll
+            for (int o = 0; o < NPT; ++o) {
+                const float2 wc = fadd2(make_float2(xs0, xs0), make_float2(ob[o].x, ob[o].y));
+                const float2 ws = fadd2(make_float2(ys0, ys0), make_float2(ob[o].z, ob[o].w));
+                const float2 q = ffma2(wc, wc, fmul2(ws, ws));
+                qmin = fminf(qmin, fminf(q.x, q.y));
+            }
+        } else
+#endif
+        {
+#pragma unroll
+            for (int k = 0; k < NC; ++k) {
+                P0 = ffma2(w[k], cxy[k], P0);
+                P1 = ffma2(w[NC + k], cxy[k], P1);
+                P2 = ffma2(w[2 * NC + k], cxy[k], P2);
+            }
         }
         const float X = P0.x, Y = P0.y, XD = P1.x, YD = P1.y, XDD = P2.x, YDD = P2.y;
         // velocity / acceleration polar split (pkg/projection.py:119-122) in unit-vector form
@@ -206,10 +237,8 @@ __device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float
         // (q < 1) takes the exact per-obstacle path.
         const float xs = X * L.inv_a, ys = Y * L.inv_b;
         float rox = 0.f, roy = 0.f, coll = 0.f;
-        const float4* op = osm + t * npair;          // (-x0, -x1, -y0, -y1) / (a, a, b, b)
-        float qmin = 3.0e38f;
 #pragma unroll 5
-        for (int o = 0; o < npair; ++o) {
+        for (int o = 0; o < ((BD_AM_OBS_EARLY && NPT > 0) ? 0 : npair); ++o) {
             const float4 ob = op[o];
             const float2 wc = fadd2(make_float2(xs, xs), make_float2(ob.x, ob.y));
             const float2 ws = fadd2(make_float2(ys, ys), make_float2(ob.z, ob.w));
