@@ -218,6 +218,33 @@ int bd_set_control_grid(bd_ctx* ctx, int n_ctrl, const double* Wd_ctrl, const do
                         double a_max, double steer_limit, double eps_v);
 int bd_controls(bd_ctx* ctx, int count, const double* xi, double* accel, double* steer, int* singular);
 
+/* ------------------------------------------------------------------ closed-loop simulation
+ * SURVEY §8f row 4.  Replaces the Python simulator tick step (pkg/highway.py:358-410: neighbour
+ * IDM + MOBIL decisions on the frozen snapshot, ego RK4 bicycle, neighbour updates, SAT collision,
+ * lane departure) and the open-loop inner loop of run_episode (pkg/highway.py:517-529) for S worlds.
+ * Traffic constants: IDMParams / MOBILParams (pkg/highway.py:73-89), ScenarioConfig.dt, wheelbase. */
+typedef struct bd_traffic {
+    double idm_v0, idm_time_headway, idm_s0, idm_a_max, idm_b_comfort, idm_delta, idm_b_hard;
+    double mobil_politeness, mobil_b_safe, mobil_a_threshold, mobil_cooldown;
+    double dt, wheelbase;
+} bd_traffic;
+
+/* Run n_steps ticks of S worlds in place.  World state (device or host pointers; host arrays are
+ * copied in and back): ego S x 8 (x, y, psi, v, accel, steer, length, width — the bd_build_scenes
+ * layout), ego_target_speed S, veh S x n_veh_max x 5 (x, y, psi, v, lateral_rate), veh_ext
+ * S x n_veh_max x 7 (length, width, target_speed, target_lane, cooldown, accel, lane_index),
+ * n_veh S, road S x 2 (lane_count, lane_width), world S x 5 (time, step_count, collided,
+ * collision_step or -1, lane_departed).  Tick j applies controls[s][min(ctrl_offset + j, n_ctrl-1)]
+ * (accel, steer).  x_end NULL: plain ticks.  x_end S: run_episode semantics — a world stops after
+ * the tick that collides or reaches ego.x >= x_end[s], and its active flag is cleared.  active S
+ * (nullable, in/out): worlds with 0 are not stepped.  steps_done S (nullable): ticks executed.
+ * snapshots (nullable): S x n_steps x (8 + 4 n_veh_max) doubles per tick: time, ego x y psi v
+ * accel steer, collided, then each neighbour's x y psi v (the run_episode step record). */
+int bd_sim_run(bd_ctx* ctx, int n_worlds, int n_veh_max, double* ego, double* ego_target_speed, double* veh,
+               double* veh_ext, const int* n_veh, const double* road, double* world, const bd_traffic* traffic,
+               int n_steps, const double* controls, int n_ctrl, int ctrl_offset, const double* x_end, int* active,
+               int* steps_done, double* snapshots);
+
 /* ------------------------------------------------------------------ CVAE warm start
  * Decoder MLP of the paper (not in the reference package):
  * (obs 55 + z 2) -> 1024 -> 1024 -> 1024 -> 1024 -> 256 -> dim, BatchNorm folded

@@ -52,6 +52,8 @@ SIGNATURES = {
     "bd_build_scenes": (c_int, [_P, c_int, c_int, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "bd_set_control_grid": (c_int, [_P, c_int, _P, _P, c_double, c_double, c_double, c_double]),
     "bd_controls": (c_int, [_P, c_int, _P, _P, _P, _P]),
+    "bd_sim_run": (c_int, [_P, c_int, c_int, _P, _P, _P, _P, _P, _P, _P, _P, c_int, _P, c_int, c_int, _P, _P, _P,
+                           _P]),
     "bd_cvae_set_weights": (c_int, [_P, c_int, _P, _P, _P]),
     "bd_cvae_decode": (c_int, [_P, c_int, _P, _P, _P]),
 }
@@ -68,6 +70,13 @@ class CemConfig(ctypes.Structure):
     _fields_ = [("batch", c_int), ("n_cons", c_int), ("n_elite", c_int), ("iterations", c_int),
                 ("am_iters", c_int), ("eta", c_double), ("gamma", c_double), ("residual_weight", c_double),
                 ("tol", c_double), ("seed", c_uint64), ("scene_offset", c_int)]
+
+
+class Traffic(ctypes.Structure):
+    """bd_traffic: IDMParams / MOBILParams (pkg/highway.py:73-89), tick length and wheelbase."""
+    _fields_ = [(n, c_double) for n in
+                ("idm_v0", "idm_time_headway", "idm_s0", "idm_a_max", "idm_b_comfort", "idm_delta", "idm_b_hard",
+                 "mobil_politeness", "mobil_b_safe", "mobil_a_threshold", "mobil_cooldown", "dt", "wheelbase")]
 
 
 class Env(ctypes.Structure):

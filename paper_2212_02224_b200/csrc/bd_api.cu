@@ -18,6 +18,7 @@
 #include "cvae_tc.cuh"
 #include <cudaTypedefs.h>
 #include "scene_kernels.cuh"
+#include "sim_kernels.cuh"
 
 using namespace bd;
 
@@ -87,6 +88,8 @@ struct bd_ctx {
     int n_ctrl = 0;
     double ctrl_wb = 0, ctrl_amax = 0, ctrl_steer = 0, ctrl_eps = 0;
     DevBuf ctrl_wd, ctrl_wdd, w_sing, w_accel, w_steer;
+    // closed-loop simulation (in/out staging of host world state)
+    DevBuf sim_io[7];
     // CVAE
     std::vector<int> cvae_dims;
     std::vector<DevBuf*> cvae_w, cvae_b, cvae_w16;
@@ -203,6 +206,18 @@ int stage_out_req(bd_ctx* ctx, T* user, size_t count, DevBuf& ws, T** out) {
         ctx->pending.push_back({user, ws.p, count * sizeof(T)});
         ctx->host_out = true;
     }
+    return 0;
+}
+
+// In/out arrays: device pointers are used in place; host arrays are copied in and copied back.
+template <class T>
+int stage_inout(bd_ctx* ctx, T* user, size_t count, DevBuf& ws, T** out) {
+    if (!user || count == 0 || is_device_ptr(user)) { *out = user; return 0; }
+    CU(ws.ensure(count * sizeof(T)));
+    CU(cudaMemcpyAsync(ws.p, user, count * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+    *out = ws.as<T>();
+    ctx->pending.push_back({user, ws.p, count * sizeof(T)});
+    ctx->host_out = true;
     return 0;
 }
 
@@ -1347,6 +1362,48 @@ int bd_cvae_decode(bd_ctx* ctx, int count, const float* obs, const float* z, dou
     }
     cvae_to_double<<<(unsigned)(((size_t)count * d[L] + 255) / 256), 256, 0, ctx->stream>>>(cur, dout,
                                                                                            (size_t)count * d[L]);
+    ctx->launches++;
+    return finish_call(ctx, false, 0);
+}
+
+
+int bd_sim_run(bd_ctx* ctx, int S, int n_max, double* ego, double* ego_ts, double* veh, double* vext, const int* n_veh,
+               const double* road, double* world, const bd_traffic* tp, int n_steps, const double* controls, int n_ctrl,
+               int ctrl_offset, const double* x_end, int* active, int* steps_done, double* snapshots) {
+    if (!ctx) return BD_ERR_VALUE;
+    if (S < 1 || n_max < 0 || n_steps < 0 || !tp || !ego || !ego_ts || !n_veh || !road || !world ||
+        (n_max > 0 && (!veh || !vext)) || (n_steps > 0 && (!controls || n_ctrl < 1)) || ctrl_offset < 0)
+        return fail(ctx, BD_ERR_VALUE, "bad sim_run arguments");
+    if (n_max > 4096) return fail(ctx, BD_ERR_VALUE, "at most 4096 neighbours per world");
+    if (!(tp->dt > 0) || !(tp->wheelbase > 0) || !(tp->idm_v0 > 0) || !(tp->idm_a_max > 0) || !(tp->idm_b_comfort > 0))
+        return fail(ctx, BD_ERR_VALUE, "traffic constants must be positive");
+    begin_call(ctx);
+    if (n_steps == 0) return 0;
+    int rc;
+    SimArgs a{};
+    a.S = S; a.n_max = n_max; a.n_steps = n_steps; a.n_ctrl = n_ctrl; a.ctrl_offset = ctrl_offset;
+    a.period = (int)std::max(1.0, std::nearbyint(1.0 / tp->dt));     // max(1, int(round(1.0 / dt)))
+    a.dt = tp->dt; a.wheelbase = tp->wheelbase;
+    a.idm_v0 = tp->idm_v0; a.idm_T = tp->idm_time_headway; a.idm_s0 = tp->idm_s0; a.idm_a = tp->idm_a_max;
+    a.idm_b = tp->idm_b_comfort; a.idm_delta = tp->idm_delta; a.idm_bhard = tp->idm_b_hard;
+    a.idm_sqrt_ab2 = 2.0 * std::sqrt(tp->idm_a_max * tp->idm_b_comfort);
+    a.pol = tp->mobil_politeness; a.b_safe = tp->mobil_b_safe; a.a_thr = tp->mobil_a_threshold;
+    a.cooldown = tp->mobil_cooldown;
+    if ((rc = stage_inout(ctx, ego, (size_t)S * 8, ctx->sim_io[0], &a.ego))) return rc;
+    if ((rc = stage_inout(ctx, ego_ts, (size_t)S, ctx->sim_io[1], &a.ego_ts))) return rc;
+    if ((rc = stage_inout(ctx, veh, (size_t)S * n_max * 5, ctx->sim_io[2], &a.veh))) return rc;
+    if ((rc = stage_inout(ctx, vext, (size_t)S * n_max * VEXT, ctx->sim_io[3], &a.vext))) return rc;
+    if ((rc = stage_inout(ctx, world, (size_t)S * 5, ctx->sim_io[4], &a.world))) return rc;
+    if ((rc = stage_inout(ctx, active, active ? (size_t)S : 0, ctx->sim_io[5], &a.active))) return rc;
+    if ((rc = stage_in(ctx, n_veh, (size_t)S, &a.n_veh))) return rc;
+    if ((rc = stage_in(ctx, road, (size_t)S * 2, &a.road))) return rc;
+    if ((rc = stage_in(ctx, controls, (size_t)S * n_ctrl * 2, &a.ctrl))) return rc;
+    if ((rc = stage_in(ctx, x_end, x_end ? (size_t)S : 0, &a.x_end))) return rc;
+    if ((rc = stage_out(ctx, steps_done, (size_t)S, ctx->sim_io[6], &a.steps_done))) return rc;
+    if ((rc = stage_out(ctx, snapshots, (size_t)S * n_steps * (8 + 4 * n_max), ctx->w_hist, &a.snap))) return rc;
+    const size_t smem = (size_t)(n_max + 1) * (6 * sizeof(double) + 2 * sizeof(int));
+    raise_smem(sim_kernel, smem);
+    sim_kernel<<<S, 128, smem, ctx->stream>>>(a);
     ctx->launches++;
     return finish_call(ctx, false, 0);
 }

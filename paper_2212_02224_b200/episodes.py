@@ -1,0 +1,279 @@
+"""Closed-loop episodes and benchmark suites for a fleet of worlds.
+
+Batched restatement of ``run_episode`` (pkg/highway.py:487-532), ``EpisodeLog``
+(:413-475) and the suite harness ``run_suite`` / ``write_outputs`` (pkg/bench.py:32-205).
+All S episodes of a batch advance in lockstep: at every replan instant one batched planning
+call (:mod:`.planners`) plans every live world from the simulator's HBM state, then one
+``bd_sim_run`` launch executes the plans open loop up to the next replan instant, stopping
+worlds on collision or at the end of the road.  Per-step records come back from the device as
+one snapshot block per stretch and are unpacked into reference-format ``EpisodeLog`` records.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .planners import PlannerEnvConfig, make_batch_planner
+from .sim import SNAP_HEAD, ScenarioConfig, SimState, Simulator, TrafficParams
+
+__all__ = ["EpisodeLog", "run_episodes", "BenchmarkSuite", "MetricsRow", "run_suite", "write_outputs",
+           "suite_from_dict", "load_suite", "METRICS_HEADER", "TIMINGS_HEADER"]
+
+METRICS_HEADER = "planner,scenario,episodes,collisions,collision_rate,mean_speed,failures"
+TIMINGS_HEADER = "planner,scenario,mean_solve_time,total_wall_time"
+
+
+@dataclass
+class EpisodeLog:
+    """Per-step record of one episode plus outcome flags (pkg/highway.py:413-475, same JSONL)."""
+
+    meta: dict
+    steps: list = field(default_factory=list)
+    plan_records: list = field(default_factory=list)
+    collided: bool = False
+    collision_step: int | None = None
+    lane_departed: bool = False
+    failed: bool = False
+    failure_reason: str = ""
+
+    def ego_speeds(self) -> np.ndarray:
+        return np.array([rec["ego"][3] for rec in self.steps])
+
+    def mean_speed(self) -> float:
+        sp = self.ego_speeds()
+        return float(sp.mean()) if sp.size else 0.0
+
+    def solve_times(self) -> list:
+        return [rec["solve_time"] for rec in self.plan_records if "solve_time" in rec]
+
+    def write_jsonl(self, path: str) -> None:
+        with open(path, "w", encoding="utf-8") as fh:
+            header = {"type": "meta", **self.meta, "collided": self.collided, "collision_step": self.collision_step,
+                      "lane_departed": self.lane_departed, "failed": self.failed,
+                      "failure_reason": self.failure_reason}
+            fh.write(json.dumps(header, sort_keys=True) + "\n")
+            for rec in self.plan_records:
+                fh.write(json.dumps({"type": "plan", **rec}, sort_keys=True) + "\n")
+            for rec in self.steps:
+                fh.write(json.dumps({"type": "step", **rec}, sort_keys=True) + "\n")
+
+    @staticmethod
+    def read_jsonl(path: str) -> "EpisodeLog":
+        meta, steps, plans = {}, [], []
+        with open(path, "r", encoding="utf-8") as fh:
+            for line in fh:
+                rec = json.loads(line)
+                kind = rec.pop("type")
+                if kind == "meta":
+                    meta = rec
+                elif kind == "step":
+                    steps.append(rec)
+                elif kind == "plan":
+                    plans.append(rec)
+        log = EpisodeLog(meta=meta, steps=steps, plan_records=plans)
+        log.collided = bool(meta.pop("collided", False))
+        log.collision_step = meta.pop("collision_step", None)
+        log.lane_departed = bool(meta.pop("lane_departed", False))
+        log.failed = bool(meta.pop("failed", False))
+        log.failure_reason = str(meta.pop("failure_reason", ""))
+        return log
+
+
+def _snapshot(rec: np.ndarray, nv: int) -> dict:
+    """The run_episode step record (pkg/highway.py:478-485) from a device snapshot row."""
+    nb = rec[SNAP_HEAD:SNAP_HEAD + 4 * nv].reshape(nv, 4)
+    return {"t": round(float(rec[0]), 6), "ego": [float(v) for v in rec[1:5]], "ctrl": [float(rec[5]), float(rec[6])],
+            "neighbors": [[float(v) for v in row] for row in nb], "collision": bool(rec[7] != 0.0)}
+
+
+def run_episodes(scenarios, planner, replan_stride: int = 5, road_end_margin: float = 60.0, device="cuda:0",
+                 record_steps: bool = True) -> list:
+    """run_episode (pkg/highway.py:487-532) for every scenario at once.
+
+    `planner` is a batch planner (:func:`.planners.make_batch_planner`); its failures end the
+    affected episode (failed=True, failure_reason "Type: message") and the others continue."""
+    scenarios = list(scenarios)
+    S = len(scenarios)
+    dts = {float(sc.dt) for sc in scenarios}
+    if len(dts) != 1:
+        raise ValueError("all scenarios of one batch must share dt")
+    dt = dts.pop()
+    if abs(planner.dt - dt) > 0:
+        raise ValueError(f"planner control grid dt={planner.dt} differs from the scenarios' dt={dt}")
+    if planner.n_ctrl < 1:
+        raise ValueError("planner horizon shorter than one tick")
+    host = SimState.spawn(scenarios)
+    road_host = host.road.copy()
+    n_veh = host.n_veh.copy()
+    st = host.to(device) if device is not None else host
+    sim = Simulator(planner.context, TrafficParams(dt=dt, wheelbase=planner.env.wheelbase))
+    planner.reset()
+    logs = [EpisodeLog(meta={"scenario": sc.to_dict(), "planner": planner.name, "replan_stride": replan_stride})
+            for sc in scenarios]
+    lengths = np.array([sc.episode_length for sc in scenarios])
+    x_end = np.array([sc.road.length - road_end_margin for sc in scenarios], dtype=np.float64)
+    active = (lengths > 0).astype(np.int32)
+    ctrl = None
+    k = offset = 0
+    while active.any():
+        if k % replan_stride == 0:
+            plan = planner.plan_cycle(st, road_host)
+            for s in np.flatnonzero(active):
+                if plan.failures[s] is not None:
+                    logs[s].failed = True
+                    logs[s].failure_reason = plan.failures[s]
+                    active[s] = 0
+                else:
+                    logs[s].plan_records.append({"step": int(k), **plan.infos[s]})
+            offset = 0
+            if not active.any():
+                break
+            ctrl = np.ascontiguousarray(np.stack([plan.accels, plan.steers], axis=-1))
+        n = replan_stride - (k % replan_stride)
+        n = int(min(n, (lengths[active.astype(bool)] - k).min()))
+        was = active.copy()
+        done, snap = sim.run(st, ctrl, n, ctrl_offset=offset, x_end=x_end, active=active, snapshots=record_steps)
+        for s in np.flatnonzero(was):
+            if record_steps:
+                logs[s].steps.extend(_snapshot(snap[s, j], int(n_veh[s])) for j in range(int(done[s])))
+        k += n
+        offset += n
+        active[(lengths <= k) & (active != 0)] = 0
+    w = st.world.cpu().numpy() if hasattr(st.world, "cpu") else st.world
+    for s, log in enumerate(logs):
+        if w[s, 2] != 0.0 and not log.failed:
+            log.collided = True
+            log.collision_step = int(w[s, 3])
+        log.lane_departed = bool(w[s, 4] != 0.0)
+    return logs
+
+
+# ----------------------------------------------------------------------------- suites
+@dataclass(frozen=True)
+class BenchmarkSuite:
+    """pkg/bench.py:32-52: every planner over the same (scenario, seed) cells."""
+
+    scenarios: tuple
+    planners: tuple
+    episodes_per_cell: int = 50
+    seeds: tuple = ()
+    env: PlannerEnvConfig = field(default_factory=PlannerEnvConfig)
+    replan_stride: int = 5
+    workers: int = 1
+
+    def __post_init__(self):
+        from .planners import BATCH_PLANNER_REGISTRY
+        unknown = [p for p in self.planners if p not in BATCH_PLANNER_REGISTRY]
+        if unknown:
+            raise ValueError(f"unknown planners in suite: {unknown}")
+        if not self.seeds:
+            object.__setattr__(self, "seeds", tuple(range(self.episodes_per_cell)))
+        if len(self.seeds) != self.episodes_per_cell:
+            raise ValueError("seed list length must equal episodes_per_cell")
+
+
+@dataclass
+class MetricsRow:
+    planner: str
+    scenario_id: str
+    episodes: int
+    collisions: int
+    collision_rate: float
+    mean_speed: float
+    mean_solve_time: float
+    failures: int
+
+    def metrics_csv(self) -> str:
+        return ",".join([self.planner, self.scenario_id, str(self.episodes), str(self.collisions),
+                         repr(self.collision_rate), repr(self.mean_speed), str(self.failures)])
+
+    def timing_csv(self, wall: float) -> str:
+        return ",".join([self.planner, self.scenario_id, repr(self.mean_solve_time), repr(wall)])
+
+
+def suite_from_dict(data: dict, workers: int | None = None) -> BenchmarkSuite:
+    env = PlannerEnvConfig(**data.get("env", {}))
+    return BenchmarkSuite(scenarios=tuple(ScenarioConfig.from_dict(sc) for sc in data["scenarios"]),
+                          planners=tuple(data["planners"]), episodes_per_cell=int(data.get("episodes_per_cell", 50)),
+                          seeds=tuple(data.get("seeds", ())), env=env,
+                          replan_stride=int(data.get("replan_stride", 5)),
+                          workers=workers if workers is not None else int(data.get("workers", 1)))
+
+
+def load_suite(path: str, workers: int | None = None) -> BenchmarkSuite:
+    import yaml
+    with open(path, "r", encoding="utf-8") as fh:
+        return suite_from_dict(yaml.safe_load(fh), workers=workers)
+
+
+def run_suite(suite: BenchmarkSuite, device="cuda:0"):
+    """run_suite (pkg/bench.py:114-170): per planner, every (scenario, seed) episode in one
+    lockstep batch (one batch per distinct dt).  Returns (rows, cell_wall, saw_numerical_failure);
+    an episode's wall time is its batch's wall time divided evenly over the batch."""
+    from dataclasses import replace
+    rows, cell_wall, saw_nf = [], {}, False
+    for pname in suite.planners:
+        cells = [(sc, seed) for sc in suite.scenarios for seed in suite.seeds]
+        results = [None] * len(cells)
+        for dt in sorted({float(sc.dt) for sc, _ in cells}):
+            idx = [i for i, (sc, _) in enumerate(cells) if float(sc.dt) == dt]
+            seeds = [cells[i][1] for i in idx]
+            planner = make_batch_planner(pname, suite.env, seed=seeds if pname == "mpc-random" else 0, dt=dt)
+            t0 = time.perf_counter()
+            logs = run_episodes([replace(cells[i][0], seed=cells[i][1]) for i in idx], planner,
+                                replan_stride=suite.replan_stride, device=device)
+            wall = (time.perf_counter() - t0) / len(idx)
+            for i, log in zip(idx, logs):
+                results[i] = {"wall": wall, "collided": log.collided, "failed": log.failed,
+                              "mean_speed": log.mean_speed(), "solve_times": log.solve_times(),
+                              "numerical_failure": "NumericalFailure" in log.failure_reason}
+        n = len(suite.seeds)
+        for c, sc in enumerate(suite.scenarios):
+            cell = results[c * n:(c + 1) * n]
+            collisions = sum(1 for r in cell if r["collided"])
+            saw_nf |= any(r["numerical_failure"] for r in cell)
+            clean = [r["mean_speed"] for r in cell if not r["collided"] and not r["failed"]]
+            st = [t for r in cell for t in r["solve_times"]]
+            rows.append(MetricsRow(pname, sc.scenario_id, len(cell), collisions, collisions / len(cell),
+                                   float(np.mean(clean)) if clean else float("nan"),
+                                   float(np.mean(st)) if st else float("nan"),
+                                   sum(1 for r in cell if r["failed"])))
+            cell_wall[f"{pname}/{sc.scenario_id}"] = float(sum(r["wall"] for r in cell))
+    return rows, cell_wall, saw_nf
+
+
+def _fingerprint(suite: BenchmarkSuite) -> str:
+    payload = {"planners": list(suite.planners), "scenarios": [sc.to_dict() for sc in suite.scenarios],
+               "episodes_per_cell": suite.episodes_per_cell, "seeds": list(suite.seeds),
+               "env": {k: getattr(suite.env, k) for k in sorted(vars(suite.env))},
+               "replan_stride": suite.replan_stride}
+    return hashlib.sha256(json.dumps(payload, sort_keys=True).encode()).hexdigest()
+
+
+def write_outputs(suite: BenchmarkSuite, rows, cell_wall: dict, out_dir: str, package_version: str | None = None):
+    """metrics.csv (byte-stable), timings.csv and manifest.json in the reference's format
+    (pkg/bench.py:173-205)."""
+    from . import __version__
+    os.makedirs(out_dir, exist_ok=True)
+    paths = {k: os.path.join(out_dir, f) for k, f in
+             (("metrics", "metrics.csv"), ("timings", "timings.csv"), ("manifest", "manifest.json"))}
+    with open(paths["metrics"], "w", encoding="utf-8") as fh:
+        fh.write(METRICS_HEADER + "\n")
+        for r in rows:
+            fh.write(r.metrics_csv() + "\n")
+    with open(paths["timings"], "w", encoding="utf-8") as fh:
+        fh.write(TIMINGS_HEADER + "\n")
+        for r in rows:
+            fh.write(r.timing_csv(cell_wall.get(f"{r.planner}/{r.scenario_id}", float("nan"))) + "\n")
+    manifest = {"config_hash": _fingerprint(suite), "seeds": list(suite.seeds),
+                "package_version": package_version or __version__, "numpy_version": np.__version__}
+    with open(paths["manifest"], "w", encoding="utf-8") as fh:
+        json.dump(manifest, fh, sort_keys=True, indent=2)
+        fh.write("\n")
+    return paths

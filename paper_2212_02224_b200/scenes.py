@@ -44,8 +44,8 @@ class HighwayRecipe:
     v_min: float = 0.5
 
 
-def _spawn(seed: int, r: HighwayRecipe):
-    """Neighbour (x, y, v) list of spawn_world (pkg/highway.py:168-205)."""
+def _spawn(seed: int, r: HighwayRecipe, with_cooldown: bool = False):
+    """Neighbour (x, y, v[, cooldown]) list of spawn_world (pkg/highway.py:168-205)."""
     rng = np.random.default_rng(seed)
     spacing = r.spawn_base_spacing / r.density
     cursor = [(25.0 if lane == r.ego_lane else -15.0) + spacing * 0.5 * rng.uniform(0.0, 1.0)
@@ -56,8 +56,9 @@ def _spawn(seed: int, r: HighwayRecipe):
         x = cursor[lane]
         cursor[lane] = x + spacing * rng.uniform(0.85, 1.15)
         v = r.neighbor_speed * (1.0 + 0.15 * rng.uniform(-1.0, 1.0))
-        rng.uniform(0.0, 2.0)   # lane-change cooldown draw of the simulator; keeps the stream aligned
-        cars.append((float(x), lane * r.lane_width, float(v)))
+        cooldown = float(rng.uniform(0.0, 2.0))   # lane-change cooldown (drawn even when unused: stream alignment)
+        cars.append((float(x), lane * r.lane_width, float(v), cooldown) if with_cooldown
+                    else (float(x), lane * r.lane_width, float(v)))
     return cars
 
 

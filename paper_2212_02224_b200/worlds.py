@@ -22,7 +22,7 @@ import numpy as np
 from ._native import Env, f64
 from .basis import PolynomialBasis
 
-__all__ = ["WorldBatch", "PlannerEnv", "build_scenes", "ControlEmitter"]
+__all__ = ["WorldBatch", "PlannerEnv", "build_scenes", "ControlEmitter", "env_struct"]
 
 
 @dataclass
@@ -83,11 +83,24 @@ def build_scenes(ctx, basis: PolynomialBasis, worlds: WorldBatch, env: PlannerEn
     m = basis.num_samples
     out = (np.empty((S, env.max_obstacles, m)), np.empty((S, env.max_obstacles, m)), np.empty((S, 6)),
            np.empty((S, 9)), np.empty((S, 55))) if outputs else (None,) * 5
-    cenv = env.c_struct()
-    ctx.call("bd_build_scenes", S, n_max, f64(worlds.ego), f64(worlds.veh),
-             np.ascontiguousarray(worlds.n_veh, dtype=np.int32), f64(worlds.road), ctypes.byref(cenv),
+    cenv = env_struct(env)
+    ctx.call("bd_build_scenes", S, n_max, _dev_or(worlds.ego, np.float64), _dev_or(worlds.veh, np.float64),
+             _dev_or(worlds.n_veh, np.int32), _dev_or(worlds.road, np.float64), ctypes.byref(cenv),
              f64(basis.times), *out)
     return out if outputs else None
+
+
+def _dev_or(a, dtype):
+    """Device tensors (e.g. the simulator's state) pass through; host data become contiguous arrays."""
+    return a if hasattr(a, "data_ptr") else np.ascontiguousarray(a, dtype=dtype)
+
+
+def env_struct(env) -> Env:
+    """bd_env from a PlannerEnv or any PlannerEnvConfig-like object (duck-typed fields)."""
+    if isinstance(env, PlannerEnv):
+        return env.c_struct()
+    return PlannerEnv(int(env.max_obstacles), float(env.obstacle_range), float(env.wheelbase), float(env.v_max),
+                      float(env.a_max), float(env.kappa_max), float(env.c_max), float(env.v_min)).c_struct()
 
 
 class ControlEmitter:
@@ -95,6 +108,7 @@ class ControlEmitter:
 
     def __init__(self, ctx, basis: PolynomialBasis, horizon: float, dt: float, env: PlannerEnv, eps_v: float = 1e-3):
         self.ctx = ctx
+        self.eps_v = float(eps_v)
         self.n_ctrl = int(horizon / dt)
         self.times = np.arange(self.n_ctrl) * dt
         _, Wd, Wdd = basis.matrices_at(self.times)       # host fp64 setup, once

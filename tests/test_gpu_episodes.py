@@ -1,0 +1,132 @@
+"""GPU: closed-loop episodes on the device simulator.
+
+* Scripted planners: the batched run_episodes reproduces the reference's run_episode logs
+  (tests/golden/episodes.npz: step records, collisions, road-end stop, episode length).
+* Real planners: every batch planner drives a short fleet of episodes through the device
+  scene build -> solve -> controls -> simulator loop; suite outputs are well formed.
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+from tests.golden_io import load
+
+pytestmark = pytest.mark.gpu
+
+
+class ScriptedBatchPlanner:
+    """Batch-planner interface with the scripted controls of tools/gen_golden.py (per world)."""
+
+    name = "scripted"
+
+    def __init__(self, kinds, ctx):
+        from paper_2212_02224_b200.planners import PlannerEnvConfig
+        self.kinds, self.context, self.env = kinds, ctx, PlannerEnvConfig()
+        self.dt, self.n_ctrl, self.c = 0.1, 50, 0
+
+    def reset(self):
+        self.c = 0
+
+    def plan_cycle(self, st, road):
+        from paper_2212_02224_b200.planners import CyclePlan
+        ctl = np.array([_controls(k, self.c) for k in self.kinds])
+        S = len(self.kinds)
+        self.c += 1
+        return CyclePlan(np.repeat(ctl[:, :1], 50, 1), np.repeat(ctl[:, 1:], 50, 1),
+                         [{"cycle": self.c - 1}] * S, [None] * S, 0.0)
+
+
+def _controls(kind, c):
+    if kind == "cruise":
+        return 0.5 * np.sin(0.7 * c), 0.02 * np.cos(0.3 * c)
+    if kind == "ram":
+        return 3.0, 0.0
+    return 1.0, 0.0
+
+
+def test_scripted_episodes_match_reference_run_episode(tmp_path):
+    from paper_2212_02224_b200._native import Context
+    from paper_2212_02224_b200.episodes import EpisodeLog, run_episodes
+    from paper_2212_02224_b200.sim import RoadSpec, ScenarioConfig
+    g = load("episodes")
+    n = int(g["n_cases"])
+    scs, kinds, refs = [], [], []
+    for k in range(n):
+        lanes, dens, nveh, seed, length, road_len = g[f"e{k}_cfg"]
+        scs.append(ScenarioConfig(RoadSpec(int(lanes), length=float(road_len)), float(dens), int(nveh), int(seed),
+                                  episode_length=int(length), scenario_id=f"case{k}"))
+        kinds.append(str(g[f"e{k}_kind"]))
+        p = tmp_path / f"r{k}.jsonl"
+        p.write_text(str(g[f"e{k}_jsonl"]))
+        refs.append(EpisodeLog.read_jsonl(str(p)))
+    logs = run_episodes(scs, ScriptedBatchPlanner(kinds, Context(0)), replan_stride=5)
+    for log, ref in zip(logs, refs):
+        assert (log.collided, log.collision_step, log.lane_departed, log.failed) == \
+            (ref.collided, ref.collision_step, ref.lane_departed, ref.failed)
+        assert log.meta["scenario"] == ref.meta["scenario"] and log.meta["replan_stride"] == 5
+        assert log.plan_records == ref.plan_records
+        assert len(log.steps) == len(ref.steps)
+        for a, b in zip(log.steps, ref.steps):
+            assert a["t"] == b["t"] and a["ctrl"] == b["ctrl"] and a["collision"] == b["collision"]
+            np.testing.assert_allclose(a["ego"], b["ego"], rtol=1e-12, atol=1e-9)
+            np.testing.assert_allclose(np.array(a["neighbors"]), np.array(b["neighbors"]), rtol=1e-12, atol=1e-9)
+        assert log.mean_speed() == pytest.approx(ref.mean_speed(), rel=1e-12)
+
+
+def _small_env(**kw):
+    from paper_2212_02224_b200.planners import PlannerEnvConfig
+    base = dict(batch_size=200, constraint_elites=60, elites=30, iterations=2, proj_iters=20)
+    base.update(kw)
+    return PlannerEnvConfig(**base)
+
+
+@pytest.mark.parametrize("name", ["mpc-bilevel", "mpc-vanilla", "mpc-random", "mpc-grid", "batch-mpc-goal"])
+def test_batch_planners_drive_closed_loop(name):
+    from paper_2212_02224_b200.episodes import run_episodes
+    from paper_2212_02224_b200.planners import make_batch_planner
+    from paper_2212_02224_b200.sim import RoadSpec, ScenarioConfig
+    scs = [ScenarioConfig(RoadSpec(3), 1.5, 20, s, episode_length=25, scenario_id="x") for s in range(6)]
+    planner = make_batch_planner(name, _small_env(), seed=list(range(6)) if name == "mpc-random" else 0)
+    logs = run_episodes(scs, planner, replan_stride=5)
+    for log in logs:
+        assert not log.failed, log.failure_reason
+        assert [r["step"] for r in log.plan_records] == list(range(0, len(log.steps), 5))[:len(log.plan_records)]
+        assert len(log.steps) == 25 or log.collided
+        if log.collided:
+            assert log.steps[-1]["collision"] and log.collision_step == len(log.steps)
+        for r in log.plan_records:
+            assert np.isfinite(r["residual"]) and np.isfinite(r["upper_cost"]) and r["solve_time"] > 0
+        sp = log.ego_speeds()
+        assert np.all(np.isfinite(sp)) and np.all(sp >= 0)
+    # the planner moved the ego forward in every episode
+    assert all(log.steps[-1]["ego"][0] > 10.0 for log in logs)
+
+
+def test_bilevel_warm_start_and_reset():
+    from paper_2212_02224_b200.episodes import run_episodes
+    from paper_2212_02224_b200.planners import make_batch_planner
+    from paper_2212_02224_b200.sim import RoadSpec, ScenarioConfig
+    scs = [ScenarioConfig(RoadSpec(4), 2.0, 24, s, episode_length=10) for s in range(3)]
+    planner = make_batch_planner("mpc-bilevel", _small_env())
+    a = run_episodes(scs, planner, replan_stride=5)
+    b = run_episodes(scs, planner, replan_stride=5)      # reset() restores cycle counter + warm mean
+    for x, y in zip(a, b):
+        assert x.steps == y.steps and [r["residual"] for r in x.plan_records] == [r["residual"] for r in y.plan_records]
+
+
+def test_run_suite_outputs(tmp_path):
+    from paper_2212_02224_b200.episodes import BenchmarkSuite, run_suite, write_outputs
+    from paper_2212_02224_b200.sim import RoadSpec, ScenarioConfig
+    suite = BenchmarkSuite(scenarios=(ScenarioConfig(RoadSpec(3), 1.5, 20, 0, episode_length=15, scenario_id="s3"),
+                                      ScenarioConfig(RoadSpec(4), 2.0, 24, 0, episode_length=15, scenario_id="s4")),
+                           planners=("mpc-bilevel", "mpc-vanilla"), episodes_per_cell=3, env=_small_env())
+    rows, walls, nf = run_suite(suite)
+    assert [(r.planner, r.scenario_id) for r in rows] == [("mpc-bilevel", "s3"), ("mpc-bilevel", "s4"),
+                                                          ("mpc-vanilla", "s3"), ("mpc-vanilla", "s4")]
+    assert all(r.episodes == 3 and 0 <= r.collisions <= 3 and r.failures == 0 for r in rows) and not nf
+    paths = write_outputs(suite, rows, walls, str(tmp_path))
+    lines = open(paths["metrics"]).read().splitlines()
+    assert lines[0] == "planner,scenario,episodes,collisions,collision_rate,mean_speed,failures" and len(lines) == 5
+    assert len(json.load(open(paths["manifest"]))["config_hash"]) == 64

@@ -13,11 +13,15 @@ Cases:
   cem_c2           teacher-forced config-2 CEM trace (B=1000, N=4, n=150, q=100) via trace_hook
                    (pkg/bilevel.py:269-270)
   cem_small        free-running solve_bilevel with default_rng(3) (B=200, N=3) for the drop-in API
+  worlds           build_scene / observe / controls_on_grid outputs
+  sim              simulator ticks: spawn_world + step
+  episodes         run_episode with scripted planners (EpisodeLog JSONL) + suite output files
 """
 
 from __future__ import annotations
 
 import argparse
+import json
 import math
 import os
 import sys
@@ -320,13 +324,140 @@ def gen_worlds():
     print(f"worlds written ({k} worlds, {xis.shape[1]} control sets, {sum(sing)} singular)")
 
 
+SIM_CASES = (  # lanes, density, vehicles, seed, steps, control script
+    (4, 2.0, 24, 0, 60, "gentle"), (3, 1.5, 30, 4, 80, "gentle"), (4, 3.0, 80, 3, 40, "gentle"),
+    (2, 1.0, 12, 2, 60, "ram"), (2, 0.4, 3, 5, 50, "swerve"), (4, 2.5, 40, 7, 100, "weave"),
+)
+
+
+def sim_controls(kind, t):
+    if kind == "gentle":
+        return 0.8 * np.sin(0.3 * t), 0.03 * np.cos(0.2 * t)
+    if kind == "ram":
+        return 3.0, 0.0
+    if kind == "swerve":
+        return 0.5, 0.12
+    return 1.2 * np.sin(0.11 * t), 0.08 * np.sin(0.05 * t)       # weave
+
+
+def gen_sim():
+    """Closed-loop simulator ticks (pkg/highway.py:358-410): spawned world state (pkg/highway.py:168-205)
+    and the full world state after every step under scripted ego controls (IDM + MOBIL neighbours,
+    RK4 ego, SAT collision, lane departure)."""
+    from bilevel_drive.highway import step
+    out = {}
+    changes = 0
+    for k, (lanes, dens, nveh, seed, nsteps, kind) in enumerate(SIM_CASES):
+        world = spawn_world(ScenarioConfig(RoadSpec(lane_count=lanes), density=dens, vehicle_count=nveh, seed=seed))
+
+        def grab():
+            e = world.ego
+            ego = np.array([e.x, e.y, e.psi, e.v, e.accel, e.steer, e.length, e.width, e.target_speed])
+            veh = np.array([[v.x, v.y, v.psi, v.v, v.lateral_rate, v.length, v.width, v.target_speed,
+                             v.target_lane, v.cooldown, v.accel, v.lane_index] for v in world.neighbors])
+            ws = np.array([world.time, world.step_count, float(world.collided),
+                           -1.0 if world.collision_step is None else float(world.collision_step),
+                           float(world.lane_departed)])
+            return ego, veh, ws
+
+        e0, v0, w0 = grab()
+        egos, vehs, wss, ctrl = [], [], [], []
+        for t in range(nsteps):
+            a, d = sim_controls(kind, t)
+            before = [v.target_lane for v in world.neighbors]
+            step(world, float(a), float(d))
+            changes += sum(b != v.target_lane for b, v in zip(before, world.neighbors))
+            e, v, w = grab()
+            egos.append(e); vehs.append(v); wss.append(w); ctrl.append((a, d))
+        out[f"s{k}_road"] = np.array([lanes, world.road.lane_width, world.road.length, world.dt])
+        out[f"s{k}_ego0"], out[f"s{k}_veh0"], out[f"s{k}_w0"] = e0, v0, w0
+        out[f"s{k}_ego"], out[f"s{k}_veh"], out[f"s{k}_w"] = np.array(egos), np.array(vehs), np.array(wss)
+        out[f"s{k}_ctrl"] = np.array(ctrl, dtype=float)
+        out[f"s{k}_cfg"] = np.array([lanes, dens, nveh, seed, nsteps])
+        print(f"  sim case {k}: collided={world.collided} at {world.collision_step}, departed={world.lane_departed}")
+    out["n_cases"] = len(SIM_CASES)
+    np.savez_compressed(os.path.join(OUT, "sim.npz"), **out)
+    print(f"sim written ({len(SIM_CASES)} worlds, {changes} neighbour lane-change decisions)")
+
+
+class _ScriptedPlanner:
+    """Dummy planner for run_episode: cycle c returns constant (accel, steer) grids."""
+
+    name = "scripted"
+
+    def __init__(self, kind):
+        self.kind = kind
+        self.c = 0
+
+    def reset(self):
+        self.c = 0
+
+    def plan_cycle(self, world):
+        a, d = episode_controls(self.kind, self.c)
+        self.c += 1
+        return np.full(50, a), np.full(50, d), {"cycle": self.c - 1}
+
+
+def episode_controls(kind, c):
+    if kind == "cruise":
+        return 0.5 * np.sin(0.7 * c), 0.02 * np.cos(0.3 * c)
+    if kind == "ram":
+        return 3.0, 0.0
+    return 1.0, 0.0                                                      # "run": to the end of the road
+
+
+EPISODE_CASES = (  # lanes, density, vehicles, seed, episode_length, road_length, planner kind
+    (4, 2.0, 24, 0, 60, 1500.0, "cruise"), (2, 1.0, 12, 2, 150, 1500.0, "ram"),
+    (3, 1.5, 20, 5, 150, 140.0, "run"), (4, 2.5, 40, 7, 23, 1500.0, "cruise"),
+)
+
+
+def gen_episodes():
+    """Closed-loop run_episode (pkg/highway.py:487-532) with scripted planners: EpisodeLog JSONL
+    (pkg/highway.py:436-474); plus suite outputs of write_outputs (pkg/bench.py:173-205)."""
+    import tempfile
+    from dataclasses import replace
+    from bilevel_drive import bench as rbench
+    from bilevel_drive.highway import run_episode
+    out = {}
+    for k, (lanes, dens, nveh, seed, length, road_len, kind) in enumerate(EPISODE_CASES):
+        sc = ScenarioConfig(RoadSpec(lane_count=lanes, length=road_len), density=dens, vehicle_count=nveh,
+                            seed=seed, episode_length=length, scenario_id=f"case{k}")
+        log = run_episode(sc, _ScriptedPlanner(kind), replan_stride=5)
+        with tempfile.TemporaryDirectory() as d:
+            path = os.path.join(d, "ep.jsonl")
+            log.write_jsonl(path)
+            out[f"e{k}_jsonl"] = np.array(open(path).read())
+        out[f"e{k}_cfg"] = np.array([lanes, dens, nveh, seed, length, road_len])
+        out[f"e{k}_kind"] = np.array(kind)
+        print(f"  episode {k}: steps={len(log.steps)} collided={log.collided} departed={log.lane_departed}")
+    out["n_cases"] = len(EPISODE_CASES)
+    # suite outputs for fixed metric rows (byte format + config fingerprint)
+    env = rbench.PlannerEnvConfig(batch_size=100, iterations=3)
+    suite = rbench.BenchmarkSuite(scenarios=(ScenarioConfig(RoadSpec(lane_count=3), 1.5, 20, 0, scenario_id="a"),
+                                             ScenarioConfig(RoadSpec(lane_count=4), 2.0, 24, 0, scenario_id="b")),
+                                  planners=("mpc-bilevel", "mpc-vanilla"), episodes_per_cell=3, env=env)
+    rows = [rbench.MetricsRow("mpc-bilevel", "a", 3, 1, 1 / 3, 11.25, 0.0123, 0),
+            rbench.MetricsRow("mpc-bilevel", "b", 3, 0, 0.0, float("nan"), float("nan"), 3),
+            rbench.MetricsRow("mpc-vanilla", "a", 3, 2, 2 / 3, 9.876543210123, 0.5, 1),
+            rbench.MetricsRow("mpc-vanilla", "b", 3, 0, 0.0, 12.0, 1e-4, 0)]
+    walls = {"mpc-bilevel/a": 1.5, "mpc-bilevel/b": 2.25, "mpc-vanilla/a": 0.1}
+    with tempfile.TemporaryDirectory() as d:
+        paths = rbench.write_outputs(suite, rows, walls, d)
+        out["suite_metrics"] = np.array(open(paths["metrics"]).read())
+        out["suite_timings"] = np.array(open(paths["timings"]).read())
+        out["suite_hash"] = np.array(json.load(open(paths["manifest"]))["config_hash"])
+    np.savez_compressed(os.path.join(OUT, "episodes.npz"), **out)
+    print("episodes written")
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", nargs="*", default=None)
     a = ap.parse_args()
     os.makedirs(OUT, exist_ok=True)
     jobs = {"basis": gen_basis, "lower": gen_lower, "scenes": gen_scenes, "cem_small": gen_cem_small,
-            "cem_c2": gen_cem_c2, "worlds": gen_worlds}
+            "cem_c2": gen_cem_c2, "worlds": gen_worlds, "sim": gen_sim, "episodes": gen_episodes}
     for name, fn in jobs.items():
         if a.only is None or name in a.only:
             fn()
