@@ -238,6 +238,29 @@ def dense_config4(device: int, steps: int = 3):
             "config": "1 scene, B=10000, 50 obstacles, 4 CEM iterations, 100 AM iterations (1 GPU)"}
 
 
+def closed_loop_suite(device: int, episodes: int = 64, length: int = 150):
+    """a fleet of closed-loop episodes (run_episode semantics, replan every 5 ticks)
+    with the reference planner's default configuration (PlannerEnvConfig: B=250, N=5, m=50 over 10 s,
+    6 obstacles, 50 AM iterations): device scene build -> CEM -> controls -> simulator, one batched
+    call per replan instant.  Host wall clock around the whole run (logs included)."""
+    from paper_2212_02224_b200.episodes import run_episodes
+    from paper_2212_02224_b200.planners import PlannerEnvConfig, make_batch_planner
+    from paper_2212_02224_b200.sim import RoadSpec, ScenarioConfig
+    scs = [ScenarioConfig(RoadSpec(4), 2.0, 24, s, episode_length=length) for s in range(episodes)]
+    planner = make_batch_planner("mpc-bilevel", PlannerEnvConfig(), device=device)
+    run_episodes(scs[:4], planner, device=f"cuda:{device}")            # warm-up (allocations, first launches)
+    t0 = time.perf_counter()
+    logs = run_episodes(scs, planner, device=f"cuda:{device}")
+    wall = time.perf_counter() - t0
+    ticks = sum(len(lg.steps) for lg in logs)
+    cycles = sum(len(lg.plan_records) for lg in logs)
+    return {"episodes_per_s": episodes / wall, "ticks_per_s": ticks / wall, "plans_per_s": cycles / wall,
+            "wall_s": wall, "ticks": ticks, "collisions": sum(lg.collided for lg in logs),
+            "failures": sum(lg.failed for lg in logs),
+            "config": f"{episodes} episodes x {length} ticks (dt 0.1 s, replan every 5), 4-lane highway, 24 "
+                      "neighbours; mpc-bilevel with PlannerEnvConfig defaults; host wall clock incl. step records"}
+
+
 def run_b200(args, rank: int, world: int, dist):
     import torch
 
@@ -363,6 +386,7 @@ def run_b200(args, rank: int, world: int, dist):
         line["cem_cycle_latency"] = cem_latency(dev)
         line["dense_config4"] = dense_config4(dev)
         line["cvae_config3_latency"] = cvae_config3(dev)
+        line["closed_loop_suite"] = closed_loop_suite(dev)
         ref, _ = cpu_reference(steps=2, warmup=1)
         line["cpu_baseline"] = ref
     print(json.dumps(line), flush=True)
