@@ -347,7 +347,7 @@ def run_b200(args, rank: int, world: int, dist):
         e2e_s = float(t.item())
     h2d = worlds.ego.nbytes + worlds.veh.nbytes + worlds.n_veh.nbytes + worlds.road.nbytes + M * 8 + S * (8 + 64) * 8
     d2h = res.best_index.nbytes + res.best_params.nbytes + res.best_xi.nbytes + 3 * S * 8 + res.stats.nbytes + \
-        res.final_mean.nbytes + res.final_cov.nbytes + res.iterations_done.nbytes + acc.nbytes + ste.nbytes + S * 4
+        res.final_mean.nbytes + res.final_cov.nbytes + res.iterations_done.nbytes + acc.nbytes + ste.nbytes + S * 4 + S * 6 * 8
 
     if rank != 0:
         return

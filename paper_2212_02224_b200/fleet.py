@@ -100,16 +100,19 @@ class FleetPlanner:
         device scene build -> device CEM cycle -> device control emission of each best trajectory.
         Returns (accels, steers, singular, FleetResult); world arrays in, controls out."""
         from .worlds import build_scenes
-        build_scenes(self.context, self.solver.basis, worlds, env)
+        b0 = build_scenes(self.context, self.solver.basis, worlds, env, b0_only=True)
         self._scenes_key = ("worlds", id(worlds))
         self.solver.projector._scene_key = None
+        # BasePlanner.initial_distribution (pkg/planners.py:218-231) on the device-built initial
+        # states: nearest lane centre to y0, speed = hypot(xdot0, ydot0)
         ms = self.layout.m_seg
-        # BasePlanner.initial_distribution (pkg/planners.py:218-231): nearest lane centre, current speed
-        y0, v0 = worlds.ego[:, 1], worlds.ego[:, 3]
-        lanes, lw = worlds.road[:, 0].astype(int), worlds.road[:, 1]
-        lane_y = np.array([(np.arange(n) * w)[np.argmin(np.abs(np.arange(n) * w - y))] for n, w, y in zip(lanes, lw, y0)])
-        S = worlds.size
-        mean = np.concatenate([np.repeat(lane_y[:, None], ms, 1), np.repeat(np.abs(v0)[:, None], ms, 1)], axis=1)
+        S = b0.shape[0]
+        road = np.asarray(worlds.road.cpu() if hasattr(worlds.road, "cpu") else worlds.road)
+        mean = np.empty((S, 2 * ms))
+        for s in range(S):
+            c = np.arange(int(road[s, 0])) * road[s, 1]
+            lane_y = float(c[np.argmin(np.abs(c - b0[s, 1]))]) if c.size else b0[s, 1]
+            mean[s] = np.concatenate([np.full(ms, lane_y), np.full(ms, float(np.hypot(b0[s, 2], b0[s, 3])))])
         cov = np.repeat(np.diag(np.concatenate([np.full(ms, sigma_offset ** 2), np.full(ms, sigma_speed ** 2)]))[None],
                         S, axis=0)
         dim, N, n2 = self.layout.dim, self.config.iterations, 2 * self.solver.basis.num_coeffs

@@ -35,7 +35,7 @@ from .behavior import ParamLayout
 from .bilevel import BiLevelConfig, LowerLevelSolver, SamplingDistribution
 from .fleet import FleetPlanner, FleetResult
 from .projection import ProjectionConfig
-from .worlds import ControlEmitter, _dev_or, env_struct
+from .worlds import ControlEmitter, build_scenes
 
 __all__ = ["PlannerEnvConfig", "PlannerFailure", "BatchMPCBiLevelPlanner", "BatchMPCVanillaPlanner",
            "BatchMPCRandomPlanner", "BatchMPCGridPlanner", "BatchMPCGoalPlanner", "BATCH_PLANNER_REGISTRY",
@@ -118,7 +118,6 @@ class _BatchPlanner:
         self.n_ctrl = int(env.horizon / dt)
         self._setup(device)
         self.emitter = ControlEmitter(self.context, self.basis, env.horizon, dt, env)
-        self._cenv = env_struct(env)
         self.cycle = 0
 
     def _weights(self) -> TrackingWeights:
@@ -129,12 +128,7 @@ class _BatchPlanner:
 
     # -- scene build from the simulator state (pkg/planners.py:99-160), b0 back to the host
     def _build(self, worlds) -> np.ndarray:
-        S = int(worlds.ego.shape[0])
-        b0 = np.empty((S, 6))
-        self.context.call("bd_build_scenes", S, int(worlds.veh.shape[1]), _dev_or(worlds.ego, np.float64),
-                          _dev_or(worlds.veh, np.float64), _dev_or(worlds.n_veh, np.int32),
-                          _dev_or(worlds.road, np.float64), ctypes.byref(self._cenv), f64(self.basis.times),
-                          None, None, b0, None, None)
+        b0 = build_scenes(self.context, self.basis, worlds, self.env, b0_only=True)
         self._invalidate_scene_cache()
         return b0
 

@@ -76,18 +76,22 @@ class PlannerEnv:
                    self.c_max, self.v_min, 5.0, 2.0)
 
 
-def build_scenes(ctx, basis: PolynomialBasis, worlds: WorldBatch, env: PlannerEnv, outputs: bool = False):
+def build_scenes(ctx, basis: PolynomialBasis, worlds: WorldBatch, env: PlannerEnv, outputs: bool = False,
+                 b0_only: bool = False):
     """Build S scenes on the device into `ctx` (replacing its scenes).  With outputs=True also
-    return (ox, oy, b0, limits, observations) as host arrays."""
+    return (ox, oy, b0, limits, observations) as host arrays; with b0_only=True return just the
+    initial states b0 (S x 6, ego_flat_state)."""
     S, n_max = worlds.size, worlds.veh.shape[1]
     m = basis.num_samples
     out = (np.empty((S, env.max_obstacles, m)), np.empty((S, env.max_obstacles, m)), np.empty((S, 6)),
            np.empty((S, 9)), np.empty((S, 55))) if outputs else (None,) * 5
+    if b0_only and not outputs:
+        out = (None, None, np.empty((S, 6)), None, None)
     cenv = env_struct(env)
     ctx.call("bd_build_scenes", S, n_max, _dev_or(worlds.ego, np.float64), _dev_or(worlds.veh, np.float64),
              _dev_or(worlds.n_veh, np.int32), _dev_or(worlds.road, np.float64), ctypes.byref(cenv),
              f64(basis.times), *out)
-    return out if outputs else None
+    return out if outputs else (out[2] if b0_only else None)
 
 
 def _dev_or(a, dtype):
