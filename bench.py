@@ -246,7 +246,7 @@ def closed_loop_suite(device: int, episodes: int = 64, length: int = 150):
     from paper_2212_02224_b200.episodes import run_episodes
     from paper_2212_02224_b200.planners import PlannerEnvConfig, make_batch_planner
     from paper_2212_02224_b200.sim import RoadSpec, ScenarioConfig
-    scs = [ScenarioConfig(RoadSpec(4), 2.0, 24, s, episode_length=length) for s in range(episodes)]
+    scs = [ScenarioConfig(RoadSpec(4), 1.0, 12, s, episode_length=length) for s in range(episodes)]
     planner = make_batch_planner("mpc-bilevel", PlannerEnvConfig(), device=device)
     run_episodes(scs[:4], planner, device=f"cuda:{device}")            # warm-up (allocations, first launches)
     t0 = time.perf_counter()
@@ -257,7 +257,7 @@ def closed_loop_suite(device: int, episodes: int = 64, length: int = 150):
     return {"episodes_per_s": episodes / wall, "ticks_per_s": ticks / wall, "plans_per_s": cycles / wall,
             "wall_s": wall, "ticks": ticks, "collisions": sum(lg.collided for lg in logs),
             "failures": sum(lg.failed for lg in logs),
-            "config": f"{episodes} episodes x {length} ticks (dt 0.1 s, replan every 5), 4-lane highway, 24 "
+            "config": f"{episodes} episodes x {length} ticks (dt 0.1 s, replan every 5), 4-lane highway, density 1, 12 "
                       "neighbours; mpc-bilevel with PlannerEnvConfig defaults; host wall clock incl. step records"}
 
 
