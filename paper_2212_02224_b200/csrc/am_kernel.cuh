@@ -340,15 +340,26 @@ __global__ void __launch_bounds__(256, BD_AM_MINB) am_kernel(const AmArgs a) {
     double* asm_ = reinterpret_cast<double*>(smem + lay.a);
     float* csm = reinterpret_cast<float*>(smem + lay.curv);
 
-    // ---- stage constants and the scene tile once per CTA
-    for (int i = threadIdx.x; i < m * WROW / 4; i += threads)
-        reinterpret_cast<float4*>(wsm)[i] = reinterpret_cast<const float4*>(a.wrow)[i];
-    const float4* og = reinterpret_cast<const float4*>(a.obs) + (size_t)scene * (n_obs / 2) * m;
-    for (int i = threadIdx.x; i < (n_obs / 2) * m; i += threads) osm[i] = og[i];
+    // ---- stage constants and the scene tile once per CTA: the basis rows and this scene's
+    //      obstacle tile arrive by TMA bulk copy (one mbarrier), the small fp64 blocks by the threads
+    __shared__ __align__(8) uint64_t stage_bar;
+    const uint32_t w_bytes = (uint32_t)m * WROW * 4, o_bytes = (uint32_t)(n_obs / 2) * m * 16;
+    if (threadIdx.x == 0) {
+        mbar_init(&stage_bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        mbar_expect_tx(&stage_bar, w_bytes + o_bytes);
+        bulk_load(wsm, a.wrow, w_bytes, &stage_bar);
+        if (o_bytes) bulk_load(osm, reinterpret_cast<const float4*>(a.obs) + (size_t)scene * (n_obs / 2) * m, o_bytes,
+                               &stage_bar);
+    }
     for (int i = threadIdx.x; i < 2 * NC * KROW; i += threads) ksm[i] = a.kblk[i];
     for (int i = threadIdx.x; i < NX * neq; i += threads) { kbsm[i] = a.kb[i]; asm_[i] = a.aeq[i]; }
     if (CURV)
         for (int i = threadIdx.x; i < 2 * a.n_curv; i += threads) csm[i] = a.curv[(size_t)scene * 2 * a.n_curv + i];
+    mbar_wait(&stage_bar, 0);
     __syncthreads();
 
     const int lane = threadIdx.x & 31;
