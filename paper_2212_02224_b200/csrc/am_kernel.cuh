@@ -209,6 +209,7 @@ __device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float
         const float gap = fabsf(sa * cv - ca * sv);                   // |sin(alpha_a - alpha_v)|
         // coupled clip window (pkg/projection.py:138-169)
         const int di = j * dstride;
+        BD_CHECK(j < (m + P - 1) / P && t < m);
         const float da_prev = INIT ? fminf(fmaxf(da, 0.f), L.a_max) : dap[di];
         float vhi = L.v_max;
         float kcur = 0.f;
@@ -270,9 +271,6 @@ __device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float
         const float2 ro = make_float2(L.a * rox, fmaf(L.b, roy, up - lo));
         // back-projection g += Wd^T r_v + Wdd^T r_a + W^T r_o (+ lane); the basis row is re-read
         // from shared memory rather than held across the clip/obstacle section (register budget)
-#if BD_AM_RELOAD_W
-        asm volatile("" ::: "memory");
-#endif
 #pragma unroll
         for (int q = 0; q < WROW / 4; ++q) {
             const float4 f = wr[q];
@@ -307,9 +305,6 @@ __device__ __forceinline__ void pair_sync() {
     asm volatile("bar.sync %0, 64;" ::"r"(1 + (int)(threadIdx.x >> 6)) : "memory");
 }
 
-#ifndef BD_AM_RELOAD_W
-#define BD_AM_RELOAD_W 0
-#endif
 #ifndef BD_AM_MINB
 #define BD_AM_MINB 2       // x 256 threads: 128 registers per thread
 #endif

@@ -3,6 +3,20 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
+
+// Device-side bounds / invariant checks (build with -DBD_CHECKS=1; tools/build_variant.sh checks
+// "-DBD_CHECKS=1").  Off in the product build.
+#ifndef BD_CHECKS
+#define BD_CHECKS 0
+#endif
+#define BD_CHECK(cond)                                                                     \
+    do {                                                                                   \
+        if (BD_CHECKS && !(cond)) {                                                        \
+            printf("BD_CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #cond);             \
+            __trap();                                                                      \
+        }                                                                                  \
+    } while (0)
 
 namespace bd {
 

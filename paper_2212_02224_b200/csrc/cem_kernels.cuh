@@ -17,24 +17,9 @@ __device__ __forceinline__ unsigned long long ordered_bits(double x) {
     return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
 
-// In-place ascending bitonic sort of (key, idx) pairs in shared memory, ties by idx
-// (== np.argsort(kind="stable") / np.lexsort((idx, key)) on distinct indices).
-__device__ void block_bitonic_sort(unsigned long long* key, int* idx, int n_pow2) {
-    for (int k = 2; k <= n_pow2; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = threadIdx.x; i < n_pow2; i += blockDim.x) {
-                const int l = i ^ j;
-                if (l > i) {
-                    const unsigned long long ki = key[i], kl = key[l];
-                    const int ii = idx[i], il = idx[l];
-                    const bool gt = (ki > kl) || (ki == kl && ii > il);
-                    if (gt == ((i & k) == 0)) { key[i] = kl; key[l] = ki; idx[i] = il; idx[l] = ii; }
-                }
-            }
-            __syncthreads();
-        }
-    }
-}
+// aug = c + w r with numpy's rounding (no FMA contraction), so near-ties order as in
+// rank_samples (pkg/bilevel.py:134-135).
+__device__ __forceinline__ double aug_cost(double c, double w, double r) { return __dadd_rn(c, __dmul_rn(w, r)); }
 
 // Warp-cooperative Cholesky of a dim x dim SPD matrix held in shared memory (row-major, fp64):
 // column j: lane 0 forms the pivot, lanes i > j the sub-diagonal entries.  Returns false (in
@@ -214,6 +199,7 @@ __global__ void __launch_bounds__(256) rank_count_kernel(const double* resid, co
         cnt += (kj < ki) || (kj == ki && j < i);
     }
     for (int o = 16; o >= 1; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    BD_CHECK(cnt >= 0 && cnt < B);
     if (lane == 0) order[(size_t)scene * B + cnt] = i;
 }
 
@@ -251,7 +237,8 @@ __global__ void __launch_bounds__(1024) rank_refit_kernel(CemState s, int it, co
     // constraint elites: first n of the stable residual order; aug = cost + w r
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         const int j = ord[i];
-        key2[i] = ordered_bits(s.cost[base + j] + s.w_res * s.resid[base + j]);
+        BD_CHECK(j >= 0 && j < s.B);
+        key2[i] = ordered_bits(aug_cost(s.cost[base + j], s.w_res, s.resid[base + j]));
         cidx[i] = j;
         if (s.cons_idx) s.cons_idx[(size_t)scene * n + i] = j;
     }
@@ -262,18 +249,19 @@ __global__ void __launch_bounds__(1024) rank_refit_kernel(CemState s, int it, co
         const int ji = cidx[i];
         int rk = 0;
         for (int k = 0; k < n; ++k) rk += (key2[k] < ki) || (key2[k] == ki && cidx[k] < ji);
+        BD_CHECK(rk >= 0 && rk < n);
         idx2[rk] = ji;
     }
     __syncthreads();
     // elite weights exp(-(aug - min aug)/gamma), uniform fallback (pkg/bilevel.py:163-172)
     const int j0 = idx2[0];
-    const double amin = s.cost[base + j0] + s.w_res * s.resid[base + j0];
+    const double amin = aug_cost(s.cost[base + j0], s.w_res, s.resid[base + j0]);
     double part = 0.0, cpart = 0.0;
     const bool staged = q <= 128;
     __syncthreads();
     for (int i = threadIdx.x; i < q; i += blockDim.x) {
         const int j = idx2[i];
-        const double aug = s.cost[base + j] + s.w_res * s.resid[base + j];
+        const double aug = aug_cost(s.cost[base + j], s.w_res, s.resid[base + j]);
         const double wi = exp(-(aug - amin) / s.gamma);
         w[i] = wi;
         part += wi;

@@ -82,6 +82,7 @@ __global__ void __launch_bounds__(256) build_scene_kernel(const SceneBuildArgs a
     for (int e = threadIdx.x; e < a.n_obs * a.m; e += blockDim.x) {
         const int i = e / a.m, t = e % a.m;
         const int j = slot_obs[i];
+        BD_CHECK(j < nv);
         double ox, oy;
         if (j >= 0) {
             ox = __dadd_rn(V[j * 5], __dmul_rn(V[j * 5 + 3], a.times[t]));

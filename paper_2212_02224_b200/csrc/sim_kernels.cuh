@@ -81,6 +81,7 @@ __device__ void sim_lf(const SimWorld& w, int lane, double x, int skip, int& lea
         if (xj > x && (leader < 0 || xj < w.x[leader])) leader = j;
         else if (xj <= x && (follower < 0 || xj > w.x[follower])) follower = j;
     }
+    BD_CHECK(leader < w.n1 && follower < w.n1 && leader != skip && follower != skip);
 }
 
 // _gap / _accel_toward (pkg/highway.py:272-280)
@@ -247,6 +248,7 @@ __global__ void __launch_bounds__(128) sim_kernel(const SimArgs a) {
             x[3] = tl; x[4] = cd; x[5] = dacc[i]; x[6] = sim_lane_of(py, lanes, lw);
             const double VB[5] = {px, py, psi, x[0], x[1]};
             hit |= sim_overlap(EA, VB);
+            BD_CHECK(i < nm && 11 + 4 * i < SNAP);
             if (snap) { snap[8 + 4 * i] = px; snap[9 + 4 * i] = py; snap[10 + 4 * i] = psi; snap[11 + 4 * i] = vel; }
         }
         hit = __syncthreads_or(hit);
