@@ -9,6 +9,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/bilevel_b200.h"
 #include "am_kernel.cuh"
 #include "bd_common.cuh"
@@ -431,6 +433,12 @@ int run_stage1(bd_ctx* ctx, int B, const double* params, double* xi_bar, double*
 }  // namespace
 
 // =====================================================================================
+// NVTX range per public call (nsys / ncu --nvtx filtering); header-only NVTX v3.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 extern "C" {
 
 int bd_abi_version(void) { return BD_ABI_VERSION; }
@@ -718,6 +726,7 @@ int bd_set_scenes(bd_ctx* ctx, int S, int n_obs, int m, const double* ox, const 
 }
 
 int bd_stage1(bd_ctx* ctx, int S, int B, const double* params, double* xi_bar, double* mu, double* b_out) {
+    NvtxRange nvtx_("bd_stage1");
     if (!ctx) return BD_ERR_VALUE;
     int rc = require_solver(ctx, true);
     if (rc) return rc;
@@ -737,6 +746,7 @@ int bd_stage1(bd_ctx* ctx, int S, int B, const double* params, double* xi_bar, d
 
 int bd_project(bd_ctx* ctx, int S, int B, const double* xi_bar, const double* b, int iters, double tol, double* xi,
                double* res, double* cost, float* hist, int* iters_used, int64_t* conflicts) {
+    NvtxRange nvtx_("bd_project");
     if (!ctx) return BD_ERR_VALUE;
     int rc = require_solver(ctx, false);
     if (rc) return rc;
@@ -766,6 +776,7 @@ int bd_project(bd_ctx* ctx, int S, int B, const double* xi_bar, const double* b,
 int bd_solve_lower(bd_ctx* ctx, int S, int B, const double* params, int iters, double tol, double* xi_bar,
                    double* mu, double* xi, double* res, double* cost, float* hist, int* iters_used,
                    int64_t* conflicts) {
+    NvtxRange nvtx_("bd_solve_lower");
     if (!ctx) return BD_ERR_VALUE;
     int rc = require_solver(ctx, true);
     if (rc) return rc;
@@ -800,6 +811,7 @@ int bd_solve_lower(bd_ctx* ctx, int S, int B, const double* params, int iters, d
 
 int bd_eval(bd_ctx* ctx, int count, const double* xi, double* x, double* y, double* xd, double* yd, double* xdd,
             double* ydd) {
+    NvtxRange nvtx_("bd_eval");
     if (!ctx) return BD_ERR_VALUE;
     if (!ctx->m) return fail(ctx, BD_ERR_STATE, "basis not set");
     if (count < 1 || !xi) return fail(ctx, BD_ERR_VALUE, "bad eval call");
@@ -821,6 +833,7 @@ int bd_eval(bd_ctx* ctx, int count, const double* xi, double* x, double* y, doub
 }
 
 int bd_residuals(bd_ctx* ctx, int S, int B, const double* xi, double* out) {
+    NvtxRange nvtx_("bd_residuals");
     if (!ctx) return BD_ERR_VALUE;
     if (!ctx->m || !ctx->S) return fail(ctx, BD_ERR_STATE, "basis / scenes not set");
     if (S != ctx->S || B < 1 || !xi || !out) return fail(ctx, BD_ERR_VALUE, "bad residual call");
@@ -843,6 +856,7 @@ int bd_residuals(bd_ctx* ctx, int S, int B, const double* xi, double* out) {
 
 int bd_solve_lower_shard(bd_ctx* ctx, int B, const double* params, int iters, double* xi_bar, double* xi,
                          double* res, double* cost, float* iter_max) {
+    NvtxRange nvtx_("bd_solve_lower_shard");
     if (!ctx) return BD_ERR_VALUE;
     int rc = require_solver(ctx, true);
     if (rc) return rc;
@@ -871,6 +885,7 @@ int bd_solve_lower_shard(bd_ctx* ctx, int B, const double* params, int iters, do
 }
 
 int bd_replay_shard(bd_ctx* ctx, int B, const double* xi_bar, int iters, double* xi, double* res, double* cost) {
+    NvtxRange nvtx_("bd_replay_shard");
     if (!ctx) return BD_ERR_VALUE;
     int rc = require_solver(ctx, false);
     if (rc) return rc;
@@ -894,6 +909,7 @@ int bd_replay_shard(bd_ctx* ctx, int B, const double* xi_bar, int iters, double*
 
 int bd_sample_philox(bd_ctx* ctx, int dim, int count, const double* mean, const double* cov, uint64_t seed,
                      int scene, int iteration, int first_index, double* params) {
+    NvtxRange nvtx_("bd_sample_philox");
     if (!ctx) return BD_ERR_VALUE;
     if (dim < 1 || dim > MAX_DIM || count < 1 || !mean || !cov || !params || first_index < 0)
         return fail(ctx, BD_ERR_VALUE, "bad sample call");
@@ -912,6 +928,7 @@ int bd_sample_philox(bd_ctx* ctx, int dim, int count, const double* mean, const 
 
 int bd_kkt_solve(bd_ctx* ctx, int nvar, int neq, const double* kkt, const double* kinv, int count,
                  const double* rhs, double* sol) {
+    NvtxRange nvtx_("bd_kkt_solve");
     if (!ctx) return BD_ERR_VALUE;
     const int nr = nvar + neq;
     if (nvar < 1 || neq < 0 || nr > 32 || count < 1 || !kkt || !kinv || !rhs || !sol)
@@ -938,6 +955,7 @@ int bd_kkt_solve(bd_ctx* ctx, int nvar, int neq, const double* kkt, const double
 
 int bd_sample(bd_ctx* ctx, int dim, int count, const double* mean, const double* cov, const double* z,
               double* params) {
+    NvtxRange nvtx_("bd_sample");
     if (!ctx) return BD_ERR_VALUE;
     if (dim < 1 || dim > MAX_DIM || count < 1 || !mean || !cov || !z || !params)
         return fail(ctx, BD_ERR_VALUE, "bad sample call");
@@ -958,6 +976,7 @@ int bd_sample(bd_ctx* ctx, int dim, int count, const double* mean, const double*
 int bd_rank_refit(bd_ctx* ctx, int S, int B, int dim, const double* resid, const double* cost, const double* params,
                   int n_cons, int n_elite, double w_res, double eta, double gamma, double* mean, double* cov,
                   int64_t* cons_idx, int64_t* elite_idx, double* elite_aug, double* stats) {
+    NvtxRange nvtx_("bd_rank_refit");
     if (!ctx) return BD_ERR_VALUE;
     if (S < 1 || B < 1 || !resid || !cost || !params || !mean || !cov || dim < 1 || dim > MAX_DIM)
         return fail(ctx, BD_ERR_VALUE, "bad rank_refit call");
@@ -1018,6 +1037,7 @@ int bd_cem_cycle(bd_ctx* ctx, int S, const bd_cem_config* cfg, const double* ini
                  const double* z, const double* warm, int64_t* best_index, double* best_params, double* best_xi,
                  double* best_cost, double* best_residual, double* best_aug, double* stats, double* final_mean,
                  double* final_cov, int* iterations_done) {
+    NvtxRange nvtx_("bd_cem_cycle");
     if (!ctx || !cfg) return BD_ERR_VALUE;
     int rc = require_solver(ctx, true);
     if (rc) return rc;
@@ -1125,6 +1145,7 @@ int bd_cem_cycle(bd_ctx* ctx, int S, const bd_cem_config* cfg, const double* ini
 int bd_build_scenes(bd_ctx* ctx, int S, int n_veh_max, const double* ego, const double* veh, const int* n_veh,
                     const double* road, const bd_env* env, const double* times, double* ox_out, double* oy_out,
                     double* b0_out, double* limits_out, double* observations) {
+    NvtxRange nvtx_("bd_build_scenes");
     if (!ctx || !env) return BD_ERR_VALUE;
     if (!ctx->m) return fail(ctx, BD_ERR_STATE, "basis not set");
     const int m = ctx->m, n_obs = env->max_obstacles;
@@ -1204,6 +1225,7 @@ int bd_set_control_grid(bd_ctx* ctx, int n_ctrl, const double* wd, const double*
 }
 
 int bd_controls(bd_ctx* ctx, int count, const double* xi, double* accel, double* steer, int* singular) {
+    NvtxRange nvtx_("bd_controls");
     if (!ctx) return BD_ERR_VALUE;
     if (!ctx->n_ctrl) return fail(ctx, BD_ERR_STATE, "control grid not set");
     if (count < 1 || !xi || !accel || !steer || !singular) return fail(ctx, BD_ERR_VALUE, "bad controls call");
@@ -1290,6 +1312,7 @@ bool make_map_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t c
 }  // namespace
 
 int bd_cvae_decode(bd_ctx* ctx, int count, const float* obs, const float* z, double* params) {
+    NvtxRange nvtx_("bd_cvae_decode");
     if (!ctx || count < 1 || !obs || !z || !params) return BD_ERR_VALUE;
     if (ctx->cvae_w.empty()) return fail(ctx, BD_ERR_STATE, "CVAE weights not set");
     begin_call(ctx);
@@ -1370,6 +1393,7 @@ int bd_cvae_decode(bd_ctx* ctx, int count, const float* obs, const float* z, dou
 int bd_sim_run(bd_ctx* ctx, int S, int n_max, double* ego, double* ego_ts, double* veh, double* vext, const int* n_veh,
                const double* road, double* world, const bd_traffic* tp, int n_steps, const double* controls, int n_ctrl,
                int ctrl_offset, const double* x_end, int* active, int* steps_done, double* snapshots) {
+    NvtxRange nvtx_("bd_sim_run");
     if (!ctx) return BD_ERR_VALUE;
     if (S < 1 || n_max < 0 || n_steps < 0 || !tp || !ego || !ego_ts || !n_veh || !road || !world ||
         (n_max > 0 && (!veh || !vext)) || (n_steps > 0 && (!controls || n_ctrl < 1)) || ctrl_offset < 0)
