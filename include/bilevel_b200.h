@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define BD_ABI_VERSION 1
+#define BD_ABI_VERSION 2
 
 #define BD_OK 0
 #define BD_ERR_VALUE (-1)      /* ValueError        pkg/batch_qp.py:99-106,223-227,265-269; pkg/projection.py:225-233 */
@@ -56,6 +56,9 @@ typedef struct bd_cem_config {
     double eta, gamma, residual_weight, tol;
     uint64_t seed;      /* Philox key when z == NULL (device RNG mode)         */
     int scene_offset;   /* global index of scene 0 (Philox counter; shard-invariant fleets) */
+    int iter_begin;     /* run CEM iterations [iter_begin, iter_end) of the cycle (0, 0 = all);  */
+    int iter_end;       /* a cycle may be split over calls on one context (state stays on the   */
+                        /* device; no other solve in between), z then covering only this range */
 } bd_cem_config;
 
 /* ------------------------------------------------------------------ lifecycle */

@@ -69,7 +69,8 @@ class CemConfig(ctypes.Structure):
     """bd_cem_config: BiLevelConfig (pkg/bilevel.py:72-97) + projection budget."""
     _fields_ = [("batch", c_int), ("n_cons", c_int), ("n_elite", c_int), ("iterations", c_int),
                 ("am_iters", c_int), ("eta", c_double), ("gamma", c_double), ("residual_weight", c_double),
-                ("tol", c_double), ("seed", c_uint64), ("scene_offset", c_int)]
+                ("tol", c_double), ("seed", c_uint64), ("scene_offset", c_int), ("iter_begin", c_int),
+                ("iter_end", c_int)]
 
 
 class Traffic(ctypes.Structure):

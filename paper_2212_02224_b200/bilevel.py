@@ -292,11 +292,6 @@ def solve_bilevel(scene: PlanningScene, solver: LowerLevelSolver, config: BiLeve
     state0 = rng.bit_generator.state
     warm = f64(warm_start.draw(B)) if warm_start is not None else None
     n_draw = N - (1 if warm is not None else 0)
-    z = np.zeros((N, B, dim))
-    if n_draw:
-        z[N - n_draw:] = rng.standard_normal((n_draw, B, dim))
-    cfg = CemConfig(B, config.constraint_elites, config.elites, N, pcfg.max_iters, config.eta, config.gamma,
-                    config.residual_weight, pcfg.tol, 0, 0)
     bi = np.zeros(1, dtype=np.int64)
     bp = np.zeros(dim)
     bx = np.zeros(2 * solver.basis.num_coeffs)
@@ -305,9 +300,27 @@ def solve_bilevel(scene: PlanningScene, solver: LowerLevelSolver, config: BiLeve
     fm = np.zeros(dim)
     fc = np.zeros((dim, dim))
     done = np.zeros(1, dtype=np.int32)
-    solver.context.call("bd_cem_cycle", 1, ctypes.byref(cfg), f64(config.init_mean), f64(config.init_cov),
-                        ptr(z), ptr(warm), ptr(bi), ptr(bp), ptr(bx), ptr(bc), ptr(br), ptr(ba), ptr(st), ptr(fm),
-                        ptr(fc), ptr(done))
+    mean0, cov0 = f64(config.init_mean), f64(config.init_cov)
+
+    def cfg_range(a, b):
+        return CemConfig(B, config.constraint_elites, config.elites, N, pcfg.max_iters, config.eta, config.gamma,
+                         config.residual_weight, pcfg.tol, 0, 0, a, b)
+
+    # Iteration 1 is launched as soon as its draws exist; the remaining N-1 batches of the caller's
+    # Generator are drawn while the GPU runs it (the stream is the same sequence as one
+    # standard_normal((N, B, dim)) call), then iterations 2..N follow in a second call.
+    z1 = None if warm is not None else rng.standard_normal((1, B, dim))
+    if N == 1:
+        solver.context.call("bd_cem_cycle", 1, ctypes.byref(cfg_range(0, 1)), mean0, cov0, ptr(z1), ptr(warm),
+                            ptr(bi), ptr(bp), ptr(bx), ptr(bc), ptr(br), ptr(ba), ptr(st), ptr(fm), ptr(fc),
+                            ptr(done))
+    else:
+        solver.context.call("bd_cem_cycle", 1, ctypes.byref(cfg_range(0, 1)), mean0, cov0, ptr(z1), ptr(warm),
+                            None, None, None, None, None, None, None, None, None, None)
+        z = rng.standard_normal((N - 1, B, dim))
+        solver.context.call("bd_cem_cycle", 1, ctypes.byref(cfg_range(1, N)), mean0, cov0, ptr(z), None,
+                            ptr(bi), ptr(bp), ptr(bx), ptr(bc), ptr(br), ptr(ba), ptr(st), ptr(fm), ptr(fc),
+                            ptr(done))
     k = int(done[0])
     attempted = N if k >= N else (1 if k <= 0 else k + 1)
     consumed = attempted - (1 if warm is not None else 0)

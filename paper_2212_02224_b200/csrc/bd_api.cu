@@ -1048,12 +1048,14 @@ int bd_cem_cycle(bd_ctx* ctx, int S, const bd_cem_config* cfg, const double* ini
         return fail(ctx, BD_ERR_VALUE, "need elites <= constraint_elites <= batch_size (<= 1024 constraint elites)");
     if (!(cfg->eta > 0 && cfg->eta <= 1) || !(cfg->gamma > 0)) return fail(ctx, BD_ERR_VALUE, "bad eta / gamma");
     if (B > (1 << 24)) return fail(ctx, BD_ERR_VALUE, "batch too large");
+    const int it0 = cfg->iter_begin, it1 = cfg->iter_end > 0 ? cfg->iter_end : N;
+    if (it0 < 0 || it0 >= it1 || it1 > N) return fail(ctx, BD_ERR_VALUE, "bad CEM iteration range");
     begin_call(ctx);
     const size_t tot = (size_t)S * B;
     const double *dz = nullptr, *dwarm = nullptr, *dm0, *dc0;
     if ((rc = stage_in(ctx, init_mean, (size_t)S * dim, &dm0))) return rc;
     if ((rc = stage_in(ctx, init_cov, (size_t)S * dim * dim, &dc0))) return rc;
-    if ((rc = stage_in(ctx, z, z ? (size_t)N * tot * dim : 0, &dz))) return rc;
+    if ((rc = stage_in(ctx, z, z ? (size_t)(it1 - it0) * tot * dim : 0, &dz))) return rc;
     if ((rc = stage_in(ctx, warm, warm ? tot * dim : 0, &dwarm))) return rc;
     CU(ctx->c_mean.ensure((size_t)S * dim * 8));
     CU(ctx->c_cov.ensure((size_t)S * dim * dim * 8));
@@ -1085,8 +1087,10 @@ int bd_cem_cycle(bd_ctx* ctx, int S, const bd_cem_config* cfg, const double* ini
     s.xi = ctx->w_xi.as<double>(); s.stats = ctx->c_stats.as<double>();
     s.best_index = ctx->c_best_idx.as<long long>(); s.best_params = ctx->c_best_p.as<double>();
     s.best_xi = ctx->c_best_xi.as<double>(); s.best_scal = ctx->c_best_s.as<double>();
-    cem_init_kernel<<<S, 64, 0, ctx->stream>>>(s, dm0, dc0);
-    ctx->launches++;
+    if (it0 == 0) {
+        cem_init_kernel<<<S, 64, 0, ctx->stream>>>(s, dm0, dc0);
+        ctx->launches++;
+    }
     CU(ctx->w_order.ensure(tot * 4));
     const size_t rsmem = rank_refit_smem(cfg->n_cons, cfg->n_elite, dim);
     raise_smem(rank_refit_kernel, rsmem);
@@ -1098,8 +1102,8 @@ int bd_cem_cycle(bd_ctx* ctx, int S, const bd_cem_config* cfg, const double* ini
     s1.xi_bar = ctx->w_xibar.as<double>(); s1.mu = nullptr; s1.b_out = db; s1.err = ctx->w_err.as<int>();
     const size_t s1smem = (size_t)(2 * s1.nr * s1.nr + 2 * NC * s1.m_seg + 8 * MAX_DIM) * 8;
     raise_smem(sample_stage1_kernel, s1smem);
-    for (int it = 0; it < N; ++it) {
-        const double* zi = dz ? dz + (size_t)it * tot * dim : nullptr;
+    for (int it = it0; it < it1; ++it) {
+        const double* zi = dz ? dz + (size_t)(it - it0) * tot * dim : nullptr;
         sample_stage1_kernel<<<(unsigned)((tot + 7) / 8), 256, s1smem, ctx->stream>>>(
             s, it, zi, it == 0 ? dwarm : nullptr, cfg->seed, cfg->scene_offset, ctx->w_params.as<double>(), s1);
         ctx->launches++;
