@@ -2,6 +2,7 @@
 // scene upload, pointer staging and the launch sequences of the hot path.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -48,7 +49,9 @@ struct DevBuf {
 struct PendingCopy {
     void* dst;
     const void* src;
-    size_t bytes;
+    size_t bytes;             // bytes written to dst (contiguous)
+    size_t src_stride = 0;    // 0: contiguous source; else elements of `elem` bytes every src_stride bytes
+    size_t elem = 0;
 };
 
 }  // namespace
@@ -82,6 +85,9 @@ struct bd_ctx {
         w_order;
     DevBuf stage[8];
     int n_stage = 0;
+    DevBuf out_pack;              // coalesced device->host outputs: gathered here, one D2H copy
+    void* out_pin = nullptr;      // pinned host staging for out_pack
+    size_t out_pin_bytes = 0;
     std::vector<PendingCopy> pending;
     bool host_out = false;
     // CEM state
@@ -103,6 +109,7 @@ struct bd_ctx {
         for (auto* b : cvae_w) delete b;
         for (auto* b : cvae_b) delete b;
         for (auto* b : cvae_w16) delete b;
+        if (out_pin) cudaFreeHost(out_pin);
     }
 };
 
@@ -230,10 +237,71 @@ void begin_call(bd_ctx* ctx) {
     cudaSetDevice(ctx->device);
 }
 
+// Gather of up to GATHER_MAX (possibly strided) device segments into one contiguous pack, so a
+// call's host outputs leave the device in a single D2H copy (one DMA instead of one per array).
+constexpr int GATHER_MAX = 24;
+struct GatherSeg { const unsigned char* src; size_t off, bytes, stride, elem; };
+struct GatherArgs { GatherSeg seg[GATHER_MAX]; int n; unsigned char* pack; };
+__global__ void gather_kernel(const GatherArgs g) {
+    const GatherSeg sg = g.seg[blockIdx.y];
+    unsigned char* dst = g.pack + sg.off;
+    if (sg.stride == 0) {
+        const size_t words = sg.bytes / 4;
+        for (size_t i = blockIdx.x * blockDim.x + threadIdx.x; i < words; i += (size_t)gridDim.x * blockDim.x)
+            reinterpret_cast<unsigned*>(dst)[i] = reinterpret_cast<const unsigned*>(sg.src)[i];
+    } else {
+        for (size_t i = blockIdx.x * blockDim.x + threadIdx.x; i < sg.bytes; i += (size_t)gridDim.x * blockDim.x)
+            dst[i] = sg.src[(i / sg.elem) * sg.stride + i % sg.elem];
+    }
+}
+
+int flush_outputs(bd_ctx* ctx) {
+    auto& pend = ctx->pending;
+    if (pend.empty()) return 0;
+    const bool single = pend.size() == 1 && pend[0].src_stride == 0;
+    if (single) {
+        CU(cudaMemcpyAsync(pend[0].dst, pend[0].src, pend[0].bytes, cudaMemcpyDeviceToHost, ctx->stream));
+        return 0;
+    }
+    std::vector<size_t> off(pend.size());
+    size_t total = 0;
+    for (size_t i = 0; i < pend.size(); ++i) { off[i] = total; total += (pend[i].bytes + 15) / 16 * 16; }
+    CU(ctx->out_pack.ensure(total));
+    if (total > ctx->out_pin_bytes) {
+        if (ctx->out_pin) cudaFreeHost(ctx->out_pin);
+        ctx->out_pin = nullptr;
+        ctx->out_pin_bytes = 0;
+        const size_t want = std::max(total, (size_t)1 << 16) * 2;
+        CU(cudaHostAlloc(&ctx->out_pin, want, cudaHostAllocDefault));
+        ctx->out_pin_bytes = want;
+    }
+    for (size_t b = 0; b < pend.size(); b += GATHER_MAX) {
+        GatherArgs g{};
+        g.n = (int)std::min(pend.size() - b, (size_t)GATHER_MAX);
+        g.pack = ctx->out_pack.as<unsigned char>();
+        size_t biggest = 0;
+        for (int i = 0; i < g.n; ++i) {
+            const PendingCopy& pc = pend[b + i];
+            g.seg[i] = {static_cast<const unsigned char*>(pc.src), off[b + i], pc.bytes, pc.src_stride, pc.elem};
+            biggest = std::max(biggest, pc.bytes);
+        }
+        const unsigned gx = (unsigned)std::min<size_t>((biggest / 4 + 255) / 256 + 1, 1024);
+        gather_kernel<<<dim3(gx, g.n), 256, 0, ctx->stream>>>(g);
+        ctx->launches++;
+    }
+    CU(cudaMemcpyAsync(ctx->out_pin, ctx->out_pack.p, total, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    for (size_t i = 0; i < pend.size(); ++i)
+        std::memcpy(pend[i].dst, static_cast<unsigned char*>(ctx->out_pin) + off[i], pend[i].bytes);
+    pend.clear();
+    return 0;
+}
+
 int finish_call(bd_ctx* ctx, bool check_err, int n_err) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(ctx, BD_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
-    for (auto& pc : ctx->pending) CU(cudaMemcpyAsync(pc.dst, pc.src, pc.bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    int rc = flush_outputs(ctx);
+    if (rc) return rc;
     const bool sync = ctx->host_out || check_err;
     if (!sync) return 0;
     CU(cudaStreamSynchronize(ctx->stream));
@@ -1129,20 +1197,27 @@ int bd_cem_cycle(bd_ctx* ctx, int S, const bd_cem_config* cfg, const double* ini
         {final_cov, ctx->c_cov.p, (size_t)S * dim * dim * 8},
         {iterations_done, ctx->c_done.p, (size_t)S * 4},
     };
-    bool any_host = false;
     for (const Out& o : outs)
         if (o.dst) {
-            CU(cudaMemcpyAsync(o.dst, o.src, o.bytes, cudaMemcpyDefault, ctx->stream));
-            any_host |= !is_device_ptr(o.dst);
+            if (is_device_ptr(o.dst)) {
+                CU(cudaMemcpyAsync(o.dst, o.src, o.bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+            } else {
+                ctx->pending.push_back({o.dst, o.src, o.bytes});
+                ctx->host_out = true;
+            }
         }
     double* scal[3] = {best_cost, best_residual, best_aug};
     for (int q = 0; q < 3; ++q)
         if (scal[q]) {
-            CU(cudaMemcpy2DAsync(scal[q], 8, ctx->c_best_s.as<double>() + q, 24, 8, S, cudaMemcpyDefault, ctx->stream));
-            any_host |= !is_device_ptr(scal[q]);
+            if (is_device_ptr(scal[q])) {
+                CU(cudaMemcpy2DAsync(scal[q], 8, ctx->c_best_s.as<double>() + q, 24, 8, S, cudaMemcpyDeviceToDevice,
+                                     ctx->stream));
+            } else {
+                ctx->pending.push_back({scal[q], ctx->c_best_s.as<double>() + q, (size_t)S * 8, 24, 8});
+                ctx->host_out = true;
+            }
         }
-    if (any_host) CU(cudaStreamSynchronize(ctx->stream));
-    return 0;
+    return finish_call(ctx, false, 0);
 }
 
 // ------------------------------------------------------------------ scenes from worlds, controls
