@@ -1093,7 +1093,7 @@ int bd_rank_refit(bd_ctx* ctx, int S, int B, int dim, const double* resid, const
     ctx->launches++;
     const size_t smem = rank_refit_smem(n_cons, n_elite, dim);
     raise_smem(rank_refit_kernel, smem);
-    rank_refit_kernel<<<S, 1024, smem, ctx->stream>>>(s, 0, ctx->w_order.as<int>());
+    rank_refit_kernel<<<S, RANK_REFIT_THREADS, smem, ctx->stream>>>(s, 0, ctx->w_order.as<int>());
     ctx->launches++;
     CU(cudaMemcpyAsync(mean, ctx->c_mean.p, (size_t)S * dim * 8, cudaMemcpyDefault, ctx->stream));
     CU(cudaMemcpyAsync(cov, ctx->c_cov.p, (size_t)S * dim * dim * 8, cudaMemcpyDefault, ctx->stream));
@@ -1181,7 +1181,7 @@ int bd_cem_cycle(bd_ctx* ctx, int S, const bd_cem_config* cfg, const double* ini
             return rc;
         rank_count_kernel<<<(unsigned)((tot + 7) / 8), 256, 0, ctx->stream>>>(s.resid, s.err, S, B,
                                                                              ctx->w_order.as<int>());
-        rank_refit_kernel<<<S, 1024, rsmem, ctx->stream>>>(s, it, ctx->w_order.as<int>());
+        rank_refit_kernel<<<S, RANK_REFIT_THREADS, rsmem, ctx->stream>>>(s, it, ctx->w_order.as<int>());
         ctx->launches += 2;
     }
     cudaError_t e = cudaGetLastError();

@@ -176,8 +176,10 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
     __syncthreads();
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
     __syncthreads();
-    double t = 0.0;
-    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+    // every warp folds the per-warp partials with shuffles (fixed order: deterministic)
+    const int nw = blockDim.x >> 5, ln = threadIdx.x & 31;
+    double t = ln < nw ? red[ln] : 0.0;
+    for (int o = 16; o >= 1; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
     return t;
 }
 
@@ -206,15 +208,18 @@ __global__ void __launch_bounds__(256) rank_count_kernel(const double* resid, co
 // Dynamic shared memory of rank_refit_kernel (bytes).
 __host__ __device__ inline size_t rank_refit_smem(int n_cons, int n_elite, int dim) {
     const int staged = n_elite <= 128 ? n_elite : 0;
-    return (size_t)n_cons * (8 + 4 + 4 + 8) + (size_t)staged * dim * 8;
+    return (size_t)n_cons * (8 + 8 + 8 + 4 + 4 + 8) + (size_t)staged * dim * 8;   // key2 augc aug2 cidx idx2 w
 }
+
+constexpr int RANK_REFIT_THREADS = 1024;
 
 // rank_samples + update_distribution + IterationStats + best record for one CEM
 // iteration, one CTA (1024 threads) per scene, on the residual order produced by
 // rank_count_kernel.  The n constraint elites are ranked by augmented cost (ties by sample
 // index, np.lexsort((idx, aug))) by counting in shared memory, the q elite set-point vectors
-// staged in shared memory and the weighted mean / covariance reduced warp-parallel in fp64.
-__global__ void __launch_bounds__(1024) rank_refit_kernel(CemState s, int it, const int* order) {
+// staged in shared memory and the weighted mean / covariance reduced warp-parallel in fp64; the
+// tail (Cholesky factor, IterationStats, best record) runs on separate warps concurrently.
+__global__ void __launch_bounds__(RANK_REFIT_THREADS) rank_refit_kernel(CemState s, int it, const int* order) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int scene = blockIdx.x;
     const int d = s.dim;
@@ -223,45 +228,60 @@ __global__ void __launch_bounds__(1024) rank_refit_kernel(CemState s, int it, co
         return;
     }
     const int n = s.n_cons, q = s.n_elite;
-    // dynamic layout (rank_refit_smem): key2 | cidx | idx2 | w | staged elite set-points
+    // dynamic layout (rank_refit_smem): key2 | aug | aug2 | cidx | idx2 | w | staged elite set-points
     unsigned long long* key2 = reinterpret_cast<unsigned long long*>(smem);
-    int* cidx = reinterpret_cast<int*>(key2 + n);
+    double* augc = reinterpret_cast<double*>(key2 + n);      // aug of constraint elite i (residual order)
+    double* aug2 = augc + n;                                  // aug by elite rank
+    int* cidx = reinterpret_cast<int*>(aug2 + n);
     int* idx2 = cidx + n;
-    double* w = reinterpret_cast<double*>(idx2 + n);
-    double* pe = w + n;                    // q <= 128 staged; larger q read from global
+    double* w = reinterpret_cast<double*>(idx2 + n);          // n ints + n ints: 8-byte aligned
+    double* pe = w + n;                                       // q <= 128 staged; larger q read from global
     __shared__ double red[32];
     __shared__ double mu_new[MAX_DIM];
     __shared__ double cnew[MAX_DIM * MAX_DIM];
+    __shared__ double csym[MAX_DIM * MAX_DIM], lsh[MAX_DIM * MAX_DIM];
     const size_t base = (size_t)scene * s.B;
     const int* ord = order + base;
     // constraint elites: first n of the stable residual order; aug = cost + w r
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         const int j = ord[i];
         BD_CHECK(j >= 0 && j < s.B);
-        key2[i] = ordered_bits(aug_cost(s.cost[base + j], s.w_res, s.resid[base + j]));
+        const double a = aug_cost(s.cost[base + j], s.w_res, s.resid[base + j]);
+        augc[i] = a;
+        key2[i] = ordered_bits(a);
         cidx[i] = j;
         if (s.cons_idx) s.cons_idx[(size_t)scene * n + i] = j;
     }
     __syncthreads();
-    // rank among the constraint elites by (aug, sample index), scatter
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const unsigned long long ki = key2[i];
-        const int ji = cidx[i];
-        int rk = 0;
-        for (int k = 0; k < n; ++k) rk += (key2[k] < ki) || (key2[k] == ki && cidx[k] < ji);
-        BD_CHECK(rk >= 0 && rk < n);
-        idx2[rk] = ji;
+    // rank among the constraint elites by (aug, sample index), scatter index and aug: a warp per
+    // elite, its lanes compare 32 keys at a time (ballot + popc)
+    {
+        const int wp = threadIdx.x >> 5, ln = threadIdx.x & 31;
+        for (int i = wp; i < n; i += blockDim.x >> 5) {
+            const unsigned long long ki = key2[i];
+            const int ji = cidx[i];
+            int rk = 0;
+            for (int k0 = 0; k0 < n; k0 += 32) {
+                const int k = k0 + ln;
+                const bool before = k < n && ((key2[k] < ki) || (key2[k] == ki && cidx[k] < ji));
+                rk += __popc(__ballot_sync(0xffffffffu, before));
+            }
+            BD_CHECK(rk >= 0 && rk < n);
+            if (ln == 0) {
+                idx2[rk] = ji;
+                aug2[rk] = augc[i];
+            }
+        }
     }
     __syncthreads();
     // elite weights exp(-(aug - min aug)/gamma), uniform fallback (pkg/bilevel.py:163-172)
     const int j0 = idx2[0];
-    const double amin = aug_cost(s.cost[base + j0], s.w_res, s.resid[base + j0]);
+    const double amin = aug2[0];
     double part = 0.0, cpart = 0.0;
     const bool staged = q <= 128;
-    __syncthreads();
     for (int i = threadIdx.x; i < q; i += blockDim.x) {
         const int j = idx2[i];
-        const double aug = aug_cost(s.cost[base + j], s.w_res, s.resid[base + j]);
+        const double aug = aug2[i];
         const double wi = exp(-(aug - amin) / s.gamma);
         w[i] = wi;
         part += wi;
@@ -299,38 +319,41 @@ __global__ void __launch_bounds__(1024) rank_refit_kernel(CemState s, int it, co
         if (lane == 0) cnew[e] = (1.0 - eta) * cov[e] + eta * acc + (r == c ? 1e-6 : 0.0);
     }
     __syncthreads();
-    __shared__ double csym[MAX_DIM * MAX_DIM], lsh[MAX_DIM * MAX_DIM];
-    if (threadIdx.x < d * d) {
-        const int r = threadIdx.x / d, c = threadIdx.x % d;
+    for (int e = threadIdx.x; e < d * d; e += blockDim.x) {
+        const int r = e / d, c = e % d;
         const double v = 0.5 * (cnew[r * d + c] + cnew[c * d + r]);
-        cov[threadIdx.x] = v;
-        csym[threadIdx.x] = v;
+        cov[e] = v;
+        csym[e] = v;
     }
     if (threadIdx.x < d) mean[threadIdx.x] = mu_new[threadIdx.x];
     __syncthreads();
-    if (threadIdx.x < 32) warp_sampling_factor(csym, lsh, s.L + scene * d * d, d, threadIdx.x);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        // IterationStats (pkg/bilevel.py:282-292)
-        const int B = s.B;
-        const double rmin = s.resid[base + ord[0]], rmax = s.resid[base + ord[B - 1]];
-        const double rmed = (B & 1) ? s.resid[base + ord[B / 2]]
-                                    : 0.5 * (s.resid[base + ord[B / 2 - 1]] + s.resid[base + ord[B / 2]]);
-        double tr = 0.0;
-        for (int i = 0; i < d; ++i) tr += cnew[i * d + i];   // symmetrisation keeps the diagonal
-        if (s.stats) {
-            double* st = s.stats + ((size_t)scene * s.iters + it) * 6;
-            st[0] = csum / q; st[1] = amin; st[2] = tr; st[3] = rmin; st[4] = rmed; st[5] = rmax;
+    if (warp == 0) {
+        warp_sampling_factor(csym, lsh, s.L + scene * d * d, d, lane);
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // IterationStats (pkg/bilevel.py:282-292)
+            const int B = s.B;
+            const double rmin = s.resid[base + ord[0]], rmax = s.resid[base + ord[B - 1]];
+            const double rmed = (B & 1) ? s.resid[base + ord[B / 2]]
+                                        : 0.5 * (s.resid[base + ord[B / 2 - 1]] + s.resid[base + ord[B / 2]]);
+            double tr = 0.0;
+            for (int i = 0; i < d; ++i) tr += cnew[i * d + i];   // symmetrisation keeps the diagonal
+            if (s.stats) {
+                double* st = s.stats + ((size_t)scene * s.iters + it) * 6;
+                st[0] = csum / q; st[1] = amin; st[2] = tr; st[3] = rmin; st[4] = rmed; st[5] = rmax;
+            }
+            // best EliteRecord = elite[0] (pkg/bilevel.py:272-280)
+            s.best_index[scene] = j0;
+            s.best_scal[scene * 3 + 0] = s.cost[base + j0];
+            s.best_scal[scene * 3 + 1] = s.resid[base + j0];
+            s.best_scal[scene * 3 + 2] = amin;
+            s.done[scene] = it + 1;
         }
-        // best EliteRecord = elite[0] (pkg/bilevel.py:272-280)
-        s.best_index[scene] = j0;
-        s.best_scal[scene * 3 + 0] = s.cost[base + j0];
-        s.best_scal[scene * 3 + 1] = s.resid[base + j0];
-        s.best_scal[scene * 3 + 2] = amin;
-        s.done[scene] = it + 1;
+    } else if (warp == 2) {
+        if (lane < d) s.best_params[scene * d + lane] = s.params[(base + j0) * d + lane];
+    } else if (warp == 3) {
+        if (lane < NX && s.xi) s.best_xi[scene * NX + lane] = s.xi[(base + j0) * NX + lane];
     }
-    if (threadIdx.x < d) s.best_params[scene * d + threadIdx.x] = s.params[(base + j0) * d + threadIdx.x];
-    if (threadIdx.x < NX && s.xi) s.best_xi[scene * NX + threadIdx.x] = s.xi[(base + j0) * NX + threadIdx.x];
 }
 
 }  // namespace bd
