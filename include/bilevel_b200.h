@@ -214,6 +214,12 @@ int bd_build_scenes(bd_ctx* ctx, int n_scenes, int n_veh_max, const double* ego,
                     const int* n_veh, const double* road, const bd_env* env, const double* times, double* ox_out,
                     double* oy_out, double* b0_out, double* limits_out, double* observations);
 
+/* Road curvature for the scenes currently in the context (e.g. after bd_build_scenes):
+ * ConstraintSpec.road_curvature = world.road.curvature (pkg/planners.py:154, pkg/constraints.py:67-72),
+ * S tables of n_curv strictly increasing abscissae cx and curvatures ck (row-major S x n_curv);
+ * n_curv = 0 removes them. */
+int bd_set_curvature(bd_ctx* ctx, int n_scenes, int n_curv, const double* cx, const double* ck);
+
 /* controls_on_grid -> flat_to_controls (pkg/planners.py:209-216, pkg/basis.py:206-234): the basis
  * derivative rows at the n_ctrl control instants (matrices_at), then per trajectory the clipped
  * (accel, steer) sequence; singular[i] = 1 where the speed drops to eps_v (SpeedSingularity). */

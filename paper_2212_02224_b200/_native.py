@@ -50,6 +50,7 @@ SIGNATURES = {
                               _P, _P, _P, _P]),
     "bd_cem_cycle": (c_int, [_P, c_int, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "bd_build_scenes": (c_int, [_P, c_int, c_int, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "bd_set_curvature": (c_int, [_P, c_int, c_int, _P, _P]),
     "bd_set_control_grid": (c_int, [_P, c_int, _P, _P, c_double, c_double, c_double, c_double]),
     "bd_controls": (c_int, [_P, c_int, _P, _P, _P, _P]),
     "bd_sim_run": (c_int, [_P, c_int, c_int, _P, _P, _P, _P, _P, _P, _P, _P, c_int, _P, c_int, c_int, _P, _P, _P,

@@ -716,6 +716,30 @@ int bd_set_projection(bd_ctx* ctx, int n_obs, double rho, int neq, const double*
     return 0;
 }
 
+// Per-scene road curvature tables (np.interp abscissae + curvatures, pkg/constraints.py:67-72),
+// fp32 for the AM kernel's clip window and fp64 for the residual evaluator; n_curv = 0 disables.
+static int upload_curvature(bd_ctx* ctx, int S, int n_curv, const double* cx, const double* ck) {
+    if (n_curv > 0) {
+        std::vector<float> cf((size_t)S * 2 * n_curv);
+        std::vector<double> cd((size_t)S * 2 * n_curv);
+        for (int s = 0; s < S; ++s)
+            for (int i = 0; i < n_curv; ++i) {
+                if (i > 0 && !(cx[s * n_curv + i] > cx[s * n_curv + i - 1]))
+                    return fail(ctx, BD_ERR_VALUE, "curvature abscissae must increase");
+                cd[(size_t)s * 2 * n_curv + i] = cx[s * n_curv + i];
+                cd[(size_t)s * 2 * n_curv + n_curv + i] = ck[s * n_curv + i];
+                cf[(size_t)s * 2 * n_curv + i] = (float)cx[s * n_curv + i];
+                cf[(size_t)s * 2 * n_curv + n_curv + i] = (float)ck[s * n_curv + i];
+            }
+        CU(ctx->curvf.ensure(cf.size() * 4));
+        CU(ctx->curv64.ensure(cd.size() * 8));
+        CU(cudaMemcpy(ctx->curvf.p, cf.data(), cf.size() * 4, cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(ctx->curv64.p, cd.data(), cd.size() * 8, cudaMemcpyHostToDevice));
+    }
+    ctx->n_curv = n_curv;
+    return 0;
+}
+
 int bd_set_scenes(bd_ctx* ctx, int S, int n_obs, int m, const double* ox, const double* oy, const bd_limits* L,
                   const double* b0, int n_curv, const double* cx, const double* ck) {
     if (!ctx) return BD_ERR_VALUE;
@@ -725,6 +749,7 @@ int bd_set_scenes(bd_ctx* ctx, int S, int n_obs, int m, const double* ox, const 
     if (n_curv > 0 && (!cx || !ck)) return fail(ctx, BD_ERR_VALUE, "curvature table missing");
     if (n_obs > 0 && (!ox || !oy)) return fail(ctx, BD_ERR_VALUE, "obstacles missing");
     begin_call(ctx);
+    int rc;
     const int neq = ctx->neq ? ctx->neq : 6;
     const size_t no = (size_t)S * n_obs * m;
     const int nop = (n_obs + 1) / 2 * 2;                         // even: two obstacles per LDS.128
@@ -767,30 +792,21 @@ int bd_set_scenes(bd_ctx* ctx, int S, int n_obs, int m, const double* ox, const 
         CU(cudaMemcpy(ctx->ox64.p, ox, no * 8, cudaMemcpyHostToDevice));
         CU(cudaMemcpy(ctx->oy64.p, oy, no * 8, cudaMemcpyHostToDevice));
     }
-    if (n_curv > 0) {
-        std::vector<float> cf((size_t)S * 2 * n_curv);
-        std::vector<double> cd((size_t)S * 2 * n_curv);
-        for (int s = 0; s < S; ++s)
-            for (int i = 0; i < n_curv; ++i) {
-                if (i > 0 && !(cx[s * n_curv + i] > cx[s * n_curv + i - 1]))
-                    return fail(ctx, BD_ERR_VALUE, "curvature abscissae must increase");
-                cd[(size_t)s * 2 * n_curv + i] = cx[s * n_curv + i];
-                cd[(size_t)s * 2 * n_curv + n_curv + i] = ck[s * n_curv + i];
-                cf[(size_t)s * 2 * n_curv + i] = (float)cx[s * n_curv + i];
-                cf[(size_t)s * 2 * n_curv + n_curv + i] = (float)ck[s * n_curv + i];
-            }
-        CU(ctx->curvf.ensure(cf.size() * 4));
-        CU(ctx->curv64.ensure(cd.size() * 8));
-        CU(cudaMemcpy(ctx->curvf.p, cf.data(), cf.size() * 4, cudaMemcpyHostToDevice));
-        CU(cudaMemcpy(ctx->curv64.p, cd.data(), cd.size() * 8, cudaMemcpyHostToDevice));
-    }
+    if ((rc = upload_curvature(ctx, S, n_curv, cx, ck))) return rc;
     CU(ctx->w_err.ensure((size_t)S * 4));
     CU(cudaMemset(ctx->w_err.p, 0, (size_t)S * 4));
     ctx->S = S;
     ctx->scene_obs = n_obs;
     ctx->obs_pad = nop;
-    ctx->n_curv = n_curv;
     return 0;
+}
+
+int bd_set_curvature(bd_ctx* ctx, int S, int n_curv, const double* cx, const double* ck) {
+    if (!ctx) return BD_ERR_VALUE;
+    if (S != ctx->S || n_curv < 0 || n_curv > 1024 || (n_curv > 0 && (!cx || !ck)))
+        return fail(ctx, BD_ERR_VALUE, "curvature tables must cover the context's %d scenes", ctx->S);
+    begin_call(ctx);
+    return upload_curvature(ctx, S, n_curv, cx, ck);
 }
 
 int bd_stage1(bd_ctx* ctx, int S, int B, const double* params, double* xi_bar, double* mu, double* b_out) {

@@ -42,6 +42,7 @@ class RoadSpec:
     lane_count: int
     lane_width: float = 4.0
     length: float = 1500.0
+    curvature: tuple | None = None      # ((xs...), (ks...)) for ConstraintSpec.road_curvature
 
     def __post_init__(self):
         if self.lane_count < 2:
@@ -130,6 +131,7 @@ class SimState:
     n_veh: object
     road: object
     world: object
+    curvature: list | None = None      # host-side per-world road curvature tables (planning only)
 
     @property
     def size(self) -> int:
@@ -142,7 +144,7 @@ class SimState:
     @property
     def worlds(self) -> WorldBatch:
         """The scene-build view (ego, veh, n_veh, road) of the same buffers."""
-        return WorldBatch(self.ego, self.veh, self.n_veh, self.road)
+        return WorldBatch(self.ego, self.veh, self.n_veh, self.road, self.curvature)
 
     def to(self, device):
         """Copy to a torch device (e.g. "cuda:0"); device=None returns host numpy arrays."""
@@ -150,6 +152,9 @@ class SimState:
         out = {}
         for f in fields(self):
             v = getattr(self, f.name)
+            if f.name == "curvature":
+                out[f.name] = v
+                continue
             if device is None:
                 out[f.name] = v.cpu().numpy() if hasattr(v, "cpu") else np.array(v)
             else:
@@ -178,6 +183,8 @@ class SimState:
                 st.veh_ext[s, j] = (5.0, 2.0, v, j % r.lane_count, cd, 0.0, j % r.lane_count)
             st.n_veh[s] = sc.vehicle_count
             st.road[s] = (r.lane_count, r.lane_width)
+        curv = [sc.road.curvature for sc in scenarios]
+        st.curvature = curv if any(c is not None for c in curv) else None
         return st
 
     @staticmethod
@@ -199,6 +206,8 @@ class SimState:
             st.road[s] = (w.road.lane_count, w.road.lane_width)
             st.world[s] = (w.time, w.step_count, float(w.collided),
                            -1.0 if w.collision_step is None else float(w.collision_step), float(w.lane_departed))
+        curv = [getattr(w.road, "curvature", None) for w in worlds]
+        st.curvature = curv if any(c is not None for c in curv) else None
         return st
 
 

@@ -22,7 +22,7 @@ import numpy as np
 from ._native import Env, f64
 from .basis import PolynomialBasis
 
-__all__ = ["WorldBatch", "PlannerEnv", "build_scenes", "ControlEmitter", "env_struct"]
+__all__ = ["WorldBatch", "PlannerEnv", "build_scenes", "ControlEmitter", "env_struct", "curvature_tables"]
 
 
 @dataclass
@@ -31,6 +31,7 @@ class WorldBatch:
     veh: np.ndarray     # S x n_max x 5: x, y, psi, v, lateral_rate (world.neighbors order)
     n_veh: np.ndarray   # S (int32)
     road: np.ndarray    # S x 2: lane_count, lane_width
+    curvature: list | None = None   # per world RoadSpec.curvature ((xs...), (ks...)) or None
 
     @property
     def size(self) -> int:
@@ -51,7 +52,8 @@ class WorldBatch:
                 veh[s, j] = (v.x, v.y, v.psi, v.v, v.lateral_rate)
             n[s] = len(w.neighbors)
             road[s] = (w.road.lane_count, w.road.lane_width)
-        return WorldBatch(ego, veh, n, road)
+        curv = [getattr(w.road, "curvature", None) for w in worlds]
+        return WorldBatch(ego, veh, n, road, curv if any(c is not None for c in curv) else None)
 
 
 @dataclass(frozen=True)
@@ -91,7 +93,32 @@ def build_scenes(ctx, basis: PolynomialBasis, worlds: WorldBatch, env: PlannerEn
     ctx.call("bd_build_scenes", S, n_max, _dev_or(worlds.ego, np.float64), _dev_or(worlds.veh, np.float64),
              _dev_or(worlds.n_veh, np.int32), _dev_or(worlds.road, np.float64), ctypes.byref(cenv),
              f64(basis.times), *out)
+    if worlds.curvature is not None and any(c is not None for c in worlds.curvature):
+        cx, ck = curvature_tables(worlds.curvature)
+        ctx.call("bd_set_curvature", S, cx.shape[1], cx, ck)
     return out if outputs else (out[2] if b0_only else None)
+
+
+def curvature_tables(curvature: list):
+    """Per-world road_curvature tables padded to one length (S x n abscissae, S x n curvatures).
+    np.interp clamps beyond the last abscissa, so padding with further abscissae at the last
+    curvature changes nothing; a world without curvature gets a zero table (kappa = 0 disables
+    the centripetal bound and its residual term exactly as road_curvature=None does)."""
+    n = max(len(c[0]) for c in curvature if c is not None)
+    S = len(curvature)
+    cx, ck = np.empty((S, n)), np.zeros((S, n))
+    for s, c in enumerate(curvature):
+        if c is None:
+            cx[s] = np.arange(n, dtype=float) * 1e9 - 1e9 * (n // 2)
+            continue
+        xs, ks = np.asarray(c[0], float), np.asarray(c[1], float)
+        if xs.shape != ks.shape or xs.ndim != 1 or xs.size < 1:
+            raise ValueError("road curvature must be two equal-length 1-d sequences")
+        L = xs.size
+        cx[s, :L], ck[s, :L] = xs, ks
+        cx[s, L:] = xs[-1] + 1e9 * np.arange(1, n - L + 1)
+        ck[s, L:] = ks[-1]
+    return cx, ck
 
 
 def _dev_or(a, dtype):

@@ -112,3 +112,42 @@ def test_spawned_worlds_build_the_host_recipe_scenes():
         np.testing.assert_array_equal(ox[s], sc.spec.obstacles_x)
         np.testing.assert_array_equal(oy[s], sc.spec.obstacles_y)
         np.testing.assert_array_equal(b0[s], sc.initial_state)
+
+
+@pytest.mark.parametrize("mixed", [False, True])
+def test_device_built_scene_with_road_curvature(mixed):
+    """road_curvature (pkg/planners.py:154): a device-built curved-road scene solves exactly like
+    the host-uploaded ConstraintSpec(road_curvature=...) scene; a world without curvature in the
+    same batch behaves as road_curvature=None (zero table)."""
+    import paper_2212_02224_b200 as bd
+    from paper_2212_02224_b200.worlds import PlannerEnv, WorldBatch, build_scenes
+    g = load("worlds")
+    solver = _solver(10)
+    rng = np.random.default_rng(3)
+    P = np.concatenate([rng.normal(4.0, 1.5, (64, 4)), rng.normal(14.0, 3.0, (64, 4))], axis=1)
+    a, b, vmin, vmax, amax, kmax, cmax, ylb, yub = g["w1_lim"]
+    curv = ((0.0, 40.0, 90.0, 160.0), (0.0, 0.02, 0.05, 0.01))
+    spec = bd.ConstraintSpec(g["w1_ox"], g["w1_oy"], a, b, vmax, amax, kmax, cmax, ylb, yub, vmin,
+                             road_curvature=(np.array(curv[0]), np.array(curv[1])))
+    _, ref = solver.solve(P, bd.PlanningScene(g["w1_b0"], spec))
+    w = _world(g, 1)
+    if mixed:      # second world: the same world without curvature, a shorter table padded for the first
+        flat = bd.ConstraintSpec(g["w1_ox"], g["w1_oy"], a, b, vmax, amax, kmax, cmax, ylb, yub, vmin)
+        _, ref_flat = solver.solve(P, bd.PlanningScene(g["w1_b0"], flat))
+        w = WorldBatch(np.repeat(w.ego, 2, 0), np.repeat(w.veh, 2, 0), np.repeat(w.n_veh, 2), np.repeat(w.road, 2, 0),
+                       [curv, None])
+    else:
+        w = WorldBatch(w.ego, w.veh, w.n_veh, w.road, [curv])
+    build_scenes(solver.context, solver.basis, w, PlannerEnv())
+    solver.projector._scene_key = ("device-built",)
+    S = w.size
+    xi = np.empty((S, 64, 22))
+    res, cost = np.empty((S, 64)), np.empty((S, 64))
+    used, conf = np.zeros(S, np.int32), np.zeros(S, np.int64)
+    solver.context.call("bd_solve_lower", S, 64, np.ascontiguousarray(np.repeat(P[None], S, 0)), 30, 1e-3, None,
+                        None, xi, res, cost, None, used, conf)
+    np.testing.assert_allclose(xi[0].T, ref.xi, rtol=1e-6, atol=1e-6)
+    np.testing.assert_allclose(res[0], ref.residuals, rtol=1e-5, atol=1e-5)
+    if mixed:
+        np.testing.assert_allclose(xi[1].T, ref_flat.xi, rtol=1e-6, atol=1e-6)
+        assert not np.allclose(xi[0], xi[1])

@@ -50,3 +50,14 @@ def test_scenario_dict_roundtrip():
     from paper_2212_02224_b200.sim import RoadSpec, ScenarioConfig
     sc = ScenarioConfig(RoadSpec(3, 3.5, 900.0), 1.5, 30, 7, episode_length=80, scenario_id="x")
     assert ScenarioConfig.from_dict(sc.to_dict()) == sc
+
+
+def test_curvature_tables_padding_preserves_interp():
+    from paper_2212_02224_b200.worlds import curvature_tables
+    tabs = [((0.0, 40.0, 90.0, 160.0), (0.0, 0.02, 0.05, 0.01)), None, ((10.0, 20.0), (0.1, -0.2)), ((5.0,), (0.3,))]
+    cx, ck = curvature_tables(tabs)
+    x = np.linspace(-500, 2000, 4001)
+    for s, t in enumerate(tabs):
+        assert np.all(np.diff(cx[s]) > 0) or cx.shape[1] == 1
+        want = np.zeros_like(x) if t is None else np.interp(x, np.array(t[0]), np.array(t[1]))
+        np.testing.assert_array_equal(np.interp(x, cx[s], ck[s]), want)
