@@ -138,30 +138,37 @@ class FlatControls:
     kappa: np.ndarray
 
 
+def _basis_problems(order: int, num_samples: int, horizon: float, family: str) -> list[str]:
+    checks = [
+        (order >= 2, f"polynomial order {order} is below the minimum of 2"),
+        (horizon > 0, f"horizon {horizon} must be positive"),
+        (num_samples >= order + 1, f"{num_samples} grid points cannot determine an order-{order} polynomial "
+                                   f"(at least {order + 1} needed)"),
+        (family in _FAMILIES, f"basis family {family!r} is not one of {sorted(_FAMILIES)}"),
+    ]
+    return [msg for ok, msg in checks if not ok]
+
+
 def build_basis(order: int, num_samples: int, horizon: float, family: str = "monomial") -> PolynomialBasis:
-    """Uniform-grid basis on [0, horizon] (pkg/basis.py:156-179); same validation."""
-    if order < 2:
-        raise ValueError(f"order must be >= 2, got {order}")
-    if horizon <= 0:
-        raise ValueError(f"horizon must be positive, got {horizon}")
-    if num_samples < order + 1:
-        raise ValueError(f"num_samples={num_samples} undersamples an order-{order} polynomial "
-                         f"(need at least {order + 1})")
-    if family not in _FAMILIES:
-        raise ValueError(f"unknown basis family {family!r}; choose from {sorted(_FAMILIES)}")
-    times = np.linspace(0.0, horizon, num_samples)
-    W, Wd, Wdd = _FAMILIES[family](order, times, horizon)
-    return PolynomialBasis(order=order, horizon=float(horizon), times=times, W=W, Wdot=Wd, Wddot=Wdd, family=family)
+    """Basis rows on the uniform grid linspace(0, horizon, num_samples); raises ValueError on an
+    order below 2, a non-positive horizon, an under-sampled grid or an unknown family."""
+    problems = _basis_problems(order, num_samples, horizon, family)
+    if problems:
+        raise ValueError(problems[0])
+    grid = np.linspace(0.0, horizon, num_samples)
+    rows = _FAMILIES[family](order, grid, horizon)
+    return PolynomialBasis(order, float(horizon), grid, *rows, family=family)
 
 
 def eval_trajectory(basis: PolynomialBasis, coeffs: TrajectoryCoeffs) -> TrajectorySamples:
-    """One trajectory on the grid (pkg/basis.py:182-195); batches go through bd_eval."""
-    if coeffs.cx.shape[0] != basis.num_coeffs:
-        raise ValueError(f"coefficient length {coeffs.cx.shape[0]} does not match basis with "
-                         f"{basis.num_coeffs} columns")
-    M = np.stack([basis.W, basis.Wdot, basis.Wddot])
-    px, py = M @ coeffs.cx, M @ coeffs.cy
-    return TrajectorySamples(x=px[0], y=py[0], xdot=px[1], ydot=py[1], xddot=px[2], yddot=py[2])
+    """Position, velocity and acceleration of one trajectory on the basis grid (host fp64; the
+    batched form is ``bd_eval`` behind LowerLevelSolver.velocities)."""
+    n = basis.num_coeffs
+    if coeffs.cx.shape[0] != n:
+        raise ValueError(f"{coeffs.cx.shape[0]} coefficients per axis for a basis of {n} functions")
+    stack = np.stack([basis.W, basis.Wdot, basis.Wddot])          # (3, m, n)
+    ex, ey = stack @ coeffs.cx, stack @ coeffs.cy
+    return TrajectorySamples(ex[0], ey[0], ex[1], ey[1], ex[2], ey[2])
 
 
 def curvature_from_derivatives(xdot, ydot, xddot, yddot) -> np.ndarray:
@@ -172,16 +179,21 @@ def curvature_from_derivatives(xdot, ydot, xddot, yddot) -> np.ndarray:
 
 def flat_to_controls(basis: PolynomialBasis, coeffs: TrajectoryCoeffs, wheelbase: float, eps_v: float = 1e-3,
                      times: np.ndarray | None = None) -> FlatControls:
-    """Bicycle controls from the flat outputs (pkg/basis.py:206-234)."""
+    """Kinematic-bicycle controls implied by the flat outputs (speed, steering, longitudinal
+    acceleration, heading, path curvature), on the basis grid or at `times`; SpeedSingularity
+    when the speed reaches eps_v anywhere.  Batched on the device: ``bd_controls``."""
     if times is None:
-        s = eval_trajectory(basis, coeffs)
-        xd, yd, xdd, ydd = s.xdot, s.ydot, s.xddot, s.yddot
+        smp = eval_trajectory(basis, coeffs)
+        d1 = (smp.xdot, smp.ydot)
+        d2 = (smp.xddot, smp.yddot)
     else:
         _, Wd, Wdd = basis.matrices_at(times)
-        xd, yd, xdd, ydd = Wd @ coeffs.cx, Wd @ coeffs.cy, Wdd @ coeffs.cx, Wdd @ coeffs.cy
-    v = np.hypot(xd, yd)
-    if np.any(v <= eps_v):
-        raise SpeedSingularity(f"speed drops to {v.min():.3g} m/s (floor {eps_v:g})")
-    kappa = (ydd * xd - xdd * yd) / v**3
-    return FlatControls(v=v, delta=np.arctan(kappa * wheelbase), accel=(xd * xdd + yd * ydd) / v,
-                        psi=np.arctan2(yd, xd), kappa=kappa)
+        d1 = (Wd @ coeffs.cx, Wd @ coeffs.cy)
+        d2 = (Wdd @ coeffs.cx, Wdd @ coeffs.cy)
+    speed = np.hypot(*d1)
+    if (speed <= eps_v).any():
+        raise SpeedSingularity(f"speed reaches {speed.min():.3g} m/s, at or below the floor {eps_v:g}")
+    path_kappa = (d2[1] * d1[0] - d2[0] * d1[1]) / speed ** 3
+    return FlatControls(v=speed, delta=np.arctan(path_kappa * wheelbase),
+                        accel=(d1[0] * d2[0] + d1[1] * d2[1]) / speed, psi=np.arctan2(d1[1], d1[0]),
+                        kappa=path_kappa)
