@@ -33,6 +33,7 @@ namespace bd {
 struct AmArgs {
     int m, neq, n_obs, n_curv, B, s_cta, max_iters;
     double rho;
+    int sorted;                 // 1: scene tiles hold each timestep's obstacles sorted by -x/a (float2)
     const float* wrow;          // m x WROW        [W | Wd | Wdd] rows, fp32
     const double* kblk;         // 2 x NC x KROW   per-axis aug-KKT inverse blocks
     const double* kb;           // NX x neq        xi-b block of the aug-KKT inverse
@@ -137,6 +138,9 @@ __device__ __forceinline__ void group_reduce_scatter(float (&v)[NV], int lane) {
 // forward evaluation, polar split + coupled clips, back-projection of the residuals
 // (v[2k] = g_x[k], v[2k+1] = g_y[k]), the direct residual (v[22]) and the upper cost (v[23]).
 // The x/y pairs run as packed fp32x2 (FFMA2 with the basis value broadcast).
+constexpr int SORT_MIN_PAIRS = 8;     // >= 16 obstacles: sorted-window obstacle pass (dense scenes)
+constexpr int SORT_MAX_OBS = 128;     // the binary search covers up to 128 obstacles per timestep
+
 #ifndef BD_AM_OBS_EARLY
 #define BD_AM_OBS_EARLY 1
 #endif
@@ -144,12 +148,15 @@ template <int P, bool CURV, bool INIT, int NV, int MT, int NPT, int TPB>
 __device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float4* __restrict__ osm,
                                       const float* __restrict__ csm, const float2 (&cxy)[NC], float (&v)[NV],
                                       float* dap, float* kap, int dstride_rt, int p, int m_rt, int npair_rt,
-                                      int n_curv, const SceneLim& L, int& conf, bool& ovf) {
+                                      int n_curv, const SceneLim& L, int& conf, bool& ovf, bool sorted_rt) {
     // MT / NPT / TPB > 0: timesteps, obstacle pairs and CTA size fixed at compile time (the
     // BASELINE shapes), so the tile addressing folds into immediates and the pair loop unrolls.
     const int m = MT ? MT : m_rt;
     const int npair = NPT ? NPT : npair_rt;
     const int dstride = TPB ? TPB : dstride_rt;
+    // dense scenes: obstacles of a timestep sorted by -x/a, only the window |X/a - x_o/a| < 1 is
+    // visited (binary search + short scan) instead of every obstacle
+    const bool sorted = NPT ? (NPT >= SORT_MIN_PAIRS) : sorted_rt;
 #pragma unroll
     for (int k = 0; k < NV; ++k) v[k] = 0.f;
     int j = 0;
@@ -166,7 +173,7 @@ __device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float
         const float4* op = osm + t * npair;          // (-x0, -x1, -y0, -y1) / (a, a, b, b)
         float qmin = 3.0e38f;
 #if BD_AM_OBS_EARLY
-        if (NPT > 0) {
+        if (NPT > 0 && NPT < SORT_MIN_PAIRS) {
             // position first, then the obstacle-distance pass interleaved with the derivative
             // chains so the tile's shared-memory latency hides behind them
 #pragma unroll
@@ -239,14 +246,40 @@ __device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float
         const float xs = X * L.inv_a, ys = Y * L.inv_b;
         float rox = 0.f, roy = 0.f, coll = 0.f;
 #pragma unroll 5
-        for (int o = 0; o < ((BD_AM_OBS_EARLY && NPT > 0) ? 0 : npair); ++o) {
+        for (int o = 0; o < ((BD_AM_OBS_EARLY && NPT > 0) || sorted ? 0 : npair); ++o) {
             const float4 ob = op[o];
             const float2 wc = fadd2(make_float2(xs, xs), make_float2(ob.x, ob.y));
             const float2 ws = fadd2(make_float2(ys, ys), make_float2(ob.z, ob.w));
             const float2 q = ffma2(wc, wc, fmul2(ws, ws));
             qmin = fminf(qmin, fminf(q.x, q.y));
         }
-        if (qmin < 1.f) {
+        if (sorted) {
+            const float2* row = reinterpret_cast<const float2*>(osm) + (size_t)t * 2 * npair;
+            const int nob = 2 * npair;
+            // rounding-safe window: every obstacle with |fl(xs + ox')| < 1 lies strictly inside
+            const float win = 1.0f + fmaf(4e-6f, fabsf(xs), 1e-5f);
+            const float lo_key = -xs - win, hi_key = -xs + win;
+            int k = 0;
+#pragma unroll
+            for (int step = 64; step > 0; step >>= 1)
+                if (k + step <= nob && row[k + step - 1].x <= lo_key) k += step;
+            for (; k < nob; ++k) {
+                const float2 ob = row[k];
+                if (!(ob.x < hi_key)) break;
+                const float wc = xs + ob.x, ws = ys + ob.y;
+                const float q = fmaf(wc, wc, ws * ws);
+                if (q < 1.f) {
+                    coll += 1.f - q;
+                    if (q > 0.f) {
+                        const float f = 1.f - rsqrtf(q);
+                        rox = fmaf(wc, f, rox);
+                        roy = fmaf(ws, f, roy);
+                    } else {
+                        rox -= 1.f;
+                    }
+                }
+            }
+        } else if (qmin < 1.f) {
             for (int o = 0; o < npair; ++o) {
                 const float4 ob = op[o];
 #pragma unroll
@@ -418,7 +451,7 @@ __global__ void __launch_bounds__(256, BD_AM_MINB) am_kernel(const AmArgs a) {
         }
     };
     sweep<P, CURV, true, NV, MT, NPT, TPB>(wsm, osm, csm, cxy, v, dap, kap, threads, p, m, n_obs / 2, a.n_curv, L,
-                                           conf, ovf);
+                                           conf, ovf, a.sorted != 0);
     reduce();
 
     const int r_lane = NX % RP, r_slot = (NX / RP) * RP;
@@ -474,7 +507,7 @@ __global__ void __launch_bounds__(256, BD_AM_MINB) am_kernel(const AmArgs a) {
         for (int q = 0; q < NC; ++q) cxy[q] = reinterpret_cast<const float2*>(sc)[q];
         // ---- projections, back-projection, residual at the new iterate
         sweep<P, CURV, false, NV, MT, NPT, TPB>(wsm, osm, csm, cxy, v, dap, kap, threads, p, m, n_obs / 2, a.n_curv,
-                                                L, conf, ovf);
+                                                L, conf, ovf, a.sorted != 0);
         reduce();
         resid = v[r_slot];
         cost = v[c_slot];
@@ -544,6 +577,30 @@ __global__ void exit_scan_kernel(const unsigned* itmax, int max_iters, double to
     const int scene = blockIdx.x;
     exit_scan_block(itmax + (size_t)scene * max_iters * ITMAX_SLOTS, max_iters, tol, scene, iters_used, replay,
                     conflicts);
+}
+
+// Dense scenes: rewrite each (scene, timestep) row of the pair tile [(-x0,-x1,-y0,-y1) per pair]
+// in place as obstacles (ox', oy') sorted ascending by ox' = -x/a (stable), the layout of the
+// sorted-window obstacle pass.  One thread per row; rows are tiny (<= a few hundred values).
+__global__ void sort_tile_kernel(float4* tile, int rows, int npair) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    float4* row4 = tile + (size_t)r * npair;
+    float2* row2 = reinterpret_cast<float2*>(row4);
+    constexpr int CAP = 256;
+    float xs[CAP], ys[CAP];
+    const int n = min(2 * npair, CAP);
+    for (int p = 0; p < n / 2; ++p) {
+        const float4 v = row4[p];
+        xs[2 * p] = v.x; xs[2 * p + 1] = v.y; ys[2 * p] = v.z; ys[2 * p + 1] = v.w;
+    }
+    for (int i = 1; i < n; ++i) {                 // insertion sort: stable, ties keep obstacle order
+        const float kx = xs[i], ky = ys[i];
+        int j = i - 1;
+        while (j >= 0 && xs[j] > kx) { xs[j + 1] = xs[j]; ys[j + 1] = ys[j]; --j; }
+        xs[j + 1] = kx; ys[j + 1] = ky;
+    }
+    for (int i = 0; i < n; ++i) row2[i] = make_float2(xs[i], ys[i]);
 }
 
 }  // namespace bd

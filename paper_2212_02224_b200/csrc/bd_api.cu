@@ -79,6 +79,7 @@ struct bd_ctx {
     DevBuf kblk, kb, aeq;
     // scenes
     int S = 0, scene_obs = 0, obs_pad = 0, n_curv = 0;
+    int obs_sorted = 0;          // scene tiles in the sorted-window layout (dense scenes)
     DevBuf obs, lim, bscene, curvf, ox64, oy64, lim64, curv64;
     // workspace
     DevBuf w_xibar, w_b, w_mu, w_xi, w_res, w_cost, w_hist, w_itmax, w_iters, w_replay, w_conf, w_err, w_params, w_done,
@@ -457,6 +458,7 @@ int run_projection(bd_ctx* ctx, int B, const double* xi_bar, const double* b, in
     a.rho = ctx->rho;
     a.wrow = ctx->wrow.as<float>(); a.kblk = ctx->kblk.as<double>(); a.kb = ctx->kb.as<double>();
     a.aeq = ctx->aeq.as<double>(); a.obs = ctx->obs.as<float4>(); a.lim = ctx->lim.as<SceneLim>();
+    a.sorted = ctx->obs_sorted;
     a.bscene = ctx->bscene.as<double>(); a.curv = ctx->curvf.as<float>();
     a.xi_bar = xi_bar; a.b = b; a.xi_out = xi; a.resid_out = res; a.cost_out = cost; a.hist_out = hist;
     a.itmax = ctx->w_itmax.as<unsigned>(); a.conflicts = conf; a.err = ctx->w_err.as<int>();
@@ -476,6 +478,7 @@ AmArgs projection_args(bd_ctx* ctx, int B, const double* xi_bar, int iters, doub
     a.rho = ctx->rho;
     a.wrow = ctx->wrow.as<float>(); a.kblk = ctx->kblk.as<double>(); a.kb = ctx->kb.as<double>();
     a.aeq = ctx->aeq.as<double>(); a.obs = ctx->obs.as<float4>(); a.lim = ctx->lim.as<SceneLim>();
+    a.sorted = ctx->obs_sorted;
     a.bscene = ctx->bscene.as<double>(); a.curv = ctx->curvf.as<float>();
     a.xi_bar = xi_bar; a.xi_out = xi; a.resid_out = res; a.cost_out = cost;
     a.itmax = ctx->w_itmax.as<unsigned>(); a.conflicts = ctx->w_conf.as<unsigned long long>();
@@ -718,6 +721,19 @@ int bd_set_projection(bd_ctx* ctx, int n_obs, double rho, int neq, const double*
 
 // Per-scene road curvature tables (np.interp abscissae + curvatures, pkg/constraints.py:67-72),
 // fp32 for the AM kernel's clip window and fp64 for the residual evaluator; n_curv = 0 disables.
+// Dense scenes get the sorted-window tile layout (am_kernel.cuh: sort_tile_kernel).
+static int finish_tile(bd_ctx* ctx, int S, int m, int nop) {
+    ctx->obs_sorted = 0;
+    if (nop >= 2 * SORT_MIN_PAIRS && nop <= 256) {
+        const int rows = S * m;
+        sort_tile_kernel<<<(rows + 127) / 128, 128, 0, ctx->stream>>>(ctx->obs.as<float4>(), rows, nop / 2);
+        ctx->launches++;
+        ctx->obs_sorted = 1;
+        CU(cudaGetLastError());
+    }
+    return 0;
+}
+
 static int upload_curvature(bd_ctx* ctx, int S, int n_curv, const double* cx, const double* ck) {
     if (n_curv > 0) {
         std::vector<float> cf((size_t)S * 2 * n_curv);
@@ -795,6 +811,7 @@ int bd_set_scenes(bd_ctx* ctx, int S, int n_obs, int m, const double* ox, const 
     if ((rc = upload_curvature(ctx, S, n_curv, cx, ck))) return rc;
     CU(ctx->w_err.ensure((size_t)S * 4));
     CU(cudaMemset(ctx->w_err.p, 0, (size_t)S * 4));
+    if ((rc = finish_tile(ctx, S, m, nop))) return rc;
     ctx->S = S;
     ctx->scene_obs = n_obs;
     ctx->obs_pad = nop;
@@ -1296,6 +1313,7 @@ int bd_build_scenes(bd_ctx* ctx, int S, int n_veh_max, const double* ego, const 
                 ctx->host_out = true;
             }
         }
+    if ((rc = finish_tile(ctx, S, m, nop))) return rc;
     ctx->S = S;
     ctx->scene_obs = n_obs;
     ctx->obs_pad = nop;
