@@ -121,3 +121,30 @@ def test_random_controls_against_oracle():
         np.testing.assert_allclose(st.veh[s, :nv], veh[:, :5], rtol=1e-10, atol=1e-8)
         np.testing.assert_array_equal(st.veh_ext[s, :nv, 3], veh[:, 8])
         np.testing.assert_array_equal(st.world[s], ws)
+
+
+def test_ragged_worlds_empty_and_crowded_against_oracle():
+    """World batches with no neighbours and with more neighbours than one CTA has threads
+    (the per-neighbour loops stride), and a 5-lane road, against the oracle restatement."""
+    from oracle import sim as osim
+    from paper_2212_02224_b200.sim import RoadSpec, ScenarioConfig, SimState
+    scs = [ScenarioConfig(RoadSpec(3), 1.0, 0, 21), ScenarioConfig(RoadSpec(5), 6.0, 200, 22),
+           ScenarioConfig(RoadSpec(2), 1.5, 9, 23)]
+    st = SimState.spawn(scs)
+    h0 = SimState.spawn(scs)
+    rng = np.random.default_rng(4)
+    ctrl = np.stack([rng.uniform(-2, 2, 25), rng.uniform(-0.1, 0.1, 25)], axis=1)[None].repeat(3, 0)
+    _sim().run(st, ctrl, 25)
+    for s, sc in enumerate(scs):
+        nv = sc.vehicle_count
+        ego = np.concatenate([h0.ego[s], [h0.ego_ts[s]]])
+        veh = np.concatenate([h0.veh[s, :nv], h0.veh_ext[s, :nv]], axis=1)
+        ws = h0.world[s]
+        road = np.array([sc.road.lane_count, sc.road.lane_width, sc.road.length, sc.dt])
+        for t in range(25):
+            ego, veh, ws = osim.step(ego, veh, ws, road, ctrl[s, t, 0], ctrl[s, t, 1])
+        np.testing.assert_allclose(st.ego[s], ego[:8], rtol=1e-10, atol=1e-8)
+        if nv:
+            np.testing.assert_allclose(st.veh[s, :nv], veh[:, :5], rtol=1e-10, atol=1e-8)
+            np.testing.assert_array_equal(st.veh_ext[s, :nv, 3], veh[:, 8])
+        np.testing.assert_array_equal(st.world[s], ws)
