@@ -157,6 +157,10 @@ int bd_solve_lower_shard(bd_ctx* ctx, int batch, const double* params, int max_i
                          double* residuals, double* cost, float* iter_max);
 int bd_replay_shard(bd_ctx* ctx, int batch, const double* xi_bar, int iterations, double* xi, double* residuals,
                     double* cost);
+/* Same, with the iteration count read on the device (one int; <= 0: keep the first pass) so a
+ * sharded CEM iteration needs no host round trip between the all-reduce and the ranking. */
+int bd_replay_shard_dev(bd_ctx* ctx, int batch, const double* xi_bar, int max_iters, const int* iterations,
+                        double* xi, double* residuals, double* cost);
 
 /* ------------------------------------------------------------------ upper level */
 

@@ -44,6 +44,7 @@ SIGNATURES = {
     "bd_kkt_solve": (c_int, [_P, c_int, c_int, _P, _P, c_int, _P, _P]),
     "bd_solve_lower_shard": (c_int, [_P, c_int, _P, c_int, _P, _P, _P, _P, _P]),
     "bd_replay_shard": (c_int, [_P, c_int, _P, c_int, _P, _P, _P]),
+    "bd_replay_shard_dev": (c_int, [_P, c_int, _P, c_int, _P, _P, _P, _P]),
     "bd_sample_philox": (c_int, [_P, c_int, c_int, _P, _P, c_uint64, c_int, c_int, c_int, _P]),
     "bd_sample": (c_int, [_P, c_int, c_int, _P, _P, _P, _P]),
     "bd_rank_refit": (c_int, [_P, c_int, c_int, c_int, _P, _P, _P, c_int, c_int, c_double, c_double, c_double, _P, _P,

@@ -1008,6 +1008,33 @@ int bd_replay_shard(bd_ctx* ctx, int B, const double* xi_bar, int iters, double*
     return finish_call(ctx, true, 1);
 }
 
+int bd_replay_shard_dev(bd_ctx* ctx, int B, const double* xi_bar, int max_iters, const int* iterations, double* xi,
+                        double* res, double* cost) {
+    NvtxRange nvtx_("bd_replay_shard_dev");
+    if (!ctx) return BD_ERR_VALUE;
+    int rc = require_solver(ctx, false);
+    if (rc) return rc;
+    if (ctx->S != 1 || B < 1 || !xi_bar || !xi || !res || !iterations || max_iters < 1)
+        return fail(ctx, BD_ERR_VALUE, "bad replay");
+    begin_call(ctx);
+    const double* dxb;
+    const int* dit;
+    double *dxi, *dres, *dcost;
+    if ((rc = stage_in(ctx, xi_bar, (size_t)B * NX, &dxb))) return rc;
+    if ((rc = stage_in(ctx, iterations, 1, &dit))) return rc;
+    if ((rc = stage_out(ctx, xi, (size_t)B * NX, ctx->w_xi, &dxi))) return rc;
+    if ((rc = stage_out(ctx, res, (size_t)B, ctx->w_res, &dres))) return rc;
+    if ((rc = stage_out(ctx, cost, (size_t)B, ctx->w_cost, &dcost))) return rc;
+    CU(ctx->w_itmax.ensure((size_t)max_iters * ITMAX_SLOTS * 4));
+    CU(ctx->w_replay.ensure(4));
+    CU(ctx->w_conf.ensure(8));
+    // the guarded kernel reads the count on the device: <= 0 returns at once, so no host decision
+    CU(cudaMemcpyAsync(ctx->w_replay.p, dit, 4, cudaMemcpyDeviceToDevice, ctx->stream));
+    AmArgs a = projection_args(ctx, B, dxb, max_iters, dxi, dres, dcost);
+    if ((rc = launch_am(ctx, a, true))) return rc;
+    return finish_call(ctx, false, 0);
+}
+
 int bd_sample_philox(bd_ctx* ctx, int dim, int count, const double* mean, const double* cov, uint64_t seed,
                      int scene, int iteration, int first_index, double* params) {
     NvtxRange nvtx_("bd_sample_philox");

@@ -90,36 +90,54 @@ class ShardedCEM:
         dist.all_gather(parts, pad, group=self.group)
         return torch.cat(parts)[: self.B]
 
+    def _all_reduce_sum(self, t: torch.Tensor) -> torch.Tensor:
+        if self.world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+        return t
+
     def run(self, init_mean, init_cov) -> ShardedResult:
+        """The CEM loop with every decision on the device: the batch-global exit iteration comes
+        from the all-reduced maxima as a device scalar that gates the replay kernel, the best
+        sample's coefficients reach every rank through an all-reduce of owner-masked rows, and
+        per-iteration records stay in device tensors until one transfer at the end -- no host
+        round trip inside the loop."""
         mean = self.b.tensor(init_mean)
         cov = self.b.tensor(init_cov)
-        stats, used_log = [], []
-        best = None
-        for it in range(self.N):
+        dev = mean.device
+        N = self.N
+        stats = torch.zeros((N, 6), dtype=torch.float64, device=dev)
+        used = torch.zeros(N, dtype=torch.int64, device=dev)
+        rec = torch.zeros(5, dtype=torch.float64, device=dev)        # index, cost, residual, aug (last iteration)
+        xi_best = torch.zeros(22, dtype=torch.float64, device=dev)
+        ks = None
+        for it in range(N):
             P = self.b.sample(mean, cov, self.seed, it, self.B)                 # full batch, every rank
             shard = self.b.solve_shard(P[self.lo:self.hi], self.am_iters)         # no exit decision
             itmax = self._all_reduce_max(shard["iter_max"].clone())              # C1
-            hit = torch.nonzero(itmax.double() <= self.tol)
-            used = int(hit[0, 0]) + 1 if hit.numel() else self.am_iters
-            if used < self.am_iters:                                              # batch-global exit fired
-                shard = dict(shard, **self.b.replay_shard(used))
-            used_log.append(used)
+            if ks is None:
+                ks = torch.arange(1, itmax.shape[0] + 1, device=itmax.device)
+            hit = itmax.double() <= self.tol
+            first = torch.where(hit, ks, torch.full_like(ks, self.am_iters)).min()     # used iterations
+            replay = torch.where(first < self.am_iters, first, torch.zeros_like(first)).to(torch.int32).reshape(1)
+            shard = self.b.replay_shard(replay, shard)                            # gated on the device
+            used[it] = first.to(dev)
             rc = torch.stack([shard["residuals"], shard["cost"]], dim=1)
             full = self._all_gather(rc)                                           # C2
             out = self.b.rank_refit(full[:, 0].contiguous(), full[:, 1].contiguous(), P, mean, cov, self.n, self.q,
                                     self.w, self.eta, self.gamma)
             mean, cov = out["mean"], out["cov"]
-            j = int(out["elite_idx"][0])
-            owner = min(j // self.shard, self.world - 1)
-            xi = torch.zeros(22, dtype=torch.float64, device=mean.device)
-            if self.rank == owner:
-                xi.copy_(shard["xi"][j - self.lo])
-            if self.world > 1:
-                dist.broadcast(xi, src=owner, group=self.group)
-            best = (j, xi.cpu().numpy(), float(full[j, 1]), float(full[j, 0]), float(out["elite_aug"][0]))
-            stats.append(np.asarray(out["stats"].cpu(), dtype=np.float64))
-        return ShardedResult(best[0], best[1], best[2], best[3], best[4], np.array(stats),
-                             mean.cpu().numpy(), cov.cpu().numpy(), used_log)
+            j = out["elite_idx"][:1]
+            mine = (j >= self.lo) & (j < self.hi)
+            row = shard["xi"].index_select(0, (j - self.lo).clamp(0, shard["xi"].shape[0] - 1))[0]
+            xi_best = self._all_reduce_sum(row * mine.to(row.dtype))             # owner's row, zeros elsewhere
+            pick = full.index_select(0, j)[0]
+            rec = torch.stack([j[0].to(torch.float64), pick[1], pick[0], out["elite_aug"][0].to(torch.float64)])
+            stats[it] = out["stats"].to(torch.float64)
+        self.b.check()
+        r = rec.cpu().numpy()
+        return ShardedResult(int(r[0]), xi_best.cpu().numpy(), float(r[1]), float(r[2]), float(r[3]),
+                             stats.cpu().numpy(), mean.cpu().numpy(), cov.cpu().numpy(),
+                             [int(u) for u in used.cpu().numpy()])
 
 
 class CudaShardBackend:
@@ -149,16 +167,23 @@ class CudaShardBackend:
         res = torch.empty(n, dtype=torch.float64, device=self.dev)
         cost = torch.empty_like(res)
         mx = torch.empty(iters, dtype=torch.float32, device=self.dev)
+        self._iters = iters
         self.ctx.call("bd_solve_lower_shard", n, P.contiguous(), iters, self._xb, xi, res, cost, mx)
         return {"xi": xi, "residuals": res, "cost": cost, "iter_max": mx}
 
-    def replay_shard(self, iters):
+    def replay_shard(self, iters, shard):
+        """Re-run the shard for iters[0] AM iterations when > 0 (device-gated, in place)."""
         n = self._xb.shape[0]
-        xi = torch.empty_like(self._xb)
-        res = torch.empty(n, dtype=torch.float64, device=self.dev)
-        cost = torch.empty_like(res)
-        self.ctx.call("bd_replay_shard", n, self._xb, iters, xi, res, cost)
-        return {"xi": xi, "residuals": res, "cost": cost}
+        self.ctx.call("bd_replay_shard_dev", n, self._xb, self._iters, iters.to(self.dev).contiguous(), shard["xi"],
+                      shard["residuals"], shard["cost"])
+        return shard
+
+    def check(self):
+        """Raise for any device error of the loop (checked once, after it)."""
+        bits = self.ctx.error_bits() if hasattr(self.ctx, "error_bits") else 0
+        if bits:
+            from .batch_qp import NumericalFailure
+            raise NumericalFailure(f"sharded CEM: device error bits {bits:#x}")
 
     def rank_refit(self, resid, cost, P, mean, cov, n, q, w, eta, gamma):
         B = resid.shape[0]

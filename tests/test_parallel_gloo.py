@@ -55,11 +55,17 @@ class OracleShardBackend:
                 "cost": torch.as_tensor(cost),
                 "iter_max": torch.as_tensor(pr["history"].max(axis=1).astype(np.float32))}
 
-    def replay_shard(self, iters):
-        self.calls.append(("replay", iters))
-        pr, cost = self._project(iters)
+    def replay_shard(self, iters, shard):
+        k = int(iters[0])                      # device-gated in the CUDA backend: <= 0 keeps the first pass
+        if k <= 0:
+            return shard
+        self.calls.append(("replay", k))
+        pr, cost = self._project(k)
         return {"xi": torch.as_tensor(pr["xi"].T.copy()), "residuals": torch.as_tensor(pr["residuals"]),
                 "cost": torch.as_tensor(cost)}
+
+    def check(self):
+        pass
 
     def rank_refit(self, resid, cost, P, mean, cov, n, q, w, eta, gamma):
         r, c = resid.numpy(), cost.numpy()
@@ -144,9 +150,13 @@ class FakeBackend:
         return {"xi": torch.zeros(n, 22, dtype=torch.float64), "residuals": P[:, 0].clone(),
                 "cost": torch.zeros(n, dtype=torch.float64), "iter_max": torch.as_tensor(self.itmax, dtype=torch.float32)}
 
-    def replay_shard(self, iters):
-        self.replays.append(iters)
-        return {}
+    def replay_shard(self, iters, shard):
+        if int(iters[0]) > 0:
+            self.replays.append(int(iters[0]))
+        return shard
+
+    def check(self):
+        pass
 
     def rank_refit(self, resid, cost, P, mean, cov, n, q, w, eta, gamma):
         order = torch.argsort(resid, stable=True)
