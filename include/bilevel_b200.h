@@ -157,6 +157,22 @@ int bd_solve_lower_shard(bd_ctx* ctx, int batch, const double* params, int max_i
                          double* residuals, double* cost, float* iter_max);
 int bd_replay_shard(bd_ctx* ctx, int batch, const double* xi_bar, int iterations, double* xi, double* residuals,
                     double* cost);
+/* Sharded batch over NVLink peer memory.  Each rank passes device arrays of the world's symmetric
+ * buffers and signal pads (e.g. torch symmetric memory: buffer_ptrs_dev / signal_pad_ptrs_dev) and
+ * the byte offsets of: gathered residuals (batch doubles), gathered costs (batch doubles), the
+ * per-rank iteration maxima (world x iters_cap floats), one coefficient row per rank (world x 22
+ * doubles).  bd_solve_lower_shard_p2p = bd_solve_lower_shard + the exchange: the AM epilogue
+ * stores every (residual, cost) into every rank's buffer at row0 + i, the maxima are published and
+ * awaited, the batch-global exit is decided on the device (iterations used -> *used) and the shard
+ * replayed if it fired -- after it every rank holds the whole batch's residuals and costs.
+ * bd_shard_p2p_best_row hands the coefficients of global row *best_index to every rank.  epoch:
+ * strictly increasing per CEM iteration, identical on all ranks. */
+int bd_shard_p2p_set(bd_ctx* ctx, int world, int rank, void* const* buffers, unsigned* const* signal_pads,
+                     size_t res_offset, size_t cost_offset, size_t itmax_offset, size_t row_offset, int iters_cap);
+int bd_solve_lower_shard_p2p(bd_ctx* ctx, int batch, const double* params, int max_iters, double* xi_bar, double* xi,
+                             double* residuals, double* cost, long long row0, unsigned epoch, double tol, int* used);
+int bd_shard_p2p_best_row(bd_ctx* ctx, const int64_t* best_index, long long row0, int batch, const double* xi_shard,
+                          unsigned epoch, double* xi_out);
 /* Same, with the iteration count read on the device (one int; <= 0: keep the first pass) so a
  * sharded CEM iteration needs no host round trip between the all-reduce and the ranking. */
 int bd_replay_shard_dev(bd_ctx* ctx, int batch, const double* xi_bar, int max_iters, const int* iterations,

@@ -9,7 +9,7 @@ from __future__ import annotations
 
 import ctypes
 import os
-from ctypes import POINTER, c_char_p, c_double, c_int, c_int64, c_uint64, c_void_p
+from ctypes import POINTER, c_char_p, c_double, c_int, c_int64, c_longlong, c_size_t, c_uint, c_uint64, c_void_p
 
 import numpy as np
 
@@ -45,6 +45,9 @@ SIGNATURES = {
     "bd_solve_lower_shard": (c_int, [_P, c_int, _P, c_int, _P, _P, _P, _P, _P]),
     "bd_replay_shard": (c_int, [_P, c_int, _P, c_int, _P, _P, _P]),
     "bd_replay_shard_dev": (c_int, [_P, c_int, _P, c_int, _P, _P, _P, _P]),
+    "bd_shard_p2p_set": (c_int, [_P, c_int, c_int, _P, _P, c_size_t, c_size_t, c_size_t, c_size_t, c_int]),
+    "bd_solve_lower_shard_p2p": (c_int, [_P, c_int, _P, c_int, _P, _P, _P, _P, c_longlong, c_uint, c_double, _P]),
+    "bd_shard_p2p_best_row": (c_int, [_P, _P, c_longlong, c_int, _P, c_uint, _P]),
     "bd_sample_philox": (c_int, [_P, c_int, c_int, _P, _P, c_uint64, c_int, c_int, c_int, _P]),
     "bd_sample": (c_int, [_P, c_int, c_int, _P, _P, _P, _P]),
     "bd_rank_refit": (c_int, [_P, c_int, c_int, c_int, _P, _P, _P, c_int, c_int, c_double, c_double, c_double, _P, _P,

@@ -57,6 +57,13 @@ struct AmArgs {
     int* iters_used;            // S (nullptr: no in-kernel scan)
     int* replay_out;            // S
     unsigned* done_ctr;         // S, zero before the launch, re-armed to zero by the last CTA
+    // sharded batch over NVLink peer memory (nullptr: off): every (residual, cost) is also stored
+    // straight into each rank's gathered arrays at global row p2p_row0 + local (the all-gather
+    // fused into the epilogue, overlapping the remaining CTAs' math)
+    void* const* p2p_bufs;      // world device pointers (symmetric buffers, peer-mapped)
+    int p2p_world;
+    long long p2p_row0;
+    size_t p2p_res_off, p2p_cost_off;
 };
 
 __device__ __forceinline__ void exit_scan_block(const unsigned* base, int max_iters, double tol, int scene,
@@ -536,6 +543,12 @@ __global__ void __launch_bounds__(256, BD_AM_MINB) am_kernel(const AmArgs a) {
         }
         if (own == r_lane) a.resid_out[row] = static_cast<double>(resid);
         if (a.cost_out && own == c_lane) a.cost_out[row] = static_cast<double>(cost);
+        if (a.p2p_bufs && (own == r_lane || own == c_lane)) {
+            const size_t off = own == r_lane ? a.p2p_res_off : a.p2p_cost_off;
+            const double val = static_cast<double>(own == r_lane ? resid : cost);
+            for (int g = 0; g < a.p2p_world; ++g)
+                reinterpret_cast<double*>(static_cast<char*>(a.p2p_bufs[g]) + off)[a.p2p_row0 + local] = val;
+        }
     } else {
         conf = 0;
         bad = false;

@@ -22,6 +22,7 @@
 #include <cudaTypedefs.h>
 #include "scene_kernels.cuh"
 #include "sim_kernels.cuh"
+#include "p2p_kernels.cuh"
 
 using namespace bd;
 
@@ -97,6 +98,10 @@ struct bd_ctx {
     int n_ctrl = 0;
     double ctrl_wb = 0, ctrl_amax = 0, ctrl_steer = 0, ctrl_eps = 0;
     DevBuf ctrl_wd, ctrl_wdd, w_sing, w_accel, w_steer;
+    // sharded batch over NVLink peer memory (bd_shard_p2p_set)
+    P2PArgs p2p{};
+    bool p2p_set = false, p2p_epilogue = false;
+    long long p2p_row0 = 0;
     // closed-loop simulation (in/out staging of host world state)
     DevBuf sim_io[7];
     // CVAE
@@ -314,6 +319,7 @@ int finish_call(bd_ctx* ctx, bool check_err, int n_err) {
         if (bits & ERR_BAD_RHS) return fail(ctx, BD_ERR_VALUE, "right-hand sides must be finite");
         if (bits & ERR_KKT_RESID) return fail(ctx, BD_ERR_NUMERICAL, "KKT residual exceeds tolerance");
         if (bits & ERR_NONFINITE) return fail(ctx, BD_ERR_NUMERICAL, "projection iterate is not finite");
+        if (bits & ERR_P2P_TIMEOUT) return fail(ctx, BD_ERR_CUDA, "peer exchange timed out (a rank never signalled)");
         if (bits & ERR_RANGE)
             return fail(ctx, BD_ERR_NUMERICAL, "projection iterate left the fp32 range of the device sweep (|x| > 1e18 m)");
     }
@@ -456,6 +462,10 @@ int run_projection(bd_ctx* ctx, int B, const double* xi_bar, const double* b, in
     AmArgs a{};
     a.m = ctx->m; a.neq = ctx->neq; a.n_obs = ctx->obs_pad; a.n_curv = ctx->n_curv; a.B = B; a.max_iters = iters;
     a.rho = ctx->rho;
+    if (ctx->p2p_epilogue) {
+        a.p2p_bufs = ctx->p2p.bufs; a.p2p_world = ctx->p2p.world; a.p2p_row0 = ctx->p2p_row0;
+        a.p2p_res_off = ctx->p2p.res_off; a.p2p_cost_off = ctx->p2p.cost_off;
+    }
     a.wrow = ctx->wrow.as<float>(); a.kblk = ctx->kblk.as<double>(); a.kb = ctx->kb.as<double>();
     a.aeq = ctx->aeq.as<double>(); a.obs = ctx->obs.as<float4>(); a.lim = ctx->lim.as<SceneLim>();
     a.sorted = ctx->obs_sorted;
@@ -476,6 +486,10 @@ AmArgs projection_args(bd_ctx* ctx, int B, const double* xi_bar, int iters, doub
     AmArgs a{};
     a.m = ctx->m; a.neq = ctx->neq; a.n_obs = ctx->obs_pad; a.n_curv = ctx->n_curv; a.B = B; a.max_iters = iters;
     a.rho = ctx->rho;
+    if (ctx->p2p_epilogue) {
+        a.p2p_bufs = ctx->p2p.bufs; a.p2p_world = ctx->p2p.world; a.p2p_row0 = ctx->p2p_row0;
+        a.p2p_res_off = ctx->p2p.res_off; a.p2p_cost_off = ctx->p2p.cost_off;
+    }
     a.wrow = ctx->wrow.as<float>(); a.kblk = ctx->kblk.as<double>(); a.kb = ctx->kb.as<double>();
     a.aeq = ctx->aeq.as<double>(); a.obs = ctx->obs.as<float4>(); a.lim = ctx->lim.as<SceneLim>();
     a.sorted = ctx->obs_sorted;
@@ -1032,6 +1046,91 @@ int bd_replay_shard_dev(bd_ctx* ctx, int B, const double* xi_bar, int max_iters,
     CU(cudaMemcpyAsync(ctx->w_replay.p, dit, 4, cudaMemcpyDeviceToDevice, ctx->stream));
     AmArgs a = projection_args(ctx, B, dxb, max_iters, dxi, dres, dcost);
     if ((rc = launch_am(ctx, a, true))) return rc;
+    return finish_call(ctx, false, 0);
+}
+
+int bd_shard_p2p_set(bd_ctx* ctx, int world, int rank, void* const* bufs, unsigned* const* sigs, size_t res_off,
+                     size_t cost_off, size_t itmax_off, size_t xi_off, int iters_cap) {
+    if (!ctx) return BD_ERR_VALUE;
+    if (world < 1 || rank < 0 || rank >= world || !bufs || !sigs || iters_cap < 1)
+        return fail(ctx, BD_ERR_VALUE, "bad peer exchange description");
+    if (!is_device_ptr(bufs) || !is_device_ptr(sigs))
+        return fail(ctx, BD_ERR_VALUE, "peer pointer tables must be device arrays");
+    ctx->p2p = P2PArgs{world, rank, iters_cap, bufs, sigs, res_off, cost_off, itmax_off, xi_off, nullptr};
+    ctx->p2p_set = true;
+    return 0;
+}
+
+int bd_solve_lower_shard_p2p(bd_ctx* ctx, int B, const double* params, int iters, double* xi_bar, double* xi,
+                             double* res, double* cost, long long row0, unsigned epoch, double tol, int* used) {
+    NvtxRange nvtx_("bd_solve_lower_shard_p2p");
+    if (!ctx) return BD_ERR_VALUE;
+    int rc = require_solver(ctx, true);
+    if (rc) return rc;
+    if (!ctx->p2p_set) return fail(ctx, BD_ERR_STATE, "peer exchange not set (bd_shard_p2p_set)");
+    if (ctx->S != 1 || ctx->with_goal || B < 1 || !params || !xi_bar || !xi || !res || iters < 1 ||
+        iters > ctx->p2p.iters_cap || row0 < 0 || epoch == 0)
+        return fail(ctx, BD_ERR_VALUE, "bad peer-exchange shard call");
+    begin_call(ctx);
+    const double* dp;
+    double *dxb, *dxi, *dres, *dcost;
+    int* dused;
+    if ((rc = stage_in(ctx, params, (size_t)B * ctx->dim, &dp))) return rc;
+    if ((rc = stage_out_req(ctx, xi_bar, (size_t)B * NX, ctx->w_xibar, &dxb))) return rc;
+    if ((rc = stage_out(ctx, xi, (size_t)B * NX, ctx->w_xi, &dxi))) return rc;
+    if ((rc = stage_out(ctx, res, (size_t)B, ctx->w_res, &dres))) return rc;
+    if ((rc = stage_out_req(ctx, cost, (size_t)B, ctx->w_cost, &dcost))) return rc;
+    if ((rc = stage_out_req(ctx, used, 1, ctx->sim_io[6], &dused))) return rc;
+    CU(ctx->w_iters.ensure(4));
+    CU(ctx->w_conf.ensure(8));
+    CU(ctx->stage[7].ensure((size_t)iters * 4));
+    P2PArgs pa = ctx->p2p;
+    pa.err = ctx->w_err.as<int>();
+    CU(cudaMemsetAsync(ctx->w_err.p, 0, 4, ctx->stream));
+    if ((rc = run_stage1(ctx, B, dp, dxb, nullptr, nullptr))) return rc;
+    ctx->p2p_epilogue = true;                 // AM epilogues store (res, cost) into every rank's buffer
+    ctx->p2p_row0 = row0;
+    rc = run_projection(ctx, B, dxb, nullptr, iters, 1.0, dxi, dres, dcost, nullptr, ctx->w_iters.as<int>(),
+                        ctx->w_conf.as<unsigned long long>(), true);
+    if (!rc) {
+        float* dmax = ctx->stage[7].as<float>();
+        itmax_reduce_kernel<<<1, 128, 0, ctx->stream>>>(ctx->w_itmax.as<unsigned>(), iters, dmax);
+        p2p_publish_kernel<<<1, 128, 0, ctx->stream>>>(pa, dmax, iters, epoch, 0);
+        p2p_wait_kernel<<<1, 32, 0, ctx->stream>>>(pa, epoch, 0);
+        p2p_exit_kernel<<<1, 128, 0, ctx->stream>>>(pa, iters, tol, ctx->w_replay.as<int>(), dused);
+        ctx->launches += 4;
+        AmArgs a = projection_args(ctx, B, dxb, iters, dxi, dres, dcost);   // replay guard (device count)
+        rc = launch_am(ctx, a, true);
+        p2p_publish_kernel<<<1, 32, 0, ctx->stream>>>(pa, nullptr, 0, epoch, 1);
+        p2p_wait_kernel<<<1, 32, 0, ctx->stream>>>(pa, epoch, 1);
+        ctx->launches += 2;
+    }
+    ctx->p2p_epilogue = false;
+    if (rc) return rc;
+    return finish_call(ctx, ctx->host_out, 1);
+}
+
+int bd_shard_p2p_best_row(bd_ctx* ctx, const int64_t* best_index, long long row0, int b_shard, const double* xi_shard,
+                          unsigned epoch, double* xi_out) {
+    NvtxRange nvtx_("bd_shard_p2p_best_row");
+    if (!ctx) return BD_ERR_VALUE;
+    if (!ctx->p2p_set) return fail(ctx, BD_ERR_STATE, "peer exchange not set (bd_shard_p2p_set)");
+    if (!best_index || !xi_shard || !xi_out || b_shard < 1 || epoch == 0) return fail(ctx, BD_ERR_VALUE, "bad row share");
+    begin_call(ctx);
+    int rc;
+    const int64_t* dbest;
+    const double* dxs;
+    double* dout;
+    if ((rc = stage_in(ctx, best_index, 1, &dbest))) return rc;
+    if ((rc = stage_in(ctx, xi_shard, (size_t)b_shard * NX, &dxs))) return rc;
+    if ((rc = stage_out(ctx, xi_out, NX, ctx->w_sing, &dout))) return rc;
+    P2PArgs pa = ctx->p2p;
+    pa.err = ctx->w_err.as<int>();
+    p2p_share_row_kernel<<<1, 32, 0, ctx->stream>>>(pa, reinterpret_cast<const long long*>(dbest), row0, b_shard, dxs,
+                                                    epoch, 2);
+    p2p_wait_kernel<<<1, 32, 0, ctx->stream>>>(pa, epoch, 2);
+    p2p_sum_rows_kernel<<<1, 32, 0, ctx->stream>>>(pa, dout);
+    ctx->launches += 3;
     return finish_call(ctx, false, 0);
 }
 

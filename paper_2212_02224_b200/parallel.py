@@ -66,7 +66,7 @@ class ShardedCEM:
     """solve_bilevel over one scene with the batch sharded across the process group."""
 
     def __init__(self, backend, batch: int, n_cons: int, n_elite: int, iterations: int, eta: float, gamma: float,
-                 residual_weight: float, am_iters: int, tol: float, seed: int, group=None):
+                 residual_weight: float, am_iters: int, tol: float, seed: int, group=None, exchange=None):
         self.b = backend
         self.B, self.n, self.q, self.N = batch, n_cons, n_elite, iterations
         self.eta, self.gamma, self.w = eta, gamma, residual_weight
@@ -74,6 +74,7 @@ class ShardedCEM:
         self.group = group
         self.rank, self.world = _world(group)
         self.lo, self.hi, self.shard = shard_range(batch, self.rank, self.world)
+        self.exchange = exchange           # P2PExchange: NVLink peer-memory exchange instead of NCCL
 
     def _all_reduce_max(self, t: torch.Tensor) -> torch.Tensor:
         if self.world > 1:
@@ -112,6 +113,20 @@ class ShardedCEM:
         ks = None
         for it in range(N):
             P = self.b.sample(mean, cov, self.seed, it, self.B)                 # full batch, every rank
+            if self.exchange is not None:
+                ex = self.exchange
+                epoch = ex.next_epoch()
+                shard = self.b.solve_shard_p2p(P[self.lo:self.hi], self.am_iters, self.lo, epoch, self.tol)
+                used[it] = shard["used"][0].to(dev)
+                full = torch.stack([ex.res, ex.cost], dim=1)                      # gathered on every rank
+                out = self.b.rank_refit(ex.res, ex.cost, P, mean, cov, self.n, self.q, self.w, self.eta, self.gamma)
+                mean, cov = out["mean"], out["cov"]
+                j = out["elite_idx"][:1]
+                xi_best = self.b.best_row_p2p(j, self.lo, shard["xi"], epoch)
+                pick = full.index_select(0, j)[0]
+                rec = torch.stack([j[0].to(torch.float64), pick[1], pick[0], out["elite_aug"][0].to(torch.float64)])
+                stats[it] = out["stats"].to(torch.float64)
+                continue
             shard = self.b.solve_shard(P[self.lo:self.hi], self.am_iters)         # no exit decision
             itmax = self._all_reduce_max(shard["iter_max"].clone())              # C1
             if ks is None:
@@ -138,6 +153,38 @@ class ShardedCEM:
         return ShardedResult(int(r[0]), xi_best.cpu().numpy(), float(r[1]), float(r[2]), float(r[3]),
                              stats.cpu().numpy(), mean.cpu().numpy(), cov.cpu().numpy(),
                              [int(u) for u in used.cpu().numpy()])
+
+
+class P2PExchange:
+    """The sharded batch's exchange over NVLink peer memory (torch symmetric memory buffers,
+    peer-mapped on every rank): the AM epilogue writes each (residual, cost) into every rank's
+    gathered arrays, maxima and the best coefficient row follow through the same buffers with
+    epoch signals (csrc/p2p_kernels.cuh) -- no NCCL call in the CEM loop."""
+
+    def __init__(self, ctx, batch: int, iters_cap: int, group=None, device=None):
+        import torch.distributed._symmetric_memory as symm
+        self.group = group if group is not None else dist.group.WORLD
+        self.rank, self.world = _world(group)
+        al = lambda x: (x + 255) // 256 * 256  # noqa: E731
+        self.res_off, self.cost_off = 0, al(8 * batch)
+        self.itmax_off = al(self.cost_off + 8 * batch)
+        self.xi_off = al(self.itmax_off + 4 * self.world * iters_cap)
+        total = al(self.xi_off + 8 * 22 * self.world)
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.buf = symm.empty(total, dtype=torch.uint8, device=dev)
+        self.buf.zero_()
+        self.hdl = symm.rendezvous(self.buf, self.group)
+        ctx.call("bd_shard_p2p_set", self.world, self.rank, int(self.hdl.buffer_ptrs_dev),
+                 int(self.hdl.signal_pad_ptrs_dev), self.res_off, self.cost_off, self.itmax_off, self.xi_off,
+                 int(iters_cap))
+        self.res = self.buf[self.res_off:self.res_off + 8 * batch].view(torch.float64)
+        self.cost = self.buf[self.cost_off:self.cost_off + 8 * batch].view(torch.float64)
+        self.epoch = 0
+        self.iters_cap = iters_cap
+
+    def next_epoch(self) -> int:
+        self.epoch += 1
+        return self.epoch
 
 
 class CudaShardBackend:
@@ -170,6 +217,24 @@ class CudaShardBackend:
         self._iters = iters
         self.ctx.call("bd_solve_lower_shard", n, P.contiguous(), iters, self._xb, xi, res, cost, mx)
         return {"xi": xi, "residuals": res, "cost": cost, "iter_max": mx}
+
+    def solve_shard_p2p(self, P, iters, row0, epoch, tol):
+        n = P.shape[0]
+        self._xb = torch.empty((n, 22), dtype=torch.float64, device=self.dev)
+        xi = torch.empty_like(self._xb)
+        res = torch.empty(n, dtype=torch.float64, device=self.dev)
+        cost = torch.empty_like(res)
+        used = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self._iters = iters
+        self.ctx.call("bd_solve_lower_shard_p2p", n, P.contiguous(), iters, self._xb, xi, res, cost, int(row0),
+                      int(epoch), float(tol), used)
+        return {"xi": xi, "residuals": res, "cost": cost, "used": used}
+
+    def best_row_p2p(self, best, row0, xi_shard, epoch):
+        out = torch.empty(22, dtype=torch.float64, device=self.dev)
+        self.ctx.call("bd_shard_p2p_best_row", best.contiguous(), int(row0), xi_shard.shape[0], xi_shard, int(epoch),
+                      out)
+        return out
 
     def replay_shard(self, iters, shard):
         """Re-run the shard for iters[0] AM iterations when > 0 (device-gated, in place)."""

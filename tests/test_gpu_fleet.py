@@ -75,3 +75,45 @@ def test_device_cem_cycle_matches_oracle_with_same_draws():
     assert rel_err_per_sample_axis(got.best_xi[0][:, None], ref.best_xi[:, None]) <= 1e-4
     np.testing.assert_allclose(got.final_mean[0], ref.mean, rtol=1e-4)
     np.testing.assert_allclose(got.stats[0][:, :3], ref.stats[:, :3], rtol=1e-4)
+
+
+@pytest.mark.parametrize("tol", [1e-3, 5.0])
+def test_sharded_p2p_exchange_world1_equals_nccl_path(tol):
+    """The NVLink peer-memory exchange (fused epilogue stores, epoch signals, device exit decision)
+    in a one-rank group (loopback) gives bit-identical results to the collective path; tol = 5
+    makes the batch-global exit fire early, exercising the device-gated replay and its re-publish."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+    from paper_2212_02224_b200.fleet import initial_distribution
+    from paper_2212_02224_b200.parallel import CudaShardBackend, P2PExchange, ShardedCEM
+    from paper_2212_02224_b200.scenes import highway_scene
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda:0"))
+    try:
+        fp = _fleet(batch=512, n=100, q=50, N=3, am_iters=60)
+        sc = highway_scene(4)
+        mean, cov = initial_distribution(sc)
+        kw = dict(batch=512, n_cons=100, n_elite=50, iterations=3, eta=0.7, gamma=0.9, residual_weight=1.0,
+                  am_iters=60, tol=tol, seed=21)
+        ref = ShardedCEM(CudaShardBackend(fp.solver, sc), **kw).run(mean, cov)
+        if tol > 1:
+            assert min(ref.iterations_used) < 60
+        be = CudaShardBackend(fp.solver, sc)
+        ex = P2PExchange(fp.context, 512, 60)
+        for _ in range(2):                       # epochs keep increasing across runs
+            got = ShardedCEM(be, exchange=ex, **kw).run(mean, cov)
+            torch.cuda.synchronize()
+            assert got.best_index == ref.best_index
+            np.testing.assert_array_equal(got.best_xi, ref.best_xi)
+            np.testing.assert_array_equal(got.mean, ref.mean)
+            np.testing.assert_array_equal(got.cov, ref.cov)
+            np.testing.assert_array_equal(got.stats, ref.stats)
+            assert got.iterations_used == ref.iterations_used
+        assert ex.epoch == 6
+    finally:
+        dist.destroy_process_group()

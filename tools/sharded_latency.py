@@ -11,7 +11,7 @@ import torch  # noqa: E402
 
 import paper_2212_02224_b200 as bd  # noqa: E402
 from paper_2212_02224_b200.fleet import FleetPlanner, initial_distribution  # noqa: E402
-from paper_2212_02224_b200.parallel import CudaShardBackend, ShardedCEM  # noqa: E402
+from paper_2212_02224_b200.parallel import CudaShardBackend, P2PExchange, ShardedCEM  # noqa: E402
 from paper_2212_02224_b200.scenes import HighwayRecipe, highway_scene  # noqa: E402
 
 basis = bd.build_basis(10, 100, 5.0, "bernstein")
@@ -30,7 +30,28 @@ for _ in range(5):
     cem.run(mean, cov)
     torch.cuda.synchronize()
     ts.append(time.perf_counter() - t0)
-print(f"ShardedCEM world=1: {1e3 * np.median(ts):.2f} ms per cycle")
+print(f"ShardedCEM world=1 (collective path): {1e3 * np.median(ts):.2f} ms per cycle")
+import socket  # noqa: E402
+
+import torch.distributed as dist  # noqa: E402
+
+with socket.socket() as s:
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                        device_id=torch.device("cuda:0"))
+cem.exchange = P2PExchange(fp.context, 10_000, 100)
+cem.run(mean, cov)
+torch.cuda.synchronize()
+ts = []
+for _ in range(5):
+    t0 = time.perf_counter()
+    cem.run(mean, cov)
+    torch.cuda.synchronize()
+    ts.append(time.perf_counter() - t0)
+print(f"ShardedCEM world=1 (peer-memory exchange): {1e3 * np.median(ts):.2f} ms per cycle")
+cem.exchange = None
+dist.destroy_process_group()
 fp.set_scenes([sc])
 fp.plan([sc], seed=1, init_mean=mean[None], init_cov=cov[None])
 ts = []
