@@ -102,7 +102,12 @@ def load() -> ctypes.CDLL:
         if not os.path.exists(LIB_PATH):
             raise ImportError(f"CUDA library missing: {LIB_PATH} (build it: python -m paper_2212_02224_b200.build)")
         lib = ctypes.CDLL(LIB_PATH)
+        # BD_AB_OLD_LIB=1 (performance A/B of older library builds only): tolerate entry points
+        # that an older build does not export
+        lax = os.environ.get("BD_AB_OLD_LIB") == "1"
         for name, (res, args) in SIGNATURES.items():
+            if lax and not hasattr(lib, name):
+                continue
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
