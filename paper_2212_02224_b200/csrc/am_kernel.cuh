@@ -340,6 +340,12 @@ __device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float
     }
 }
 
+// The all-gather fused into the epilogue: one value into every rank's symmetric buffer
+// (kept out of line so the main loop's register allocation does not see it).
+__device__ __noinline__ void p2p_store_all(void* const* bufs, int world, size_t off, long long row, double val) {
+    for (int g = 0; g < world; ++g) reinterpret_cast<double*>(static_cast<char*>(bufs[g]) + off)[row] = val;
+}
+
 // Pair barrier of the two warps that share a sample when P == 64 (named barriers 1..4).
 __device__ __forceinline__ void pair_sync() {
     asm volatile("bar.sync %0, 64;" ::"r"(1 + (int)(threadIdx.x >> 6)) : "memory");
@@ -543,12 +549,9 @@ __global__ void __launch_bounds__(256, BD_AM_MINB) am_kernel(const AmArgs a) {
         }
         if (own == r_lane) a.resid_out[row] = static_cast<double>(resid);
         if (a.cost_out && own == c_lane) a.cost_out[row] = static_cast<double>(cost);
-        if (a.p2p_bufs && (own == r_lane || own == c_lane)) {
-            const size_t off = own == r_lane ? a.p2p_res_off : a.p2p_cost_off;
-            const double val = static_cast<double>(own == r_lane ? resid : cost);
-            for (int g = 0; g < a.p2p_world; ++g)
-                reinterpret_cast<double*>(static_cast<char*>(a.p2p_bufs[g]) + off)[a.p2p_row0 + local] = val;
-        }
+        if (a.p2p_bufs && (own == r_lane || own == c_lane))
+            p2p_store_all(a.p2p_bufs, a.p2p_world, own == r_lane ? a.p2p_res_off : a.p2p_cost_off,
+                          a.p2p_row0 + local, static_cast<double>(own == r_lane ? resid : cost));
     } else {
         conf = 0;
         bad = false;
