@@ -66,7 +66,8 @@ struct AmArgs {
     size_t p2p_res_off, p2p_cost_off;
 };
 
-__device__ __forceinline__ void exit_scan_block(const unsigned* base, int max_iters, double tol, int scene,
+// out of line: run by one CTA per scene, kept away from the main loop's register allocation
+__device__ __noinline__ void exit_scan_block(const unsigned* base, int max_iters, double tol, int scene,
                                                 int* iters_used, int* replay, unsigned long long* conflicts) {
     __shared__ int red[32];
     int first = max_iters;
