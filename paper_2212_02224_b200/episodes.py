@@ -85,11 +85,13 @@ class EpisodeLog:
         return log
 
 
-def _snapshot(rec: np.ndarray, nv: int) -> dict:
-    """The run_episode step record (pkg/highway.py:478-485) from a device snapshot row."""
-    nb = rec[SNAP_HEAD:SNAP_HEAD + 4 * nv].reshape(nv, 4)
-    return {"t": round(float(rec[0]), 6), "ego": [float(v) for v in rec[1:5]], "ctrl": [float(rec[5]), float(rec[6])],
-            "neighbors": [[float(v) for v in row] for row in nb], "collision": bool(rec[7] != 0.0)}
+def _snapshots(block: np.ndarray, nv: int) -> list:
+    """run_episode step records (pkg/highway.py:478-485) from a block of device snapshot rows
+    (one C-level tolist() per block, then plain list slicing)."""
+    head = block[:, :SNAP_HEAD].tolist()
+    nbrs = block[:, SNAP_HEAD:SNAP_HEAD + 4 * nv].reshape(block.shape[0], nv, 4).tolist()
+    return [{"t": round(h[0], 6), "ego": h[1:5], "ctrl": h[5:7], "neighbors": nb, "collision": h[7] != 0.0}
+            for h, nb in zip(head, nbrs)]
 
 
 def run_episodes(scenarios, planner, replan_stride: int = 5, road_end_margin: float = 60.0, device="cuda:0",
@@ -139,9 +141,9 @@ def run_episodes(scenarios, planner, replan_stride: int = 5, road_end_margin: fl
         n = int(min(n, (lengths[active.astype(bool)] - k).min()))
         was = active.copy()
         done, snap = sim.run(st, ctrl, n, ctrl_offset=offset, x_end=x_end, active=active, snapshots=record_steps)
-        for s in np.flatnonzero(was):
-            if record_steps:
-                logs[s].steps.extend(_snapshot(snap[s, j], int(n_veh[s])) for j in range(int(done[s])))
+        if record_steps:
+            for s in np.flatnonzero(was):
+                logs[s].steps.extend(_snapshots(snap[s, :int(done[s])], int(n_veh[s])))
         k += n
         offset += n
         active[(lengths <= k) & (active != 0)] = 0
