@@ -168,3 +168,26 @@ def test_evaluate_batch_baseline_planners(case):
     assert rec.index == int(el[0])
     assert abs(rec.augmented_cost - ea[0]) <= 1e-3 * (1 + abs(ea[0]))
     assert diag["batch"] == B and diag["proj_iterations"] == int(g["iterations_used"])
+
+
+@pytest.mark.parametrize("case", ["goal", "warm"])
+def test_solve_bilevel_goal_layout_and_warm_start(case):
+    """solve_bilevel with the goal layout (per-sample goal rows) and with a WarmStartSource for
+    iteration 1 reproduce the reference's seeded runs (tests/golden/cem_variants.npz)."""
+    import paper_2212_02224_b200 as bd
+    g = load("cem_variants")
+    layout = bd.ParamLayout(4, with_goal=(case == "goal"))
+    basis = bd.build_basis(10, 100, 5.0, "bernstein")
+    solver = bd.LowerLevelSolver(basis, bd.TrackingWeights(), layout, bd.ProjectionConfig(1.0, 40, 1e-3),
+                                 g["ox"].shape[0])
+    cfg = bd.BiLevelConfig(200, 60, 20, 3, 0.7, 0.9, 1.0, g[f"{case}_mean"], g[f"{case}_cov"])
+    ws = bd.WarmStartSource(g["warm_samples"], layout) if case == "warm" else None
+    res = bd.solve_bilevel(_scene(g), solver, cfg, np.random.default_rng(5), warm_start=ws)
+    assert not res.degraded and len(res.diagnostics) == 3
+    assert res.best.index == int(g[f"{case}_best_index"])
+    np.testing.assert_allclose(res.best.params.to_vector(), g[f"{case}_best_params"], rtol=1e-10, atol=1e-10)
+    assert rel_err_per_sample_axis(res.best.coeffs.stacked()[:, None], g[f"{case}_best_xi"][:, None]) <= XI_TOL
+    stats = np.array([[s.elite_mean_upper_cost, s.best_augmented_cost, s.cov_trace, s.residual_min,
+                       s.residual_median, s.residual_max] for s in res.diagnostics])
+    np.testing.assert_allclose(stats[:, :3], g[f"{case}_stats"][:, :3], rtol=1e-4)
+    np.testing.assert_allclose(res.distribution.mean, g[f"{case}_final_mean"], rtol=1e-4)

@@ -16,6 +16,7 @@ Cases:
   worlds           build_scene / observe / controls_on_grid outputs
   sim              simulator ticks: spawn_world + step
   episodes         run_episode with scripted planners (EpisodeLog JSONL) + suite output files
+  cem_variants     solve_bilevel with the goal layout and with a warm-start source
 """
 
 from __future__ import annotations
@@ -451,13 +452,50 @@ def gen_episodes():
     print("episodes written")
 
 
+def gen_cem_variants():
+    """solve_bilevel (pkg/bilevel.py:228-295) with the goal layout (per-sample goal rows in b,
+    pkg/batch_qp.py:189-192,236-238) and with a WarmStartSource for iteration 1
+    (pkg/bilevel.py:250-251), seeded default_rng(5)."""
+    from bilevel_drive.behavior import WarmStartSource
+    env = env_for(iters=40)
+    basis = build_basis(10, 100, 5.0, "bernstein")
+    sc = highway_scene(env, basis, 3, 1.5, 18, 6)
+    out = scene_arrays(sc)
+    y0, v0 = sc.initial_state[1], 10.0
+    cases = {
+        "goal": (ParamLayout(4, with_goal=True),
+                 np.concatenate([np.full(4, y0), np.full(4, v0), [60.0, 4.0]]),
+                 np.diag(np.concatenate([np.full(4, 1.5 ** 2), np.full(4, 3.0 ** 2), [25.0, 4.0]])), None),
+        "warm": (ParamLayout(4), np.concatenate([np.full(4, y0), np.full(4, v0)]),
+                 np.diag(np.concatenate([np.full(4, 1.5 ** 2), np.full(4, 3.0 ** 2)])),
+                 np.random.default_rng(11).normal([y0] * 4 + [v0] * 4, [1.0] * 4 + [2.0] * 4, (37, 8))),
+    }
+    for name, (layout, mean, cov, warm) in cases.items():
+        solver = LowerLevelSolver(basis, TrackingWeights(), layout, ProjectionConfig(1.0, 40, 1e-3), 10)
+        cfg = BiLevelConfig(batch_size=200, constraint_elites=60, elites=20, iterations=3, eta=0.7, gamma=0.9,
+                            residual_weight=1.0, init_mean=mean, init_cov=cov)
+        ws = WarmStartSource(warm, layout) if warm is not None else None
+        res = solve_bilevel(sc, solver, cfg, np.random.default_rng(5), warm_start=ws)
+        stats = np.array([[s.elite_mean_upper_cost, s.best_augmented_cost, s.cov_trace, s.residual_min,
+                           s.residual_median, s.residual_max] for s in res.diagnostics])
+        out.update({f"{name}_mean": mean, f"{name}_cov": cov, f"{name}_best_index": res.best.index,
+                    f"{name}_best_params": res.best.params.to_vector(),
+                    f"{name}_best_xi": np.concatenate([res.best.coeffs.cx, res.best.coeffs.cy]),
+                    f"{name}_stats": stats, f"{name}_final_mean": res.distribution.mean})
+        if warm is not None:
+            out[f"{name}_samples"] = warm
+        print(f"  cem {name}: best {res.best.index}, cost {res.best.upper_cost:.2f}")
+    np.savez_compressed(os.path.join(OUT, "cem_variants.npz"), **out)
+    print("cem_variants written")
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", nargs="*", default=None)
     a = ap.parse_args()
     os.makedirs(OUT, exist_ok=True)
     jobs = {"basis": gen_basis, "lower": gen_lower, "scenes": gen_scenes, "cem_small": gen_cem_small,
-            "cem_c2": gen_cem_c2, "worlds": gen_worlds, "sim": gen_sim, "episodes": gen_episodes}
+            "cem_c2": gen_cem_c2, "worlds": gen_worlds, "sim": gen_sim, "episodes": gen_episodes, "cem_variants": gen_cem_variants}
     for name, fn in jobs.items():
         if a.only is None or name in a.only:
             fn()
