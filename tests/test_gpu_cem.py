@@ -170,10 +170,11 @@ def test_evaluate_batch_baseline_planners(case):
     assert diag["batch"] == B and diag["proj_iterations"] == int(g["iterations_used"])
 
 
-@pytest.mark.parametrize("case", ["goal", "warm"])
+@pytest.mark.parametrize("case", ["goal", "warm", "curve"])
 def test_solve_bilevel_goal_layout_and_warm_start(case):
-    """solve_bilevel with the goal layout (per-sample goal rows) and with a WarmStartSource for
-    iteration 1 reproduce the reference's seeded runs (tests/golden/cem_variants.npz)."""
+    """solve_bilevel with the goal layout (per-sample goal rows), with a WarmStartSource for
+    iteration 1 and on a curved road reproduce the reference's seeded runs
+    (tests/golden/cem_variants.npz)."""
     import paper_2212_02224_b200 as bd
     g = load("cem_variants")
     layout = bd.ParamLayout(4, with_goal=(case == "goal"))
@@ -182,7 +183,12 @@ def test_solve_bilevel_goal_layout_and_warm_start(case):
                                  g["ox"].shape[0])
     cfg = bd.BiLevelConfig(200, 60, 20, 3, 0.7, 0.9, 1.0, g[f"{case}_mean"], g[f"{case}_cov"])
     ws = bd.WarmStartSource(g["warm_samples"], layout) if case == "warm" else None
-    res = bd.solve_bilevel(_scene(g), solver, cfg, np.random.default_rng(5), warm_start=ws)
+    scene = _scene(g)
+    if case == "curve":
+        from dataclasses import replace
+        scene = bd.PlanningScene(scene.initial_state, replace(scene.spec, road_curvature=(g["curve_xs"], g["curve_ks"])),
+                                 scene.lane_centers)
+    res = bd.solve_bilevel(scene, solver, cfg, np.random.default_rng(5), warm_start=ws)
     assert not res.degraded and len(res.diagnostics) == 3
     assert res.best.index == int(g[f"{case}_best_index"])
     np.testing.assert_allclose(res.best.params.to_vector(), g[f"{case}_best_params"], rtol=1e-10, atol=1e-10)

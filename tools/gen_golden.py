@@ -470,12 +470,19 @@ def gen_cem_variants():
                  np.diag(np.concatenate([np.full(4, 1.5 ** 2), np.full(4, 3.0 ** 2)])),
                  np.random.default_rng(11).normal([y0] * 4 + [v0] * 4, [1.0] * 4 + [2.0] * 4, (37, 8))),
     }
+    cases["curve"] = (ParamLayout(4), cases["warm"][1], cases["warm"][2], None)
+    from dataclasses import replace as dc_replace
+    curved = PlanningScene(initial_state=sc.initial_state, lane_centers=sc.lane_centers,
+                           spec=dc_replace(sc.spec, road_curvature=(np.array([0.0, 30.0, 70.0, 140.0]),
+                                                                    np.array([0.0, 0.03, 0.06, 0.02]))))
+    out.update(curve_xs=curved.spec.road_curvature[0], curve_ks=curved.spec.road_curvature[1])
     for name, (layout, mean, cov, warm) in cases.items():
+        scene = curved if name == "curve" else sc
         solver = LowerLevelSolver(basis, TrackingWeights(), layout, ProjectionConfig(1.0, 40, 1e-3), 10)
         cfg = BiLevelConfig(batch_size=200, constraint_elites=60, elites=20, iterations=3, eta=0.7, gamma=0.9,
                             residual_weight=1.0, init_mean=mean, init_cov=cov)
         ws = WarmStartSource(warm, layout) if warm is not None else None
-        res = solve_bilevel(sc, solver, cfg, np.random.default_rng(5), warm_start=ws)
+        res = solve_bilevel(scene, solver, cfg, np.random.default_rng(5), warm_start=ws)
         stats = np.array([[s.elite_mean_upper_cost, s.best_augmented_cost, s.cov_trace, s.residual_min,
                            s.residual_median, s.residual_max] for s in res.diagnostics])
         out.update({f"{name}_mean": mean, f"{name}_cov": cov, f"{name}_best_index": res.best.index,
