@@ -254,9 +254,12 @@ class BatchEvaluatePlanner(_BatchPlanner):
         S = b0.shape[0]
         mean, cov = self._initial(b0, centers)
         pts = [np.atleast_2d(np.asarray(self._points(s, b0, centers, mean[s], cov), float)) for s in range(S)]
-        B = pts[0].shape[0]
-        if any(p.shape[0] != B for p in pts):
-            raise ValueError("every world must evaluate the same number of set-points per cycle")
+        counts = [p.shape[0] for p in pts]
+        B = max(counts)
+        # worlds with fewer candidates (e.g. fewer lanes) are padded with copies of their first
+        # point: a copy has the same residual and cost and a larger index, so it never outranks
+        # the original, and the batch-global exit (max residual) is unchanged
+        pts = [p if p.shape[0] == B else np.concatenate([p, np.repeat(p[:1], B - p.shape[0], axis=0)]) for p in pts]
         P = f64(np.stack(pts))                                   # S x B x dim
         dim, n2 = self.layout.dim, 2 * self.basis.num_coeffs
         xi = np.empty((S, B, n2))
@@ -279,7 +282,7 @@ class BatchEvaluatePlanner(_BatchPlanner):
         acc, ste, failures = self._emit(xi[rows, best], np.ones(S, bool))
         infos = [None if failures[s] is not None else
                  {"residual": float(res[s, best[s]]), "upper_cost": float(cost[s, best[s]]),
-                  "proj_iterations": int(used[s]), "batch": int(B)} for s in range(S)]
+                  "proj_iterations": int(used[s]), "batch": int(counts[s])} for s in range(S)]
         return CyclePlan(acc, ste, infos, failures, 0.0)
 
 
@@ -319,7 +322,7 @@ class BatchMPCRandomPlanner(BatchEvaluatePlanner):
 
 class BatchMPCGridPlanner(BatchEvaluatePlanner):
     """MPCGridPlanner (pkg/planners.py:341-385) with its default grid: lane centres x
-    (0.5, 0.75, 1.0) v_max; worlds in one batch must have the same lane count."""
+    (0.5, 0.75, 1.0) v_max."""
 
     name = "mpc-grid"
 

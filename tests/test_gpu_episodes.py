@@ -130,3 +130,32 @@ def test_run_suite_outputs(tmp_path):
     lines = open(paths["metrics"]).read().splitlines()
     assert lines[0] == "planner,scenario,episodes,collisions,collision_rate,mean_speed,failures" and len(lines) == 5
     assert len(json.load(open(paths["manifest"]))["config_hash"]) == 64
+
+
+@pytest.mark.parametrize("name", ["mpc-vanilla", "mpc-grid", "batch-mpc-goal", "mpc-random"])
+def test_batch_planners_match_reference_plan_cycle(name):
+    """One batched plan_cycle over 3 worlds (device scene build -> solve -> rank -> controls) against
+    the reference planners' own plan_cycle on the same worlds (tests/golden/planners.npz)."""
+    from paper_2212_02224_b200.planners import PlannerEnvConfig, make_batch_planner
+    from paper_2212_02224_b200.sim import SimState
+    g = load("planners")
+    n = int(g["n_worlds"])
+    n_max = max(g[f"w{k}_veh"].shape[0] for k in range(n))
+    st = SimState(np.zeros((n, 8)), np.zeros(n), np.zeros((n, n_max, 5)), np.zeros((n, n_max, 7)),
+                  np.zeros(n, np.int32), np.zeros((n, 2)), np.zeros((n, 5)))
+    for k in range(n):
+        e, v = g[f"w{k}_ego"], g[f"w{k}_veh"]
+        st.ego[k], st.ego_ts[k] = e[:8], e[8]
+        st.veh[k, : len(v)], st.veh_ext[k, : len(v)] = v[:, :5], v[:, 5:]
+        st.n_veh[k] = len(v)
+        st.road[k], st.world[k] = g[f"w{k}_road"], g[f"w{k}_world"]
+    planner = make_batch_planner(name, PlannerEnvConfig(), seed=list(range(n)) if name == "mpc-random" else 0)
+    plan = planner.plan_cycle(st.to("cuda:0"), st.road)
+    for k in range(n):
+        assert plan.failures[k] is None
+        info = plan.infos[k]
+        r_ref, c_ref = float(g[f"{name}_{k}_residual"]), float(g[f"{name}_{k}_cost"])
+        assert abs(info["residual"] - r_ref) <= 1e-3 * (1 + r_ref)
+        assert abs(info["upper_cost"] - c_ref) <= 1e-4 * max(c_ref, 1.0)
+        np.testing.assert_allclose(plan.accels[k], g[f"{name}_{k}_accel"], rtol=1e-3, atol=2e-3)
+        np.testing.assert_allclose(plan.steers[k], g[f"{name}_{k}_steer"], rtol=1e-3, atol=2e-4)

@@ -17,6 +17,7 @@ Cases:
   sim              simulator ticks: spawn_world + step
   episodes         run_episode with scripted planners (EpisodeLog JSONL) + suite output files
   cem_variants     solve_bilevel with the goal layout and with a warm-start source
+  planners         baseline planners' plan_cycle (vanilla, grid, goal, random) on a few worlds
 """
 
 from __future__ import annotations
@@ -496,13 +497,43 @@ def gen_cem_variants():
     print("cem_variants written")
 
 
+def gen_planners():
+    """Baseline planners' plan_cycle (pkg/planners.py:198-216, 309-412) on spawned + stepped worlds
+    with the PlannerEnvConfig defaults: controls on the 0.1 s grid and the plan diagnostics."""
+    from bilevel_drive.highway import step
+    from bilevel_drive.planners import make_planner
+    out = {}
+    worlds = []
+    for k, (lanes, dens, nveh, seed, nsteps) in enumerate(((4, 2.0, 24, 0, 0), (3, 1.5, 20, 5, 13), (2, 1.0, 10, 9, 7))):
+        w = spawn_world(ScenarioConfig(RoadSpec(lane_count=lanes), density=dens, vehicle_count=nveh, seed=seed))
+        for t in range(nsteps):
+            step(w, 0.6 * np.sin(0.4 * t), 0.02 * np.cos(0.3 * t))
+        worlds.append(w)
+        e = w.ego
+        out[f"w{k}_ego"] = np.array([e.x, e.y, e.psi, e.v, e.accel, e.steer, e.length, e.width, e.target_speed])
+        out[f"w{k}_veh"] = np.array([[v.x, v.y, v.psi, v.v, v.lateral_rate, v.length, v.width, v.target_speed,
+                                      v.target_lane, v.cooldown, v.accel, v.lane_index] for v in w.neighbors])
+        out[f"w{k}_road"] = np.array([w.road.lane_count, w.road.lane_width])
+        out[f"w{k}_world"] = np.array([w.time, w.step_count, 0.0, -1.0, 0.0])
+    env = PlannerEnvConfig()
+    for name in ("mpc-vanilla", "mpc-grid", "batch-mpc-goal", "mpc-random"):
+        for k, w in enumerate(worlds):
+            planner = make_planner(name, env, seed=k)
+            acc, ste, info = planner.plan_cycle(w)
+            out[f"{name}_{k}_accel"], out[f"{name}_{k}_steer"] = acc, ste
+            out[f"{name}_{k}_residual"], out[f"{name}_{k}_cost"] = info["residual"], info["upper_cost"]
+    out["n_worlds"] = len(worlds)
+    np.savez_compressed(os.path.join(OUT, "planners.npz"), **out)
+    print("planners written")
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", nargs="*", default=None)
     a = ap.parse_args()
     os.makedirs(OUT, exist_ok=True)
     jobs = {"basis": gen_basis, "lower": gen_lower, "scenes": gen_scenes, "cem_small": gen_cem_small,
-            "cem_c2": gen_cem_c2, "worlds": gen_worlds, "sim": gen_sim, "episodes": gen_episodes, "cem_variants": gen_cem_variants}
+            "cem_c2": gen_cem_c2, "worlds": gen_worlds, "sim": gen_sim, "episodes": gen_episodes, "cem_variants": gen_cem_variants, "planners": gen_planners}
     for name, fn in jobs.items():
         if a.only is None or name in a.only:
             fn()
