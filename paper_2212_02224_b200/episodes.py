@@ -226,7 +226,10 @@ def run_suite(suite: BenchmarkSuite, device="cuda:0"):
         for dt in sorted({float(sc.dt) for sc, _ in cells}):
             idx = [i for i, (sc, _) in enumerate(cells) if float(sc.dt) == dt]
             seeds = [cells[i][1] for i in idx]
-            planner = make_batch_planner(pname, suite.env, seed=seeds if pname == "mpc-random" else 0, dt=dt)
+            # each episode's planner draws from its own Generator seeded like the reference's
+            # make_planner(name, env, seed=seed) (mpc-bilevel and mpc-random)
+            kw = {"generator_seeds": seeds} if pname == "mpc-bilevel" else {}
+            planner = make_batch_planner(pname, suite.env, seed=seeds if pname == "mpc-random" else 0, dt=dt, **kw)
             t0 = time.perf_counter()
             logs = run_episodes([replace(cells[i][0], seed=cells[i][1]) for i in idx], planner,
                                 replan_stride=suite.replan_stride, device=device)

@@ -175,6 +175,15 @@ class BatchMPCBiLevelPlanner(_BatchPlanner):
 
     name = "mpc-bilevel"
 
+    def __init__(self, env: PlannerEnvConfig, seed=0, dt: float = 0.1, device: int = 0,
+                 generator_seeds=None):
+        """generator_seeds (one per world): draw each world's samples from its own numpy Generator
+        exactly like the reference planner (default_rng(seed), reset per episode), instead of the
+        device Philox stream -- closed loops then replay the reference planner's randomness."""
+        self.generator_seeds = None if generator_seeds is None else [int(x) for x in generator_seeds]
+        self._rngs = None
+        super().__init__(env, seed, dt, device)
+
     def _setup(self, device):
         env = self.env
         cfg = BiLevelConfig(env.batch_size, env.constraint_elites, env.elites, env.iterations, env.eta, env.gamma,
@@ -191,6 +200,27 @@ class BatchMPCBiLevelPlanner(_BatchPlanner):
     def reset(self):
         super().reset()
         self._warm = None
+        self._rngs = None
+
+    def _draws(self, S: int):
+        """(N, S*B, dim) normals from the worlds' Generators (state kept for failure rewinds)."""
+        if self._rngs is None:
+            if len(self.generator_seeds) != S:
+                raise ValueError(f"{len(self.generator_seeds)} generator seeds for {S} worlds")
+            self._rngs = [np.random.default_rng(x) for x in self.generator_seeds]
+        env = self.env
+        self._rng_state = [r.bit_generator.state for r in self._rngs]
+        z = np.stack([r.standard_normal((env.iterations, env.batch_size, self.layout.dim)) for r in self._rngs], axis=1)
+        return np.ascontiguousarray(z.reshape(env.iterations, S * env.batch_size, self.layout.dim))
+
+    def _rewind(self, done: np.ndarray):
+        """Leave each Generator where the reference's solve_bilevel would (pkg/bilevel.py:248-261)."""
+        N = self.env.iterations
+        for s, k in enumerate(done):
+            attempted = N if k >= N else (1 if k <= 0 else k + 1)
+            if attempted != N:
+                self._rngs[s].bit_generator.state = self._rng_state[s]
+                self._rngs[s].standard_normal((attempted, self.env.batch_size, self.layout.dim))
 
     def _plan(self, b0, centers) -> CyclePlan:
         env = self.env
@@ -205,9 +235,12 @@ class BatchMPCBiLevelPlanner(_BatchPlanner):
                           np.zeros(S, np.int32))
         # one Philox stream per (seed, cycle): worlds are distinguished by their scene index
         cfg = self.fleet.cem_config((self.seed * 1_000_003 + self.cycle) & 0xFFFFFFFFFFFF, 0)
-        self.context.call("bd_cem_cycle", S, ctypes.byref(cfg), f64(mean), f64(covs), None, None, out.best_index,
+        z = self._draws(S) if self.generator_seeds is not None else None
+        self.context.call("bd_cem_cycle", S, ctypes.byref(cfg), f64(mean), f64(covs), z, None, out.best_index,
                           out.best_params, out.best_xi, out.best_cost, out.best_residual, out.best_aug, out.stats,
                           out.final_mean, out.final_cov, out.iterations_done)
+        if z is not None:
+            self._rewind(out.iterations_done)
         ok = out.iterations_done > 0
         acc, ste, failures = self._emit(out.best_xi, ok)
         infos = []
@@ -359,9 +392,9 @@ BATCH_PLANNER_REGISTRY = {cls.name: cls for cls in (BatchMPCBiLevelPlanner, Batc
                                                       BatchMPCGoalPlanner)}
 
 
-def make_batch_planner(name: str, env: PlannerEnvConfig, seed=0, dt: float = 0.1, device: int = 0):
+def make_batch_planner(name: str, env: PlannerEnvConfig, seed=0, dt: float = 0.1, device: int = 0, **kw):
     try:
         cls = BATCH_PLANNER_REGISTRY[name]
     except KeyError:
         raise ValueError(f"unknown planner {name!r}; choose from {sorted(BATCH_PLANNER_REGISTRY)}") from None
-    return cls(env, seed=seed, dt=dt, device=device)
+    return cls(env, seed=seed, dt=dt, device=device, **kw)

@@ -516,6 +516,13 @@ def gen_planners():
         out[f"w{k}_road"] = np.array([w.road.lane_count, w.road.lane_width])
         out[f"w{k}_world"] = np.array([w.time, w.step_count, 0.0, -1.0, 0.0])
     env = PlannerEnvConfig()
+    for k, w in enumerate(worlds):                   # MPCBiLevelPlanner: two cycles (warm mean, rng stream)
+        planner = make_planner("mpc-bilevel", env, seed=k)
+        for c in range(2):
+            acc, ste, info = planner.plan_cycle(w)
+            out[f"mpc-bilevel_{k}_{c}_accel"], out[f"mpc-bilevel_{k}_{c}_steer"] = acc, ste
+            out[f"mpc-bilevel_{k}_{c}_residual"], out[f"mpc-bilevel_{k}_{c}_cost"] = info["residual"], info["upper_cost"]
+            out[f"mpc-bilevel_{k}_{c}_params"] = planner._warm_mean
     for name in ("mpc-vanilla", "mpc-grid", "batch-mpc-goal", "mpc-random"):
         for k, w in enumerate(worlds):
             planner = make_planner(name, env, seed=k)
