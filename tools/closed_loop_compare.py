@@ -44,8 +44,23 @@ for r in range(a.repeats):
     for lg in run_episodes(scs, planner):
         ours.append({"steps": len(lg.steps), "collided": lg.collided, "lane_departed": lg.lane_departed,
                      "mean_speed": lg.mean_speed(), "failed": lg.failed})
+# the reference planner's own randomness (make_planner(..., seed=0) for every episode there)
+planner = make_batch_planner("mpc-bilevel", PlannerEnvConfig(), generator_seeds=[0] * len(scs))
+same = []
+per_episode = []
+for sd, lg in zip(seeds, run_episodes(scs, planner)):
+    e = ref["episodes"][str(sd)]
+    mine = {"steps": len(lg.steps), "collided": lg.collided, "lane_departed": lg.lane_departed,
+            "mean_speed": lg.mean_speed(), "failed": lg.failed}
+    same.append(mine)
+    per_episode.append({"seed": sd, "ref_steps": e["steps"], "b200_steps": mine["steps"],
+                        "ref_collided": e["collided"], "b200_collided": mine["collided"],
+                        "ref_mean_speed": e["mean_speed"], "b200_mean_speed": mine["mean_speed"]})
 res = {"config": c, "reference": summary(list(ref["episodes"].values())), "b200": summary(ours),
-       "b200_repeats": a.repeats}
+       "b200_repeats": a.repeats, "b200_reference_generators": summary(same),
+       "same_outcome_episodes": int(sum(p["ref_steps"] == p["b200_steps"] and p["ref_collided"] == p["b200_collided"]
+                                       for p in per_episode)),
+       "per_episode_reference_generators": per_episode}
 print(json.dumps(res, indent=1))
 if a.out:
     json.dump(res, open(a.out, "w"), indent=1)
