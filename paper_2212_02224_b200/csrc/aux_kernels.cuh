@@ -25,16 +25,47 @@ struct S1Args {
     int* err;
 };
 
+// Shared-memory row stride of the staged KKT blocks (doubles): even, so rows are 16-byte aligned
+// for double2 loads, and an odd number of 16-byte units, so the lanes of a warp -- each reading
+// its own row at the same column -- hit distinct banks (an unpadded stride of 28 makes 8 lanes
+// collide on every load).
+__host__ __device__ __forceinline__ int s1_ld(int nr) {
+    const int ld = (nr + 1) & ~1;
+    return (ld / 2) % 2 ? ld : ld + 2;
+}
+// per-warp staging of the right-hand side / solution vector (broadcast reads in the mat-vecs)
+constexpr int S1_VEC = 32;
+
 __device__ __forceinline__ void stage1_load(const S1Args& a, double* kinv, double* kkt, double* qm) {
-    const int nn = a.nr * a.nr;
-    for (int i = threadIdx.x; i < nn; i += blockDim.x) { kinv[i] = a.kinv[i]; kkt[i] = a.kkt[i]; }
+    const int nn = a.nr * a.nr, ld = s1_ld(a.nr);
+    for (int i = threadIdx.x; i < a.nr * ld; i += blockDim.x) {
+        const int r = i / ld, c = i - r * ld;
+        kinv[i] = c < a.nr ? a.kinv[r * a.nr + c] : 0.0;
+        kkt[i] = c < a.nr ? a.kkt[r * a.nr + c] : 0.0;
+    }
+    (void)nn;
     if (!a.rhs_in)
         for (int i = threadIdx.x; i < NC * a.m_seg; i += blockDim.x) { qm[i] = a.qmx[i]; qm[NC * a.m_seg + i] = a.qmy[i]; }
 }
 
 // One sample per warp; pr points at its behaviour vector (global or shared memory).
+// Row i of M (staged with stride ld) times the warp's vector v, summed in column order.
+__device__ __forceinline__ double s1_rowdot(const double* M, const double* v, int i, int nr, int ld) {
+    const double2* m2 = reinterpret_cast<const double2*>(M + (size_t)i * ld);
+    const double2* v2 = reinterpret_cast<const double2*>(v);
+    double s = 0.0;
+    int j = 0;
+    for (; j + 1 < nr; j += 2) {
+        const double2 m = m2[j >> 1], x = v2[j >> 1];
+        s = fma(m.x, x.x, s);
+        s = fma(m.y, x.y, s);
+    }
+    if (j < nr) s = fma(M[(size_t)i * ld + j], v[j], s);
+    return s;
+}
+
 __device__ __forceinline__ void stage1_body(const S1Args& a, int row, const double* pr, const double* kinv,
-                                            const double* kkt, const double* qm) {
+                                            const double* kkt, const double* qm, double* vec) {
     const int lane = threadIdx.x & 31;
     const int i = lane;
     double rhs = 0.0;
@@ -57,16 +88,15 @@ __device__ __forceinline__ void stage1_body(const S1Args& a, int row, const doub
         else rhs = a.bscene[(size_t)scene * a.neq + e];
     }
     }
-    double sol = 0.0;
-    for (int j = 0; j < a.nr; ++j) {
-        const double rj = __shfl_sync(0xffffffffu, rhs, j);
-        if (i < a.nr) sol = fma(kinv[i * a.nr + j], rj, sol);
-    }
-    double res = 0.0;
-    for (int j = 0; j < a.nr; ++j) {
-        const double sj = __shfl_sync(0xffffffffu, sol, j);
-        if (i < a.nr) res = fma(kkt[i * a.nr + j], sj, res);
-    }
+    const int ld = s1_ld(a.nr);
+    if (i < a.nr) vec[i] = rhs;
+    __syncwarp();
+    const double sol = i < a.nr ? s1_rowdot(kinv, vec, i, a.nr, ld) : 0.0;
+    __syncwarp();
+    if (i < a.nr) vec[i] = sol;
+    __syncwarp();
+    double res = i < a.nr ? s1_rowdot(kkt, vec, i, a.nr, ld) : 0.0;
+    __syncwarp();
     res = fabs(res - rhs);
     double scale = fabs(rhs);
     for (int o = 16; o >= 1; o >>= 1) {
@@ -92,13 +122,15 @@ __device__ __forceinline__ void stage1_body(const S1Args& a, int row, const doub
 __global__ void __launch_bounds__(256) stage1_kernel(const S1Args a) {
     extern __shared__ __align__(16) unsigned char smem[];
     double* kinv = reinterpret_cast<double*>(smem);
-    double* kkt = kinv + a.nr * a.nr;
-    double* qm = kkt + a.nr * a.nr;                       // qmx | qmy
+    double* kkt = kinv + a.nr * s1_ld(a.nr);
+    double* qm = kkt + a.nr * s1_ld(a.nr);                       // qmx | qmy
+    double* vw = qm + 2 * NC * a.m_seg;                          // per-warp vectors
     stage1_load(a, kinv, kkt, qm);
     __syncthreads();
     const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (row >= a.total) return;
-    stage1_body(a, row, a.rhs_in ? nullptr : a.params + (size_t)row * a.dim, kinv, kkt, qm);
+    stage1_body(a, row, a.rhs_in ? nullptr : a.params + (size_t)row * a.dim, kinv, kkt, qm,
+                vw + (threadIdx.x >> 5) * S1_VEC);
 }
 
 // K4 + K1 fused for the CEM cycle: p = mean + z L^T (pkg/bilevel.py:51-57; z from the caller
@@ -108,9 +140,10 @@ __global__ void __launch_bounds__(256) sample_stage1_kernel(CemState cs, int it,
                                                            const S1Args a) {
     extern __shared__ __align__(16) unsigned char smem[];
     double* kinv = reinterpret_cast<double*>(smem);
-    double* kkt = kinv + a.nr * a.nr;
-    double* qm = kkt + a.nr * a.nr;
+    double* kkt = kinv + a.nr * s1_ld(a.nr);
+    double* qm = kkt + a.nr * s1_ld(a.nr);
     double* pw = qm + 2 * NC * a.m_seg;                  // one behaviour vector per warp
+    double* vw = pw + (blockDim.x >> 5) * MAX_DIM;       // per-warp mat-vec vectors
     stage1_load(a, kinv, kkt, qm);
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -127,7 +160,7 @@ __global__ void __launch_bounds__(256) sample_stage1_kernel(CemState cs, int it,
         if (z != nullptr) {
             for (int q = 0; q < d; ++q) zz[q] = z[(size_t)row * d + q];
         } else {
-            philox_normals(seed, scene + scene_offset, it, j, zz, d);
+            philox_normals_warp(seed, scene + scene_offset, it, j, zz, d, lane);
         }
         if (lane < d) {
             const double* L = cs.L + scene * d * d;
@@ -138,7 +171,7 @@ __global__ void __launch_bounds__(256) sample_stage1_kernel(CemState cs, int it,
     }
     __syncwarp();
     if (lane < d) params[(size_t)row * d + lane] = pr[lane];
-    stage1_body(a, row, pr, kinv, kkt, qm);
+    stage1_body(a, row, pr, kinv, kkt, qm, vw + wid * S1_VEC);
 }
 
 // SamplingDistribution.sample (pkg/bilevel.py:51-57) for one distribution: the factor is

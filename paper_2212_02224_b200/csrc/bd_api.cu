@@ -508,7 +508,7 @@ int run_stage1(bd_ctx* ctx, int B, const double* params, double* xi_bar, double*
     s.kinv = ctx->kinv1.as<double>(); s.params = params; s.bscene = ctx->bscene.as<double>();
     s.xi_bar = xi_bar; s.mu = mu; s.b_out = b_out; s.err = ctx->w_err.as<int>();
     const int warps = 8;
-    const size_t smem = (size_t)(2 * s.nr * s.nr + 2 * NC * s.m_seg) * 8;
+    const size_t smem = (size_t)(2 * s.nr * s1_ld(s.nr) + 2 * NC * s.m_seg + warps * S1_VEC) * 8;
     raise_smem(stage1_kernel, smem);
     stage1_kernel<<<(s.total + warps - 1) / warps, warps * 32, smem, ctx->stream>>>(s);
     ctx->launches++;
@@ -1173,7 +1173,7 @@ int bd_kkt_solve(bd_ctx* ctx, int nvar, int neq, const double* kkt, const double
     S1Args s{};
     s.total = count; s.B = count; s.nr = nr; s.nvar = nvar; s.neq = neq;
     s.kkt = dk; s.kinv = dki; s.rhs_in = dr; s.sol_out = ds; s.err = ctx->w_err.as<int>();
-    const size_t smem = (size_t)(2 * nr * nr) * 8;
+    const size_t smem = (size_t)(2 * nr * s1_ld(nr) + 8 * S1_VEC) * 8;
     raise_smem(stage1_kernel, smem);
     stage1_kernel<<<(count + 7) / 8, 256, smem, ctx->stream>>>(s);
     ctx->launches++;
@@ -1327,7 +1327,7 @@ int bd_cem_cycle(bd_ctx* ctx, int S, const bd_cem_config* cfg, const double* ini
     s1.qmx = ctx->qmx.as<double>(); s1.qmy = ctx->qmy.as<double>(); s1.kkt = ctx->kkt1.as<double>();
     s1.kinv = ctx->kinv1.as<double>(); s1.params = ctx->w_params.as<double>(); s1.bscene = ctx->bscene.as<double>();
     s1.xi_bar = ctx->w_xibar.as<double>(); s1.mu = nullptr; s1.b_out = db; s1.err = ctx->w_err.as<int>();
-    const size_t s1smem = (size_t)(2 * s1.nr * s1.nr + 2 * NC * s1.m_seg + 8 * MAX_DIM) * 8;
+    const size_t s1smem = (size_t)(2 * s1.nr * s1_ld(s1.nr) + 2 * NC * s1.m_seg + 8 * MAX_DIM + 8 * S1_VEC) * 8;
     raise_smem(sample_stage1_kernel, s1smem);
     for (int it = it0; it < it1; ++it) {
         const double* zi = dz ? dz + (size_t)(it - it0) * tot * dim : nullptr;

@@ -98,6 +98,27 @@ __device__ void philox_normals(uint64_t seed, uint32_t scene, uint32_t it, uint3
     }
 }
 
+// Warp-cooperative form for one sample per warp: lane l draws Box-Muller pair l (the same
+// counter block and arithmetic as philox_normals, so bit-identical values) and the d normals are
+// broadcast to every lane.  Must be called by all 32 lanes.
+__device__ void philox_normals_warp(uint64_t seed, uint32_t scene, uint32_t it, uint32_t sample, double* z, int d,
+                                    int lane) {
+    double a = 0.0, b = 0.0;
+    if (lane < (d + 1) / 2) {
+        uint32_t c[4] = {sample, it, scene, (uint32_t)(lane / 2)};
+        philox4(c, seed);
+        const int q = (2 * lane) & 3;
+        const double u1 = ((double)c[q] + 0.5) * 2.3283064365386963e-10;
+        const double u2 = ((double)c[q + 1] + 0.5) * 2.3283064365386963e-10;
+        const double r = sqrt(-2.0 * log(u1));
+        double sn, co;
+        sincospi(2.0 * u2, &sn, &co);
+        a = r * co;
+        b = r * sn;
+    }
+    for (int k = 0; k < d; ++k) z[k] = __shfl_sync(0xffffffffu, (k & 1) ? b : a, k >> 1);
+}
+
 // ---------------------------------------------------------------- CEM state
 struct CemState {
     int S, B, dim, n_cons, n_elite, iters;
