@@ -35,7 +35,7 @@ struct AmArgs {
     double rho;
     int sorted;                 // 1: scene tiles hold each timestep's obstacles sorted by -x/a (float2)
     const float* wrow;          // m x WROW        [W | Wd | Wdd] rows, fp32
-    const double* kblk;         // 2 x NC x KROW   per-axis aug-KKT inverse blocks
+    const double* kblk;         // NX x KSTR       aug-KKT inverse rows by value index (2 kk + axis)
     const double* kb;           // NX x neq        xi-b block of the aug-KKT inverse
     const double* aeq;          // neq x NX
     const float4* obs;          // S x m x n_obs/2 pairs (-x0/a, -x1/a, -y0/b, -y1/b), n_obs padded to even
@@ -97,7 +97,7 @@ struct AmSmem {
         size_t o = 0;
         w = o;    o = align_up(o + (size_t)m * WROW * 4, 16);
         obs = o;  o = align_up(o + (size_t)n_obs * m * 8, 16);          // n_obs already padded to even
-        k = o;    o = align_up(o + (size_t)2 * NC * KROW * 8, 16);
+        k = o;    o = align_up(o + (size_t)NX * KSTR * 8, 16);
         kb = o;   o = align_up(o + (size_t)NX * neq * 8, 16);
         a = o;    o = align_up(o + (size_t)neq * NX * 8, 16);
         curv = o; o = align_up(o + (size_t)2 * n_curv * 4, 16);
@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(256, BD_AM_MINB) am_kernel(const AmArgs a) {
         if (o_bytes) bulk_load(osm, reinterpret_cast<const float4*>(a.obs) + (size_t)scene * (n_obs / 2) * m, o_bytes,
                                &stage_bar);
     }
-    for (int i = threadIdx.x; i < 2 * NC * KROW; i += threads) ksm[i] = a.kblk[i];
+    for (int i = threadIdx.x; i < NX * KSTR; i += threads) ksm[i] = a.kblk[i];
     for (int i = threadIdx.x; i < NX * neq; i += threads) { kbsm[i] = a.kb[i]; asm_[i] = a.aeq[i]; }
     if (CURV)
         for (int i = threadIdx.x; i < 2 * a.n_curv; i += threads) csm[i] = a.curv[(size_t)scene * 2 * a.n_curv + i];
@@ -497,7 +497,7 @@ __global__ void __launch_bounds__(256, BD_AM_MINB) am_kernel(const AmArgs a) {
             const int i = own + RP * r;
             if (i < NX) {
                 const int ax = i & 1, kk = i >> 1;
-                const double2* kr = reinterpret_cast<const double2*>(ksm + (ax * NC + kk) * KROW);
+                const double2* kr = reinterpret_cast<const double2*>(ksm + i * KSTR);
                 const double2* ur = reinterpret_cast<const double2*>(su + ax * KROW);
                 double s0 = first ? dl[ax * NC + kk] : 0.0, s1 = 0.0;
 #pragma unroll

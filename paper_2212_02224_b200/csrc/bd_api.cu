@@ -714,10 +714,10 @@ int bd_set_projection(bd_ctx* ctx, int n_obs, double rho, int neq, const double*
         for (int j = NC; j < NX; ++j)
             if (kinv[i * nr + j] != 0.0 || kinv[j * nr + i] != 0.0)
                 return fail(ctx, BD_ERR_STRUCTURE, "augmented KKT inverse couples the x and y blocks");
-    std::vector<double> kb((size_t)2 * NC * KROW, 0.0), kbx((size_t)NX * neq), ae((size_t)neq * NX);
+    std::vector<double> kb((size_t)NX * KSTR, 0.0), kbx((size_t)NX * neq), ae((size_t)neq * NX);
     for (int ax = 0; ax < 2; ++ax)
         for (int i = 0; i < NC; ++i)
-            for (int j = 0; j < NC; ++j) kb[(ax * NC + i) * KROW + j] = kinv[(ax * NC + i) * nr + ax * NC + j];
+            for (int j = 0; j < NC; ++j) kb[(2 * i + ax) * KSTR + j] = kinv[(ax * NC + i) * nr + ax * NC + j];
     for (int i = 0; i < NX; ++i)
         for (int e = 0; e < neq; ++e) kbx[i * neq + e] = kinv[i * nr + NX + e];
     memcpy(ae.data(), a_eq, ae.size() * 8);

@@ -23,7 +23,10 @@ namespace bd {
 constexpr int NC = 11;             // coefficients per axis: Bernstein order 10 (pkg/basis.py:156-179)
 constexpr int NX = 2 * NC;         // stacked xi = (c_x, c_y)
 constexpr int WROW = 36;           // one timestep of [W | Wd | Wdd] in fp32, padded to 9 x float4
-constexpr int KROW = 12;           // fp64 row stride of the per-axis aug-KKT inverse blocks (6 x double2)
+constexpr int KROW = 12;           // fp64 row stride of the per-axis u vectors in the AM scratch (6 x double2)
+constexpr int KSTR = 14;           // fp64 row stride of the aug-KKT inverse rows in shared memory: rows are
+                                   // stored by value index (2 kk + axis), the 8 consecutive rows a lane
+                                   // group reads sit 7 x 16 B apart -> conflict-free LDS.128
 constexpr int MAX_NEQ = 9;         // 6 initial-state rows (+3 goal rows), pkg/batch_qp.py:181-193
 constexpr int MAX_DIM = 16;        // behaviour vector length (2*m_seg [+2])
 constexpr int ITMAX_SLOTS = 32;    // spread slots for the per-iteration batch max (early exit)
