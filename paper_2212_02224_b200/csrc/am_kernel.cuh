@@ -219,9 +219,12 @@ __device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float
         const float iv = dv2 > 0.f ? rsqrtf(dv2) : 0.f;
         const float ia = da2 > 0.f ? rsqrtf(da2) : 0.f;
         const float dv = dv2 * iv, da = da2 * ia;
-        const float cv = dv2 > 0.f ? XD * iv : 1.f, sv = YD * iv;     // atan2(0,0) = 0
-        const float ca = da2 > 0.f ? XDD * ia : 1.f, sa = YDD * ia;
-        const float gap = fabsf(sa * cv - ca * sv);                   // |sin(alpha_a - alpha_v)|
+        // |sin(alpha_a - alpha_v)| = |a x v| / (|a| |v|); a zero vector has angle 0 (atan2(0, 0)),
+        // i.e. unit vector (1, 0): |sin| = |y| / |.| of the other vector.  The cross product is
+        // shared with the curvature residual below.
+        const float cross = fabsf(fmaf(YDD, XD, -XDD * YD));
+        const float gap = dv2 > 0.f ? (da2 > 0.f ? cross * iv * ia : fabsf(YD) * iv) : fabsf(YDD) * ia;
+        const float cv = dv2 > 0.f ? XD * iv : 1.f;                   // cos(alpha_v), curvature bound only
         // coupled clip window (pkg/projection.py:138-169)
         const int di = j * dstride;
         BD_CHECK(j < (m + P - 1) / P && t < m);
@@ -332,7 +335,7 @@ __device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float
             r += fmaxf(dv - L.v_max, 0.f) + fmaxf(L.v_min - dv, 0.f);
             r += fmaxf(da - L.a_max, 0.f);
             const float sp = fmaxf(dv, 1e-6f);
-            r += fmaxf(__fdividef(fabsf(YDD * XD - XDD * YD), sp * sp * sp) - L.k_max, 0.f);
+            r += fmaxf(__fdividef(cross, sp * sp * sp) - L.k_max, 0.f);
             if (CURV) r += fmaxf(XD * XD * kcur - L.c_max, 0.f);
             v[NX] += r;
             const float e = dv - L.v_max;
