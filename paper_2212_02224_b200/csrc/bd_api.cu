@@ -748,6 +748,20 @@ static int finish_tile(bd_ctx* ctx, int S, int m, int nop) {
     return 0;
 }
 
+// Stable residual order of every scene (rank_count_kernel / its shared-memory form).
+static void launch_rank_count(bd_ctx* ctx, const double* resid, const int* err, int S, int B, int* order) {
+    if (B <= RANK_SMEM_MAX) {
+        const size_t smem = (size_t)B * 8;
+        raise_smem(rank_count_smem_kernel, smem);
+        rank_count_smem_kernel<<<dim3((unsigned)((B + 31) / 32), (unsigned)S), 256, smem, ctx->stream>>>(resid, err, B,
+                                                                                                      order);
+    } else {
+        const size_t tot = (size_t)S * B;
+        rank_count_kernel<<<(unsigned)((tot + 7) / 8), 256, 0, ctx->stream>>>(resid, err, S, B, order);
+    }
+    ctx->launches++;
+}
+
 static int upload_curvature(bd_ctx* ctx, int S, int n_curv, const double* cx, const double* ck) {
     if (n_curv > 0) {
         std::vector<float> cf((size_t)S * 2 * n_curv);
@@ -1248,8 +1262,7 @@ int bd_rank_refit(bd_ctx* ctx, int S, int B, int dim, const double* resid, const
     s.best_index = ctx->c_best_idx.as<long long>(); s.best_params = ctx->c_best_p.as<double>();
     s.best_xi = ctx->c_best_xi.as<double>(); s.best_scal = ctx->c_best_s.as<double>();
     CU(ctx->w_order.ensure(tot * 4));
-    rank_count_kernel<<<(unsigned)((tot + 7) / 8), 256, 0, ctx->stream>>>(dr, nullptr, S, B, ctx->w_order.as<int>());
-    ctx->launches++;
+    launch_rank_count(ctx, dr, nullptr, S, B, ctx->w_order.as<int>());
     const size_t smem = rank_refit_smem(n_cons, n_elite, dim);
     raise_smem(rank_refit_kernel, smem);
     rank_refit_kernel<<<S, RANK_REFIT_THREADS, smem, ctx->stream>>>(s, 0, ctx->w_order.as<int>());
@@ -1338,10 +1351,9 @@ int bd_cem_cycle(bd_ctx* ctx, int S, const bd_cem_config* cfg, const double* ini
                                  ctx->w_xi.as<double>(), ctx->w_res.as<double>(), ctx->w_cost.as<double>(), nullptr,
                                  ctx->w_iters.as<int>(), ctx->w_conf.as<unsigned long long>())))
             return rc;
-        rank_count_kernel<<<(unsigned)((tot + 7) / 8), 256, 0, ctx->stream>>>(s.resid, s.err, S, B,
-                                                                             ctx->w_order.as<int>());
+        launch_rank_count(ctx, s.resid, s.err, S, B, ctx->w_order.as<int>());
         rank_refit_kernel<<<S, RANK_REFIT_THREADS, rsmem, ctx->stream>>>(s, it, ctx->w_order.as<int>());
-        ctx->launches += 2;
+        ctx->launches++;
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(ctx, BD_ERR_CUDA, "CEM launch: %s", cudaGetErrorString(e));

@@ -226,6 +226,34 @@ __global__ void __launch_bounds__(256) rank_count_kernel(const double* resid, co
     if (lane == 0) order[(size_t)scene * B + cnt] = i;
 }
 
+// Same ranking with the scene's keys staged once per CTA in shared memory (B <= RANK_SMEM_MAX):
+// grid (ceil(B / 32), S), 8 warps x 4 samples per CTA.  Cuts the L2 traffic of the per-warp
+// scans from B doubles per sample to B keys per 32 samples.
+constexpr int RANK_SMEM_MAX = 12288;
+__global__ void __launch_bounds__(256) rank_count_smem_kernel(const double* resid, const int* err, int B, int* order) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem);
+    const int scene = blockIdx.y;
+    if (err && err[scene]) return;
+    const double* r = resid + (size_t)scene * B;
+    for (int j = threadIdx.x; j < B; j += blockDim.x) keys[j] = ordered_bits(__ldg(r + j));
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int q = 0; q < 4; ++q) {
+        const int i = blockIdx.x * 32 + warp * 4 + q;
+        if (i >= B) break;
+        const unsigned long long ki = keys[i];
+        int cnt = 0;
+        for (int j = lane; j < B; j += 32) {
+            const unsigned long long kj = keys[j];
+            cnt += (kj < ki) || (kj == ki && j < i);
+        }
+        for (int o = 16; o >= 1; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        BD_CHECK(cnt >= 0 && cnt < B);
+        if (lane == 0) order[(size_t)scene * B + cnt] = i;
+    }
+}
+
 // Dynamic shared memory of rank_refit_kernel (bytes).
 __host__ __device__ inline size_t rank_refit_smem(int n_cons, int n_elite, int dim) {
     const int staged = n_elite <= 128 ? n_elite : 0;
