@@ -2,11 +2,12 @@
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--scenes-per-gpu S]
 
-Workload (BASELINE.json configs[1] run as a fleet, config 5 style): every step is one full
-CEM planning cycle -- B=1000 set-point samples, 10 obstacles, 4 CEM iterations, top-150
-constraint elites / top-100 elites, 100 AM iterations, m=100 timesteps over 5 s, order-10
-Bernstein basis -- for each of S synthetic highway scenes per GPU (independent scenes are
-sharded over ranks, no collective on the data path: weak scaling).  value = S*N * 4 * 1000
+Workload (BASELINE.json config 5: 4096 scenes sharded over 8 GPUs, i.e. S = 512 scenes per GPU,
+each a config-2 planning cycle): every step is one full CEM planning cycle -- B=1000 set-point
+samples, 10 obstacles, 4 CEM iterations, top-150 constraint elites / top-100 elites, 100 AM
+iterations, m=100 timesteps over 5 s, order-10 Bernstein basis -- for each of S synthetic
+highway scenes per GPU (independent scenes are sharded over ranks, no collective on the data
+path: weak scaling).  value = S*N * 4 * 1000
 trajectories / max-over-ranks device time.  The single-scene config-2 cycle latency
 (p50/p99, host call -> host-visible best xi) is measured through the public solve_bilevel.
 
@@ -398,7 +399,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--scenes-per-gpu", type=int, default=64)
+    ap.add_argument("--scenes-per-gpu", type=int, default=512)     # BASELINE config 5: 4096 scenes / 8 GPUs
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
