@@ -66,7 +66,9 @@ struct AmArgs {
     size_t p2p_res_off, p2p_cost_off;
 };
 
-// out of line: run by one CTA per scene, kept away from the main loop's register allocation
+// Batch-global early exit (pkg/projection.py:329): the first iteration whose batch maximum
+// residual is <= tol sets iterations_used and, if that is before max_iters, the replay count.
+// Out of line: run by one CTA per scene, kept away from the main loop's register allocation.
 __device__ __noinline__ void exit_scan_block(const unsigned* base, int max_iters, double tol, int scene,
                                                 int* iters_used, int* replay, unsigned long long* conflicts) {
     __shared__ int red[32];
@@ -589,17 +591,6 @@ __global__ void __launch_bounds__(256, BD_AM_MINB) am_kernel(const AmArgs a) {
             if (threadIdx.x == 0) a.done_ctr[scene] = 0u;
         }
     }
-}
-
-// Batch-global early exit (pkg/projection.py:329): first iteration whose batch max
-// residual is <= tol.  Sets iterations_used and, if that is before max_iters, the
-// replay count (the replay re-runs the deterministic kernel for exactly that many
-// iterations) and clears the scene's conflict counter for the replay.
-__global__ void exit_scan_kernel(const unsigned* itmax, int max_iters, double tol, int* iters_used, int* replay,
-                                 unsigned long long* conflicts) {
-    const int scene = blockIdx.x;
-    exit_scan_block(itmax + (size_t)scene * max_iters * ITMAX_SLOTS, max_iters, tol, scene, iters_used, replay,
-                    conflicts);
 }
 
 // Dense scenes: rewrite each (scene, timestep) row of the pair tile [(-x0,-x1,-y0,-y1) per pair]

@@ -163,34 +163,6 @@ __global__ void cem_init_kernel(CemState s, const double* mean0, const double* c
     }
 }
 
-// p = mean + z L^T (pkg/bilevel.py:51-57) or the warm-start tile (pkg/behavior.py:113-115).
-__global__ void sample_kernel(CemState s, int it, const double* z, const double* warm, uint64_t seed,
-                              int scene_offset, double* params) {
-    const int id = blockIdx.x * blockDim.x + threadIdx.x;
-    if (id >= s.S * s.B) return;
-    const int scene = id / s.B, j = id % s.B;
-    const int d = s.dim;
-    if (s.err[scene]) return;
-    double* out = params + (size_t)id * d;
-    if (warm != nullptr) {
-        for (int q = 0; q < d; ++q) out[q] = warm[(size_t)id * d + q];
-        return;
-    }
-    double zz[MAX_DIM];
-    if (z != nullptr) {
-        for (int q = 0; q < d; ++q) zz[q] = z[(size_t)id * d + q];
-    } else {
-        philox_normals(seed, scene + scene_offset, it, j, zz, d);
-    }
-    const double* L = s.L + scene * d * d;
-    const double* mu = s.mean + scene * d;
-    for (int r = 0; r < d; ++r) {
-        double acc = 0.0;
-        for (int q = 0; q < d; ++q) acc = fma(zz[q], L[r * d + q], acc);
-        out[r] = mu[r] + acc;
-    }
-}
-
 // Block-wide sum of one double per thread (result valid in every thread).
 __device__ __forceinline__ double block_sum(double v, double* red) {
     for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
