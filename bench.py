@@ -253,7 +253,7 @@ def dense_config4(device: int, steps: int = 3):
             "config": "1 scene, B=10000, 50 obstacles, 4 CEM iterations, 100 AM iterations (1 GPU)"}
 
 
-def closed_loop_suite(device: int, episodes: int = 64, length: int = 150):
+def closed_loop_suite(device: int, episodes: int = 256, length: int = 150):
     """a fleet of closed-loop episodes (run_episode semantics, replan every 5 ticks)
     with the reference planner's default configuration (PlannerEnvConfig: B=250, N=5, m=50 over 10 s,
     6 obstacles, 50 AM iterations): device scene build -> CEM -> controls -> simulator, one batched
