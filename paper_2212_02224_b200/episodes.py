@@ -43,6 +43,8 @@ class EpisodeLog:
     failure_reason: str = ""
 
     def ego_speeds(self) -> np.ndarray:
+        if isinstance(self.steps, _StepRecords):
+            return self.steps.ego_speeds()
         return np.array([rec["ego"][3] for rec in self.steps])
 
     def mean_speed(self) -> float:
@@ -85,6 +87,59 @@ class EpisodeLog:
         return log
 
 
+class _StepRecords(list):
+    """EpisodeLog.steps filled lazily: the device snapshot blocks are kept as arrays and turned into
+    the reference's per-step dicts on first read (suite metrics only need the ego speeds, which
+    come straight from the arrays)."""
+
+    def __init__(self, nv: int):
+        super().__init__()
+        self._nv = nv
+        self._blocks = []
+
+    def _add_block(self, block: np.ndarray) -> None:
+        if self._blocks is None:
+            super().extend(_snapshots(block, self._nv))
+        else:
+            self._blocks.append(block)
+
+    def _fill(self) -> None:
+        if self._blocks is not None:
+            blocks, self._blocks = self._blocks, None
+            for b in blocks:
+                super().extend(_snapshots(b, self._nv))
+
+    def ego_speeds(self) -> np.ndarray:
+        if self._blocks is not None:
+            return np.concatenate([b[:, 4] for b in self._blocks]) if self._blocks else np.zeros(0)
+        return np.array([rec["ego"][3] for rec in self])
+
+    def __len__(self):
+        return sum(b.shape[0] for b in self._blocks) if self._blocks is not None else super().__len__()
+
+    def __bool__(self):
+        return len(self) > 0
+
+
+def _materialising(name):
+    base = getattr(list, name)
+
+    def method(self, *a, **kw):
+        self._fill()
+        for x in a:                    # list's C fast paths read another list's storage directly
+            if isinstance(x, _StepRecords):
+                x._fill()
+        return base(self, *a, **kw)
+    method.__name__ = name
+    return method
+
+
+for _name in ("__iter__", "__getitem__", "__eq__", "__ne__", "__lt__", "__le__", "__gt__", "__ge__", "__contains__",
+              "__reversed__", "__repr__", "append", "extend", "insert", "pop", "remove", "index", "count", "copy",
+              "__add__", "__iadd__", "__mul__", "__setitem__", "__delitem__", "sort", "reverse", "clear"):
+    setattr(_StepRecords, _name, _materialising(_name))
+
+
 def _snapshots(block: np.ndarray, nv: int) -> list:
     """run_episode step records (pkg/highway.py:478-485) from a block of device snapshot rows
     (one C-level tolist() per block, then plain list slicing)."""
@@ -116,8 +171,8 @@ def run_episodes(scenarios, planner, replan_stride: int = 5, road_end_margin: fl
     st = host.to(device) if device is not None else host
     sim = Simulator(planner.context, TrafficParams(dt=dt, wheelbase=planner.env.wheelbase))
     planner.reset()
-    logs = [EpisodeLog(meta={"scenario": sc.to_dict(), "planner": planner.name, "replan_stride": replan_stride})
-            for sc in scenarios]
+    logs = [EpisodeLog(meta={"scenario": sc.to_dict(), "planner": planner.name, "replan_stride": replan_stride},
+                       steps=_StepRecords(int(n_veh[s]))) for s, sc in enumerate(scenarios)]
     lengths = np.array([sc.episode_length for sc in scenarios])
     x_end = np.array([sc.road.length - road_end_margin for sc in scenarios], dtype=np.float64)
     active = (lengths > 0).astype(np.int32)
@@ -143,7 +198,8 @@ def run_episodes(scenarios, planner, replan_stride: int = 5, road_end_margin: fl
         done, snap = sim.run(st, ctrl, n, ctrl_offset=offset, x_end=x_end, active=active, snapshots=record_steps)
         if record_steps:
             for s in np.flatnonzero(was):
-                logs[s].steps.extend(_snapshots(snap[s, :int(done[s])], int(n_veh[s])))
+                if done[s]:
+                    logs[s].steps._add_block(snap[s, :int(done[s])].copy())
         k += n
         offset += n
         active[(lengths <= k) & (active != 0)] = 0
