@@ -373,12 +373,16 @@ int dispatch_am(bd_ctx* ctx, AmArgs a, int P, int threads, bool replay_pass, int
     a.s_cta = threads / P;
     const bool curv = a.n_curv > 0;
     const int dflt = P == 32 ? 64 : 128;
-    // compile-time shapes of the BASELINE configs (m = 100; 10 or 50 obstacles), default CTA size
+    // compile-time shapes of the BASELINE configs (m = 100; 10 or 50 obstacles) and of the
+    // reference planner's defaults (PlannerEnvConfig: m = 50, 6 obstacles), default CTA size
     const bool fixed = !curv && a.m == 100 && threads == dflt;
+    const bool fixed50 = !curv && a.m == 50 && a.n_obs == 6 && threads == dflt;
 #define AM_CASE(PP)                                                                                          \
     case PP:                                                                                                 \
         if (fixed && a.n_obs == 10)                                                                          \
             return launch_am_t<PP, false, 100, 5, (PP == 32 ? 64 : 128)>(ctx, a, threads, replay_pass, occ);  \
+        if (fixed50)                                                                                         \
+            return launch_am_t<PP, false, 50, 3, (PP == 32 ? 64 : 128)>(ctx, a, threads, replay_pass, occ);   \
         if (fixed && a.n_obs == 50)                                                                          \
             return launch_am_t<PP, false, 100, 25, (PP == 32 ? 64 : 128)>(ctx, a, threads, replay_pass, occ); \
         return curv ? launch_am_t<PP, true>(ctx, a, threads, replay_pass, occ)                               \
