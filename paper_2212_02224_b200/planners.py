@@ -137,15 +137,23 @@ class _BatchPlanner:
         return [np.arange(int(n)) * w for n, w in road]
 
     def _initial(self, b0, centers):
-        """BasePlanner.initial_distribution (pkg/planners.py:218-231) per world."""
+        """BasePlanner.initial_distribution (pkg/planners.py:218-231) for all worlds at once: the
+        lane centre nearest to y0 (first on ties, like argmin) and the speed hypot(xdot0, ydot0)."""
         env, ms = self.env, self.env.m_seg
         S = b0.shape[0]
+        width = max((c.size for c in centers), default=0)
+        if width == 0:
+            lane_y = b0[:, 1].copy()
+        else:
+            tab = np.full((S, width), np.inf)
+            for s, c in enumerate(centers):
+                tab[s, :c.size] = c
+            pick = tab[np.arange(S), np.argmin(np.abs(tab - b0[:, 1:2]), axis=1)]
+            empty = np.array([c.size == 0 for c in centers])
+            lane_y = np.where(empty, b0[:, 1], pick)
         mean = np.empty((S, 2 * ms))
-        for s in range(S):
-            y0, c = b0[s, 1], centers[s]
-            lane_y = float(c[np.argmin(np.abs(c - y0))]) if c.size else y0
-            speed = float(np.hypot(b0[s, 2], b0[s, 3]))
-            mean[s] = np.concatenate([np.full(ms, lane_y), np.full(ms, speed)])
+        mean[:, :ms] = lane_y[:, None]
+        mean[:, ms:] = np.hypot(b0[:, 2], b0[:, 3])[:, None]
         cov = np.diag(np.concatenate([np.full(ms, env.sigma_offset ** 2), np.full(ms, env.sigma_speed ** 2)]))
         return mean, cov
 
