@@ -534,13 +534,44 @@ def gen_planners():
     print("planners written")
 
 
+def gen_harness():
+    """The harness callers of the path (pkg/bench.py:208-367): canonical_scene, bilevel_config_for,
+    an emit_convergence_trace run, and replay_to_csv of the episode logs in episodes.npz."""
+    import tempfile
+    from bilevel_drive import bench as rbench
+    out = {}
+    env = PlannerEnvConfig(batch_size=200, iterations=4)
+    sc = rbench.canonical_scene(env)
+    cfg = rbench.bilevel_config_for(env, sc, batch_size=300, iterations=2)
+    out.update(canon_ox=sc.spec.obstacles_x, canon_oy=sc.spec.obstacles_y, canon_b0=sc.initial_state,
+               canon_lanes=sc.lane_centers, canon_limits=np.array([sc.spec.ellipse_a, sc.spec.ellipse_b, sc.spec.v_min,
+                                                                   sc.spec.v_max, sc.spec.a_max, sc.spec.kappa_max,
+                                                                   sc.spec.c_max, sc.spec.y_lb, sc.spec.y_ub]),
+               cfg_mean=cfg.init_mean, cfg_cov=cfg.init_cov,
+               cfg_sizes=np.array([cfg.batch_size, cfg.constraint_elites, cfg.elites, cfg.iterations]))
+    trace = rbench.emit_convergence_trace(env, seed=3)
+    out["trace_jsonl"] = np.array("".join(json.dumps(r, sort_keys=True) + "\n" for r in trace))
+    eps = np.load(os.path.join(OUT, "episodes.npz"))
+    with tempfile.TemporaryDirectory() as d:
+        for k in range(int(eps["n_cases"])):
+            log_path, csv_path = os.path.join(d, f"e{k}.jsonl"), os.path.join(d, f"e{k}.csv")
+            with open(log_path, "w") as fh:
+                fh.write(str(eps[f"e{k}_jsonl"]))
+            rbench.replay_to_csv(log_path, csv_path)
+            out[f"replay_{k}"] = np.array(open(csv_path).read())
+    out["n_replays"] = int(eps["n_cases"])
+    np.savez_compressed(os.path.join(OUT, "harness.npz"), **out)
+    print(f"harness written ({len(trace)} trace records)")
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", nargs="*", default=None)
     a = ap.parse_args()
     os.makedirs(OUT, exist_ok=True)
     jobs = {"basis": gen_basis, "lower": gen_lower, "scenes": gen_scenes, "cem_small": gen_cem_small,
-            "cem_c2": gen_cem_c2, "worlds": gen_worlds, "sim": gen_sim, "episodes": gen_episodes, "cem_variants": gen_cem_variants, "planners": gen_planners}
+            "cem_c2": gen_cem_c2, "worlds": gen_worlds, "sim": gen_sim, "episodes": gen_episodes, "cem_variants": gen_cem_variants, "planners": gen_planners,
+            "harness": gen_harness}
     for name, fn in jobs.items():
         if a.only is None or name in a.only:
             fn()
