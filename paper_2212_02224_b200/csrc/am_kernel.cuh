@@ -226,7 +226,11 @@ __device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float
         // i.e. unit vector (1, 0): |sin| = |y| / |.| of the other vector.  The cross product is
         // shared with the curvature residual below.
         const float cross = fabsf(fmaf(YDD, XD, -XDD * YD));
-        const float gap = dv2 > 0.f ? (da2 > 0.f ? cross * iv * ia : fabsf(YD) * iv) : fabsf(YDD) * ia;
+        // written as selects (a nested ternary compiled to a divergent branch): da2 == 0 makes
+        // cross == 0, dv2 == 0 makes iv == 0
+        const float gv = (da2 > 0.f ? cross : fabsf(YD)) * iv;
+        const float gva = gv * ia;
+        const float gap = dv2 > 0.f ? (da2 > 0.f ? gva : gv) : fabsf(YDD) * ia;
         const float cv = dv2 > 0.f ? XD * iv : 1.f;                   // cos(alpha_v), curvature bound only
         // coupled clip window (pkg/projection.py:138-169)
         const int di = j * dstride;
