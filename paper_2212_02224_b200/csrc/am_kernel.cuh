@@ -158,7 +158,7 @@ template <int P, bool CURV, bool INIT, int NV, int MT, int NPT, int TPB>
 __device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float4* __restrict__ osm,
                                       const float* __restrict__ csm, const float2 (&cxy)[NC], float (&v)[NV],
                                       float* dap, float* kap, int dstride_rt, int p, int m_rt, int npair_rt,
-                                      int n_curv, const SceneLim& L, int& conf, bool& ovf, bool sorted_rt,
+                                      int n_curv, const SceneLim& L, int& conf, bool sorted_rt,
                                       bool want_cost = true) {
     // MT / NPT / TPB > 0: timesteps, obstacle pairs and CTA size fixed at compile time (the
     // BASELINE shapes), so the tile addressing folds into immediates and the pair loop unrolls.
@@ -459,13 +459,22 @@ __global__ void __launch_bounds__(256, BD_AM_MINB) am_kernel(const AmArgs a) {
             sc[i] = static_cast<float>(c[r]);
         }
     }
+    // A sample whose iterate leaves the fp32 range of the sweep (Bernstein rows are a partition of
+    // unity, so |X| <= max|c|, |Xd| <= 4 max|c|, |Xdd| <= 15 max|c|; below 1e17 every square stays
+    // < 3e38) is marked out of range (`ovf`, sticky); its later non-finite values are not a batch
+    // failure, and it reports an infinite residual and cost with its stage-1 coefficients: it ranks
+    // after every finite sample, as the reference's huge / NaN residuals do for such set-points.
+    bool ovf = false;
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r)
+        if (own + RP * r < NX) ovf |= !(fabs(c[r]) < 1e17);
     gsync();
     float2 cxy[NC];
 #pragma unroll
     for (int q = 0; q < NC; ++q) cxy[q] = reinterpret_cast<const float2*>(sc)[q];
 
     int conf = 0;
-    bool bad = false, ovf = false;
+    bool bad = false;
     float v[NV];
     float* xbuf = reinterpret_cast<float*>(smem + lay.scr + (size_t)slot * AmSmem::SCR_BYTES + 672);
     auto reduce = [&]() {
@@ -477,7 +486,7 @@ __global__ void __launch_bounds__(256, BD_AM_MINB) am_kernel(const AmArgs a) {
         }
     };
     sweep<P, CURV, true, NV, MT, NPT, TPB>(wsm, osm, csm, cxy, v, dap, kap, threads, p, m, n_obs / 2, a.n_curv, L,
-                                           conf, ovf, a.sorted != 0);
+                                           conf, a.sorted != 0);
     reduce();
 
     const int r_lane = NX % RP, r_slot = (NX / RP) * RP;
@@ -521,10 +530,9 @@ __global__ void __launch_bounds__(256, BD_AM_MINB) am_kernel(const AmArgs a) {
                 }
                 s0 = fma(kr[NC / 2].x, su[ax * KROW + NC - 1], s0);
                 c[r] += s0 + s1;
-                bad |= !isfinite(c[r]);
-                // fp32 range of the sweep: Bernstein rows are a partition of unity, so |X| <= max|c|,
-                // |Xd| <= 4 max|c|, |Xdd| <= 15 max|c| on this basis; 1e17 keeps every square < 3e38
-                ovf |= !(fabs(c[r]) < 1e17);
+                const double ac = fabs(c[r]);
+                bad |= !(ac <= DBL_MAX);                      // NaN / inf (pkg/projection.py:290-291)
+                ovf |= (ac >= 1e17) && (ac <= DBL_MAX);
                 sc[i] = static_cast<float>(c[r]);
             }
         }
@@ -533,7 +541,7 @@ __global__ void __launch_bounds__(256, BD_AM_MINB) am_kernel(const AmArgs a) {
         for (int q = 0; q < NC; ++q) cxy[q] = reinterpret_cast<const float2*>(sc)[q];
         // ---- projections, back-projection, residual at the new iterate
         sweep<P, CURV, false, NV, MT, NPT, TPB>(wsm, osm, csm, cxy, v, dap, kap, threads, p, m, n_obs / 2, a.n_curv,
-                                                L, conf, ovf, a.sorted != 0, it == iters - 1);   // cost: last sweep only
+                                                L, conf, a.sorted != 0, it == iters - 1);   // cost: last sweep only
         reduce();
         resid = v[r_slot];
         cost = v[c_slot];
@@ -542,18 +550,33 @@ __global__ void __launch_bounds__(256, BD_AM_MINB) am_kernel(const AmArgs a) {
         if (a.hist_out && owner && active)
             a.hist_out[((size_t)scene * a.max_iters + it) * a.B + local] = resid;
         if (a.replay == nullptr) {
-            float mx = owner ? resid : 0.f;
+            const float rk = resid != resid ? INFINITY : resid;   // a NaN never passes the exit test
+            float mx = owner ? rk : 0.f;
             if (P < 32) {
 #pragma unroll
                 for (int o = 16; o >= 1; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
                 if (lane == 0) atomicMax(itm + (size_t)it * ITMAX_SLOTS, float_key(mx));
             } else if (owner) {
-                atomicMax(itm + (size_t)it * ITMAX_SLOTS, float_key(resid));
+                atomicMax(itm + (size_t)it * ITMAX_SLOTS, float_key(rk));
             }
         }
     }
 
-    // ---- outputs
+    // ---- outputs (out-of-range samples: stage-1 coefficients, +inf residual and cost)
+    {
+        constexpr unsigned gmask = RP >= 32 ? 0xffffffffu : ((1u << (RP & 31)) - 1u);
+        const bool gov = (__ballot_sync(0xffffffffu, ovf) & (gmask << (lane & ~(RP - 1)))) != 0u;
+        if (gov) {
+            bad = false;
+            resid = INFINITY;
+            cost = INFINITY;
+#pragma unroll
+            for (int r = 0; r < ROWS; ++r) {
+                const int i = own + RP * r;
+                if (i < NX) c[r] = a.xi_bar[row * NX + (i & 1) * NC + (i >> 1)];
+            }
+        }
+    }
     if (active) {
 #pragma unroll
         for (int r = 0; r < ROWS; ++r) {
@@ -568,16 +591,13 @@ __global__ void __launch_bounds__(256, BD_AM_MINB) am_kernel(const AmArgs a) {
     } else {
         conf = 0;
         bad = false;
-        ovf = false;
     }
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) conf += __shfl_xor_sync(0xffffffffu, conf, o);
     const unsigned anybad = __ballot_sync(0xffffffffu, bad);
-    const unsigned anyovf = __ballot_sync(0xffffffffu, ovf);
     if (lane == 0) {
         if (conf) atomicAdd(a.conflicts + scene, (unsigned long long)conf);
         if (anybad) atomicOr(a.err + scene, ERR_NONFINITE);
-        if (anyovf) atomicOr(a.err + scene, ERR_RANGE);
     }
     // ---- batch-global early exit folded into the last CTA of the scene (no extra launch)
     if (a.replay == nullptr && a.done_ctr != nullptr) {

@@ -320,8 +320,6 @@ int finish_call(bd_ctx* ctx, bool check_err, int n_err) {
         if (bits & ERR_KKT_RESID) return fail(ctx, BD_ERR_NUMERICAL, "KKT residual exceeds tolerance");
         if (bits & ERR_NONFINITE) return fail(ctx, BD_ERR_NUMERICAL, "projection iterate is not finite");
         if (bits & ERR_P2P_TIMEOUT) return fail(ctx, BD_ERR_CUDA, "peer exchange timed out (a rank never signalled)");
-        if (bits & ERR_RANGE)
-            return fail(ctx, BD_ERR_NUMERICAL, "projection iterate left the fp32 range of the device sweep (|x| > 1e18 m)");
     }
     return 0;
 }

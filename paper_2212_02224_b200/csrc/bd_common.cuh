@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cfloat>
 #include <cstdio>
 
 // Device-side bounds / invariant checks (build with -DBD_CHECKS=1; tools/build_variant.sh checks
@@ -35,7 +36,6 @@ constexpr int ITMAX_SLOTS = 32;    // spread slots for the per-iteration batch m
 constexpr int ERR_NONFINITE = 1;   // NumericalFailure: non-finite iterate (pkg/projection.py:290-291)
 constexpr int ERR_KKT_RESID = 2;   // NumericalFailure: stage-1 KKT residual (pkg/batch_qp.py:272-279)
 constexpr int ERR_BAD_RHS = 4;     // ValueError: non-finite right-hand side (pkg/batch_qp.py:105-106)
-constexpr int ERR_RANGE = 8;       // NumericalFailure: iterate outside the fp32 range of the device sweep
 constexpr int ERR_P2P_TIMEOUT = 16; // RuntimeError: a peer never signalled (sharded exchange)
 
 // Per-scene scalars in the form the AM kernel consumes (ConstraintSpec, pkg/constraints.py:31-42).

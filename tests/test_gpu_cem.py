@@ -197,3 +197,35 @@ def test_solve_bilevel_goal_layout_and_warm_start(case):
                        s.residual_median, s.residual_max] for s in res.diagnostics])
     np.testing.assert_allclose(stats[:, :3], g[f"{case}_stats"][:, :3], rtol=1e-4)
     np.testing.assert_allclose(res.distribution.mean, g[f"{case}_final_mean"], rtol=1e-4)
+
+
+def test_absurd_warm_start_rows_do_not_degrade():
+    """A warm start with a few set-points far off the road (pkg/bilevel.py:249-251): they rank
+    last in both implementations, the run is not degraded and elites / best / refit match."""
+    import paper_2212_02224_b200 as bd
+    from paper_2212_02224_b200.harness import canonical_scene
+    from paper_2212_02224_b200.planners import PlannerEnvConfig
+    g = load("absurd")
+    scene = canonical_scene(PlannerEnvConfig(num_samples=100, max_obstacles=10))
+    basis = bd.build_basis(10, 100, 5.0, "bernstein")
+    solver = bd.LowerLevelSolver(basis, bd.TrackingWeights(), bd.ParamLayout(4), bd.ProjectionConfig(1.0, 100, 1e-3), 10)
+    cfg = bd.BiLevelConfig(200, 60, 20, 3, 0.7, 0.9, 1.0, g["cem_mean"], g["cem_cov"])
+    ws = bd.WarmStartSource(g["warm"], bd.ParamLayout(4))
+    seen = []
+    res = bd.solve_bilevel(scene, solver, cfg, np.random.default_rng(4), warm_start=ws,
+                           trace_hook=lambda it, p, pr, c, e: seen.append(np.asarray(e).copy()))
+    assert not res.degraded and not bool(g["cem_degraded"])
+    assert not set(seen[0].tolist()) & {5, 50, 120, 199}
+    np.testing.assert_array_equal(seen[0], g["cem_elites"][0])
+    # free-running fast path: same best record and refit as the reference
+    fast = bd.solve_bilevel(scene, solver, cfg, np.random.default_rng(4), warm_start=ws)
+    assert not fast.degraded and len(fast.diagnostics) == 3
+    assert fast.best.index == int(g["cem_best_index"])
+    np.testing.assert_allclose(fast.best.params.to_vector(), g["cem_best_params"], rtol=1e-6)
+    np.testing.assert_allclose(fast.distribution.mean, g["cem_final_mean"], rtol=1e-4)
+    st = np.array([[s.elite_mean_upper_cost, s.best_augmented_cost, s.cov_trace, s.residual_min,
+                    s.residual_median, s.residual_max] for s in fast.diagnostics])
+    np.testing.assert_allclose(st[:, :5], g["cem_stats"][:, :5], rtol=1e-3, atol=1e-3)
+    # iteration 1 holds the absurd rows: the reference's max is huge, the device's +inf
+    assert np.isinf(st[0, 5]) and g["cem_stats"][0, 5] > 1e15
+    np.testing.assert_allclose(st[1:, 5], g["cem_stats"][1:, 5], rtol=1e-3, atol=1e-3)

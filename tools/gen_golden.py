@@ -564,6 +564,51 @@ def gen_harness():
     print(f"harness written ({len(trace)} trace records)")
 
 
+def gen_absurd():
+    """Set-points far outside any road (|offset| up to 1e300): the reference's fp64 projection
+    returns huge / NaN residuals for them (pkg/projection.py:216-339, pkg/constraints.py:95-153)
+    and they rank last; a CEM run with such warm-start rows (pkg/bilevel.py:249-251) is not
+    degraded."""
+    import warnings
+    from bilevel_drive.behavior import WarmStartSource
+    env = PlannerEnvConfig(num_samples=100, max_obstacles=10)
+    sc = canonical_scene(env)
+    basis = build_basis(10, 100, 5.0, "bernstein")
+    solver = LowerLevelSolver(basis, TrackingWeights(), ParamLayout(4), ProjectionConfig(1.0, 100, 1e-3), 10)
+    P = np.random.default_rng(1).normal([0] * 4 + [12] * 4, [1.5] * 4 + [3] * 4, (12, 8))
+    P[3, :4] = 1e25
+    P[7, 4:] = 1e300
+    P[9] = -1e18
+    P[10, 1] = 1e17
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        _, proj = solver.solve(P, sc)
+        xd, yd = solver.velocities(proj.xi)
+    from bilevel_drive.bilevel import upper_cost_batch
+    out = {"lower_params": P, "lower_resid": proj.residuals, "lower_cost": upper_cost_batch(xd, yd, sc.spec.v_max),
+           "lower_xi": proj.xi}
+    warm = np.random.default_rng(2).normal([0] * 4 + [12] * 4, [1.5] * 4 + [3] * 4, (200, 8))
+    warm[5, :4] = 1e25
+    warm[50, 4:] = -1e18
+    warm[120, 1] = 1e17
+    warm[199] = 3e20
+    cfg = bilevel_config_for(env, sc, batch_size=200, iterations=3)
+    cfg = BiLevelConfig(batch_size=200, constraint_elites=60, elites=20, iterations=3, eta=cfg.eta, gamma=cfg.gamma,
+                        residual_weight=cfg.residual_weight, init_mean=cfg.init_mean, init_cov=cfg.init_cov)
+    elites = []
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        res = solve_bilevel(sc, solver, cfg, np.random.default_rng(4), warm_start=WarmStartSource(warm, ParamLayout(4)),
+                            trace_hook=lambda it, p, pr, c, e: elites.append(np.asarray(e)))
+    out.update(warm=warm, cem_mean=cfg.init_mean, cem_cov=cfg.init_cov, cem_best_index=res.best.index,
+               cem_best_params=res.best.params.to_vector(), cem_elites=np.stack(elites), cem_degraded=res.degraded,
+               cem_stats=np.array([[s.elite_mean_upper_cost, s.best_augmented_cost, s.cov_trace, s.residual_min,
+                                    s.residual_median, s.residual_max] for s in res.diagnostics]),
+               cem_final_mean=res.distribution.mean, cem_final_cov=res.distribution.cov)
+    np.savez_compressed(os.path.join(OUT, "absurd.npz"), **out)
+    print(f"absurd written: lower resid {proj.residuals[[3, 7, 9, 10]]}, cem best {res.best.index}")
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", nargs="*", default=None)
@@ -571,7 +616,7 @@ if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
     jobs = {"basis": gen_basis, "lower": gen_lower, "scenes": gen_scenes, "cem_small": gen_cem_small,
             "cem_c2": gen_cem_c2, "worlds": gen_worlds, "sim": gen_sim, "episodes": gen_episodes, "cem_variants": gen_cem_variants, "planners": gen_planners,
-            "harness": gen_harness}
+            "harness": gen_harness, "absurd": gen_absurd}
     for name, fn in jobs.items():
         if a.only is None or name in a.only:
             fn()
