@@ -16,11 +16,11 @@ sys.path.insert(0, "/root/reference/pkg/src")
 
 
 def one(args):
-    seed, lanes, density, vehicles, length = args
+    seed, lanes, density, vehicles, length, planner = args
     from bilevel_drive.highway import RoadSpec, ScenarioConfig, run_episode
     from bilevel_drive.planners import PlannerEnvConfig, make_planner
     sc = ScenarioConfig(RoadSpec(lanes), density, vehicles, seed, episode_length=length)
-    log = run_episode(sc, make_planner("mpc-bilevel", PlannerEnvConfig(), seed=0))
+    log = run_episode(sc, make_planner(planner, PlannerEnvConfig(), seed=0))
     return seed, {"steps": len(log.steps), "collided": log.collided, "collision_step": log.collision_step,
                   "lane_departed": log.lane_departed, "failed": log.failed, "mean_speed": log.mean_speed(),
                   "solve_time": sum(log.solve_times()) / max(1, len(log.solve_times()))}
@@ -34,10 +34,11 @@ if __name__ == "__main__":
     ap.add_argument("--vehicles", type=int, default=12)
     ap.add_argument("--length", type=int, default=150)
     ap.add_argument("--workers", type=int, default=os.cpu_count())
+    ap.add_argument("--planner", default="mpc-bilevel")
     ap.add_argument("--out", required=True)
     a = ap.parse_args()
     with ProcessPoolExecutor(a.workers) as ex:
-        res = dict(ex.map(one, [(s, a.lanes, a.density, a.vehicles, a.length) for s in a.seeds]))
-    cfg = {"lanes": a.lanes, "density": a.density, "vehicles": a.vehicles, "length": a.length}
+        res = dict(ex.map(one, [(s, a.lanes, a.density, a.vehicles, a.length, a.planner) for s in a.seeds]))
+    cfg = {"lanes": a.lanes, "density": a.density, "vehicles": a.vehicles, "length": a.length, "planner": a.planner}
     json.dump({"config": cfg, "episodes": {str(k): v for k, v in sorted(res.items())}}, open(a.out, "w"), indent=1)
     print(json.dumps(cfg), sum(v["collided"] for v in res.values()), "collisions of", len(res))
