@@ -70,3 +70,24 @@ def test_bench_suite_from_yaml(tmp_path):
     manifest = json.loads((outdir / "manifest.json").read_text())
     assert manifest["seeds"] == [4, 9]
     assert len((outdir / "timings.csv").read_text().splitlines()) == 3
+
+
+def test_bench_rerun_is_byte_identical(tmp_path):
+    """SPEC acceptance 7: rerunning a suite with the same config writes a
+    byte-identical metrics file (timings go to the side file)."""
+    import yaml
+    from paper_2212_02224_b200.__main__ import main
+    cfg = {"planners": ["mpc-bilevel", "mpc-random", "mpc-vanilla"], "episodes_per_cell": 3,
+           "env": {"batch_size": 300, "constraint_elites": 90, "elites": 30, "iterations": 3},
+           "scenarios": [{"scenario_id": "d", "lane_count": 4, "density": 2.0, "vehicle_count": 24,
+                          "episode_length": 40},
+                         {"scenario_id": "s", "lane_count": 2, "density": 1.0, "vehicle_count": 10,
+                          "episode_length": 40}]}
+    path = tmp_path / "suite.yaml"
+    path.write_text(yaml.safe_dump(cfg))
+    runs = []
+    for k in range(2):
+        out = tmp_path / f"o{k}"
+        assert main(["bench", "--config", str(path), "--output", str(out)]) == 0
+        runs.append(((out / "metrics.csv").read_bytes(), (out / "manifest.json").read_bytes()))
+    assert runs[0] == runs[1]

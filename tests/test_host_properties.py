@@ -77,3 +77,15 @@ def test_spawn_layout_invariants(lanes, dens, n, seed):
         for k in range(lanes):                  # cursors advance along each lane
             xs = st_.veh[0, :n][lane == k, 0]
             assert np.all(np.diff(xs) > 0)
+
+
+@settings(max_examples=200, deadline=None)
+@given(st.lists(st.floats(-20, 20), min_size=3, max_size=3), st.lists(st.floats(-20, 20), min_size=3, max_size=3),
+       st.floats(2.0, 6.0), st.floats(1.5, 2.5), st.floats(2.0, 6.0), st.floats(1.5, 2.5))
+def test_footprint_overlap_is_symmetric(pa, pb, la, wa, lb, wb):
+    """SPEC acceptance 8 "collision-detector symmetry": the separating-axis footprint test of the
+    simulator (pkg/highway.py:339-355, restated in oracle/sim.py) is symmetric."""
+    from oracle.sim import overlap
+    a = (pa[0], pa[1] / 4.0, pa[2] / 10.0, la, wa)
+    b = (pb[0], pb[1] / 4.0, pb[2] / 10.0, lb, wb)
+    assert overlap(a, b) == overlap(b, a)
