@@ -274,22 +274,29 @@ __global__ void __launch_bounds__(RANK_REFIT_THREADS) rank_refit_kernel(CemState
         if (s.cons_idx) s.cons_idx[(size_t)scene * n + i] = j;
     }
     __syncthreads();
-    // rank among the constraint elites by (aug, sample index), scatter index and aug: a warp per
-    // elite, its lanes compare 32 keys at a time (ballot + popc)
+    // rank among the constraint elites by (aug, sample index), scatter index and aug: four
+    // threads per elite, each counting the keys that precede it in a quarter of the list, the
+    // four counts summed with two shuffles (the group is four aligned lanes of one warp)
     {
-        const int wp = threadIdx.x >> 5, ln = threadIdx.x & 31;
-        for (int i = wp; i < n; i += blockDim.x >> 5) {
-            const unsigned long long ki = key2[i];
-            const int ji = cidx[i];
+        const int quarter = (n + 3) / 4;
+        for (int t0 = 0; t0 < 4 * n; t0 += blockDim.x) {
+            const int t = t0 + threadIdx.x;
+            const int i = t >> 2, g = t & 3;
             int rk = 0;
-            for (int k0 = 0; k0 < n; k0 += 32) {
-                const int k = k0 + ln;
-                const bool before = k < n && ((key2[k] < ki) || (key2[k] == ki && cidx[k] < ji));
-                rk += __popc(__ballot_sync(0xffffffffu, before));
+            if (i < n) {
+                const unsigned long long ki = key2[i];
+                const int ji = cidx[i];
+                const int k1 = min(n, (g + 1) * quarter);
+                for (int k = g * quarter; k < k1; ++k) {
+                    const unsigned long long kk = key2[k];
+                    rk += (kk < ki) || (kk == ki && cidx[k] < ji);
+                }
             }
-            BD_CHECK(rk >= 0 && rk < n);
-            if (ln == 0) {
-                idx2[rk] = ji;
+            rk += __shfl_xor_sync(0xffffffffu, rk, 1);
+            rk += __shfl_xor_sync(0xffffffffu, rk, 2);
+            if (i < n && g == 0) {
+                BD_CHECK(rk >= 0 && rk < n);
+                idx2[rk] = cidx[i];
                 aug2[rk] = augc[i];
             }
         }
@@ -321,25 +328,44 @@ __global__ void __launch_bounds__(RANK_REFIT_THREADS) rank_refit_kernel(CemState
     const double eta = s.eta;
     double* mean = s.mean + scene * d;
     double* cov = s.cov + scene * d * d;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     auto P = [&](int i, int r) -> double {
         return staged ? pe[i * d + r] : s.params[(base + idx2[i]) * d + r];
     };
-    for (int r = warp; r < d; r += nwarp) {
+    // every thread takes one entry and a strided chunk of the elites; the chunk partials are
+    // folded in a fixed order (deterministic)
+    __shared__ double partial[RANK_REFIT_THREADS];
+    {
+        const int chunks = blockDim.x / d, e = threadIdx.x % d, ch = threadIdx.x / d;
         double acc = 0.0;
-        for (int i = lane; i < q; i += 32) acc = fma(w[i], P(i, r), acc);
-        for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) mu_new[r] = (1.0 - eta) * mean[r] + eta * acc;
+        if (ch < chunks)
+            for (int i = ch; i < q; i += chunks) acc = fma(w[i], P(i, e), acc);
+        partial[threadIdx.x] = acc;
+        __syncthreads();
+        if (threadIdx.x < d) {
+            double t = 0.0;
+            for (int k = 0; k < chunks; ++k) t += partial[k * d + threadIdx.x];
+            mu_new[threadIdx.x] = (1.0 - eta) * mean[threadIdx.x] + eta * t;
+        }
+        __syncthreads();
     }
-    __syncthreads();
-    for (int e = warp; e < d * d; e += nwarp) {
+    {
+        const int dd = d * d, chunks = blockDim.x / dd, e = threadIdx.x % dd, ch = threadIdx.x / dd;
         const int r = e / d, c = e % d;
         double acc = 0.0;
-        for (int i = lane; i < q; i += 32) acc = fma(w[i] * (P(i, r) - mu_new[r]), P(i, c) - mu_new[c], acc);
-        for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) cnew[e] = (1.0 - eta) * cov[e] + eta * acc + (r == c ? 1e-6 : 0.0);
+        if (ch < chunks) {
+            const double mr = mu_new[r], mc = mu_new[c];
+            for (int i = ch; i < q; i += chunks) acc = fma(w[i] * (P(i, r) - mr), P(i, c) - mc, acc);
+        }
+        partial[threadIdx.x] = acc;
+        __syncthreads();
+        if (threadIdx.x < dd) {
+            double t = 0.0;
+            for (int k = 0; k < chunks; ++k) t += partial[k * dd + threadIdx.x];
+            cnew[threadIdx.x] = (1.0 - eta) * cov[threadIdx.x] + eta * t + (r == c ? 1e-6 : 0.0);
+        }
+        __syncthreads();
     }
-    __syncthreads();
     for (int e = threadIdx.x; e < d * d; e += blockDim.x) {
         const int r = e / d, c = e % d;
         const double v = 0.5 * (cnew[r * d + c] + cnew[c * d + r]);
