@@ -138,6 +138,12 @@ def test_errors_follow_reference():
     # non-finite set-points: the reference's QPRightHandSideBatch raises ValueError
     with pytest.raises(ValueError, match="finite"):
         solver.solve(np.full((2, 8), np.nan), _scene(g))
+    # an empty batch is rejected, a single 1-D behaviour vector is a batch of one (reference:
+    # "batch must hold at least one sample"; np.atleast_2d of the parameters)
+    with pytest.raises(ValueError):
+        solver.solve(np.zeros((0, 8)), _scene(g))
+    _, one = solver.solve(np.asarray(g["params"])[0], _scene(g))
+    assert one.xi.shape == (22, 1) and one.residuals.shape == (1,)
 
 
 def test_absurd_setpoints_rank_last():
