@@ -69,13 +69,17 @@ struct AmArgs {
 // Batch-global early exit (pkg/projection.py:329): the first iteration whose batch maximum
 // residual is <= tol sets iterations_used and, if that is before max_iters, the replay count.
 // Out of line: run by one CTA per scene, kept away from the main loop's register allocation.
-__device__ __noinline__ void exit_scan_block(const unsigned* base, int max_iters, double tol, int scene,
+__device__ __noinline__ void exit_scan_block(unsigned* base, int max_iters, double tol, int scene,
                                                 int* iters_used, int* replay, unsigned long long* conflicts) {
     __shared__ int red[32];
     int first = max_iters;
     for (int it = threadIdx.x; it < max_iters; it += blockDim.x) {
         unsigned mx = 0;
-        for (int s = 0; s < ITMAX_SLOTS; ++s) mx = max(mx, __ldcg(base + (size_t)it * ITMAX_SLOTS + s));
+        for (int s = 0; s < ITMAX_SLOTS; ++s) {
+            unsigned* slot = base + (size_t)it * ITMAX_SLOTS + s;
+            mx = max(mx, __ldcg(slot));
+            __stcg(slot, 0u);                   // re-arm for the next launch (no memset needed)
+        }
         if (static_cast<double>(__uint_as_float(mx)) <= tol && it < first) first = it;
     }
     for (int o = 16; o >= 1; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));

@@ -85,6 +85,7 @@ struct bd_ctx {
     // workspace
     DevBuf w_xibar, w_b, w_mu, w_xi, w_res, w_cost, w_hist, w_itmax, w_iters, w_replay, w_conf, w_err, w_params, w_done,
         w_order;
+    size_t itmax_clean = 0;       // leading bytes of w_itmax known to be zero (re-armed by the exit scan)
     DevBuf stage[8];
     int n_stage = 0;
     DevBuf out_pack;              // coalesced device->host outputs: gathered here, one D2H copy
@@ -449,18 +450,32 @@ int require_solver(bd_ctx* ctx, bool need_stage1) {
 }
 
 // Projection core: xi_bar, b device pointers -> outputs in device buffers.
+// The per-iteration batch-maximum slots; a reallocation loses the zeroed prefix.
+int ensure_itmax(bd_ctx* ctx, size_t bytes) {
+    if (ctx->w_itmax.bytes < bytes) {
+        ctx->itmax_clean = 0;
+        CU(ctx->w_itmax.ensure(bytes));
+    }
+    return 0;
+}
+
 int run_projection(bd_ctx* ctx, int B, const double* xi_bar, const double* b, int iters, double tol, double* xi,
                    double* res, double* cost, float* hist, int* iters_used, unsigned long long* conf,
-                   bool external_exit = false) {
+                   bool external_exit = false, bool count_conflicts = true) {
     const int S = ctx->S;
-    CU(ctx->w_itmax.ensure((size_t)S * iters * ITMAX_SLOTS * 4));
+    const size_t itmax_bytes = (size_t)S * iters * ITMAX_SLOTS * 4;
+    if (int rc = ensure_itmax(ctx, itmax_bytes)) return rc;
     CU(ctx->w_replay.ensure((size_t)S * 4));
     if (ctx->w_done.bytes < (size_t)S * 4) {
         CU(ctx->w_done.ensure((size_t)S * 4));
         CU(cudaMemsetAsync(ctx->w_done.p, 0, (size_t)S * 4, ctx->stream));
     }
-    CU(cudaMemsetAsync(ctx->w_itmax.p, 0, (size_t)S * iters * ITMAX_SLOTS * 4, ctx->stream));
-    CU(cudaMemsetAsync(conf, 0, (size_t)S * 8, ctx->stream));
+    // the per-iteration batch maxima must start at zero; the in-kernel exit scan re-zeroes what it
+    // read, so back-to-back full passes skip the memset (sharded passes scan outside the kernel)
+    if (external_exit || ctx->itmax_clean < itmax_bytes)
+        CU(cudaMemsetAsync(ctx->w_itmax.p, 0, itmax_bytes, ctx->stream));
+    ctx->itmax_clean = external_exit ? 0 : std::max(ctx->itmax_clean, itmax_bytes);
+    if (count_conflicts) CU(cudaMemsetAsync(conf, 0, (size_t)S * 8, ctx->stream));
     AmArgs a{};
     a.m = ctx->m; a.neq = ctx->neq; a.n_obs = ctx->obs_pad; a.n_curv = ctx->n_curv; a.B = B; a.max_iters = iters;
     a.rho = ctx->rho;
@@ -479,6 +494,7 @@ int run_projection(bd_ctx* ctx, int B, const double* xi_bar, const double* b, in
     a.done_ctr = ctx->w_done.as<unsigned>();
     if (external_exit) a.done_ctr = nullptr;   // sharded batch: the exit is decided across ranks
     int rc = launch_am(ctx, a, false);     // its last CTA per scene runs the exit scan
+    if (rc) ctx->itmax_clean = 0;
     if (rc || external_exit) return rc;
     return launch_am(ctx, a, true);        // replay guard: exits at once unless an early exit fired
 }
@@ -1028,7 +1044,7 @@ int bd_replay_shard(bd_ctx* ctx, int B, const double* xi_bar, int iters, double*
     if ((rc = stage_out(ctx, xi, (size_t)B * NX, ctx->w_xi, &dxi))) return rc;
     if ((rc = stage_out(ctx, res, (size_t)B, ctx->w_res, &dres))) return rc;
     if ((rc = stage_out(ctx, cost, (size_t)B, ctx->w_cost, &dcost))) return rc;
-    CU(ctx->w_itmax.ensure((size_t)iters * ITMAX_SLOTS * 4));
+    if ((rc = ensure_itmax(ctx, (size_t)iters * ITMAX_SLOTS * 4))) return rc;
     CU(ctx->w_replay.ensure(4));
     CU(ctx->w_conf.ensure(8));
     CU(cudaMemsetAsync(ctx->w_err.p, 0, 4, ctx->stream));
@@ -1055,7 +1071,7 @@ int bd_replay_shard_dev(bd_ctx* ctx, int B, const double* xi_bar, int max_iters,
     if ((rc = stage_out(ctx, xi, (size_t)B * NX, ctx->w_xi, &dxi))) return rc;
     if ((rc = stage_out(ctx, res, (size_t)B, ctx->w_res, &dres))) return rc;
     if ((rc = stage_out(ctx, cost, (size_t)B, ctx->w_cost, &dcost))) return rc;
-    CU(ctx->w_itmax.ensure((size_t)max_iters * ITMAX_SLOTS * 4));
+    if ((rc = ensure_itmax(ctx, (size_t)max_iters * ITMAX_SLOTS * 4))) return rc;
     CU(ctx->w_replay.ensure(4));
     CU(ctx->w_conf.ensure(8));
     // the guarded kernel reads the count on the device: <= 0 returns at once, so no host decision
@@ -1351,7 +1367,8 @@ int bd_cem_cycle(bd_ctx* ctx, int S, const bd_cem_config* cfg, const double* ini
         ctx->launches++;
         if ((rc = run_projection(ctx, B, ctx->w_xibar.as<double>(), db, cfg->am_iters, cfg->tol,
                                  ctx->w_xi.as<double>(), ctx->w_res.as<double>(), ctx->w_cost.as<double>(), nullptr,
-                                 ctx->w_iters.as<int>(), ctx->w_conf.as<unsigned long long>())))
+                                 ctx->w_iters.as<int>(), ctx->w_conf.as<unsigned long long>(), false,
+                                 false)))   // clip conflicts are not reported by the CEM cycle
             return rc;
         launch_rank_count(ctx, s.resid, s.err, S, B, ctx->w_order.as<int>());
         rank_refit_kernel<<<S, RANK_REFIT_THREADS, rsmem, ctx->stream>>>(s, it, ctx->w_order.as<int>());
