@@ -37,13 +37,13 @@ __host__ __device__ __forceinline__ int s1_ld(int nr) {
 constexpr int S1_VEC = 32;
 
 __device__ __forceinline__ void stage1_load(const S1Args& a, double* kinv, double* kkt, double* qm) {
-    const int nn = a.nr * a.nr, ld = s1_ld(a.nr);
-    for (int i = threadIdx.x; i < a.nr * ld; i += blockDim.x) {
-        const int r = i / ld, c = i - r * ld;
-        kinv[i] = c < a.nr ? a.kinv[r * a.nr + c] : 0.0;
-        kkt[i] = c < a.nr ? a.kkt[r * a.nr + c] : 0.0;
-    }
-    (void)nn;
+    // a warp per row, a lane per column (no index division; coalesced row reads)
+    const int ld = s1_ld(a.nr), lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int r = threadIdx.x >> 5; r < a.nr; r += nw)
+        for (int c = lane; c < ld; c += 32) {
+            kinv[r * ld + c] = c < a.nr ? a.kinv[r * a.nr + c] : 0.0;
+            kkt[r * ld + c] = c < a.nr ? a.kkt[r * a.nr + c] : 0.0;
+        }
     if (!a.rhs_in)
         for (int i = threadIdx.x; i < NC * a.m_seg; i += blockDim.x) { qm[i] = a.qmx[i]; qm[NC * a.m_seg + i] = a.qmy[i]; }
 }
