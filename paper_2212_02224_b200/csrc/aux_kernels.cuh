@@ -64,16 +64,21 @@ __device__ __forceinline__ double s1_rowdot(const double* M, const double* v, in
     return s;
 }
 
+// DEF: the default layout (28 KKT rows = 22 coefficients + 6 equalities, 4 segments, no goal rows,
+// behaviour vector of 8) as compile-time constants, so the row loops unroll without bounds checks.
+constexpr int S1_DEF_NR = NX + 6, S1_DEF_MS = 4, S1_DEF_DIM = 8;
+template <bool DEF = false>
 __device__ __forceinline__ void stage1_body(const S1Args& a, int row, const double* pr, const double* kinv,
                                             const double* kkt, const double* qm, double* vec) {
     const int lane = threadIdx.x & 31;
     const int i = lane;
+    const int nr = DEF ? S1_DEF_NR : a.nr;
     double rhs = 0.0;
-    if (a.rhs_in) {
-        if (i < a.nr) rhs = a.rhs_in[(size_t)row * a.nr + i];
+    if (!DEF && a.rhs_in) {
+        if (i < nr) rhs = a.rhs_in[(size_t)row * nr + i];
     } else {
     const int scene = row / a.B;
-    const int ms = a.m_seg;
+    const int ms = DEF ? S1_DEF_MS : a.m_seg;
     if (i < NC) {
         double s = 0.0;
         for (int k = 0; k < ms; ++k) s = fma(qm[i * ms + k], pr[ms + k], s);
@@ -82,20 +87,20 @@ __device__ __forceinline__ void stage1_body(const S1Args& a, int row, const doub
         double s = 0.0;
         for (int k = 0; k < ms; ++k) s = fma(qm[NC * ms + (i - NC) * ms + k], pr[k], s);
         rhs = -s;
-    } else if (i < a.nr) {
+    } else if (i < nr) {
         const int e = i - NX;
-        if (a.with_goal && e >= 6) rhs = (e == 6) ? pr[2 * ms] : (e == 7) ? pr[2 * ms + 1] : 0.0;
+        if (!DEF && a.with_goal && e >= 6) rhs = (e == 6) ? pr[2 * ms] : (e == 7) ? pr[2 * ms + 1] : 0.0;
         else rhs = a.bscene[(size_t)scene * a.neq + e];
     }
     }
-    const int ld = s1_ld(a.nr);
-    if (i < a.nr) vec[i] = rhs;
+    const int ld = s1_ld(nr);
+    if (i < nr) vec[i] = rhs;
     __syncwarp();
-    const double sol = i < a.nr ? s1_rowdot(kinv, vec, i, a.nr, ld) : 0.0;
+    const double sol = i < nr ? s1_rowdot(kinv, vec, i, nr, ld) : 0.0;
     __syncwarp();
-    if (i < a.nr) vec[i] = sol;
+    if (i < nr) vec[i] = sol;
     __syncwarp();
-    double res = i < a.nr ? s1_rowdot(kkt, vec, i, a.nr, ld) : 0.0;
+    double res = i < nr ? s1_rowdot(kkt, vec, i, nr, ld) : 0.0;
     __syncwarp();
     res = fabs(res - rhs);
     double scale = fabs(rhs);
@@ -104,15 +109,16 @@ __device__ __forceinline__ void stage1_body(const S1Args& a, int row, const doub
         scale = fmax(scale, __shfl_xor_sync(0xffffffffu, scale, o));
     }
     const bool finite_rhs = __all_sync(0xffffffffu, isfinite(rhs));
-    if (lane == 0 && !finite_rhs) atomicOr(a.err + (a.rhs_in ? 0 : row / a.B), ERR_BAD_RHS);
-    else if (lane == 0 && !(res <= 1e-8 * (1.0 + scale))) atomicOr(a.err + (a.rhs_in ? 0 : row / a.B), ERR_KKT_RESID);
-    if (a.rhs_in) {
-        if (i < a.nr) a.sol_out[(size_t)row * a.nr + i] = sol;
+    if (lane == 0 && !finite_rhs) atomicOr(a.err + (!DEF && a.rhs_in ? 0 : row / a.B), ERR_BAD_RHS);
+    else if (lane == 0 && !(res <= 1e-8 * (1.0 + scale)))
+        atomicOr(a.err + (!DEF && a.rhs_in ? 0 : row / a.B), ERR_KKT_RESID);
+    if (!DEF && a.rhs_in) {
+        if (i < nr) a.sol_out[(size_t)row * nr + i] = sol;
         return;
     }
     if (i < NX) {
         if (a.xi_bar) a.xi_bar[(size_t)row * NX + i] = sol;
-    } else if (i < a.nr) {
+    } else if (i < nr) {
         const int e = i - NX;
         if (a.mu) a.mu[(size_t)row * a.neq + e] = sol;
         if (a.b_out) a.b_out[(size_t)row * a.neq + e] = rhs;
@@ -135,6 +141,7 @@ __global__ void __launch_bounds__(256) stage1_kernel(const S1Args a) {
 
 // K4 + K1 fused for the CEM cycle: p = mean + z L^T (pkg/bilevel.py:51-57; z from the caller
 // or device Philox; the warm-start tile on iteration 1) written to params, then stage 1.
+template <bool DEF>
 __global__ void __launch_bounds__(256) sample_stage1_kernel(CemState cs, int it, const double* z, const double* warm,
                                                            uint64_t seed, int scene_offset, double* params,
                                                            const S1Args a) {
@@ -151,7 +158,7 @@ __global__ void __launch_bounds__(256) sample_stage1_kernel(CemState cs, int it,
     if (row >= a.total) return;
     const int scene = row / a.B, j = row % a.B;
     if (cs.err[scene]) return;                          // failed scene: frozen until the cycle ends
-    const int d = cs.dim;
+    const int d = DEF ? S1_DEF_DIM : cs.dim;
     double* pr = pw + wid * MAX_DIM;
     if (warm != nullptr) {
         if (lane < d) pr[lane] = warm[(size_t)row * d + lane];
@@ -171,7 +178,7 @@ __global__ void __launch_bounds__(256) sample_stage1_kernel(CemState cs, int it,
     }
     __syncwarp();
     if (lane < d) params[(size_t)row * d + lane] = pr[lane];
-    stage1_body(a, row, pr, kinv, kkt, qm, vw + wid * S1_VEC);
+    stage1_body<DEF>(a, row, pr, kinv, kkt, qm, vw + wid * S1_VEC);
 }
 
 // SamplingDistribution.sample (pkg/bilevel.py:51-57) for one distribution: the factor is

@@ -1359,10 +1359,13 @@ int bd_cem_cycle(bd_ctx* ctx, int S, const bd_cem_config* cfg, const double* ini
     s1.kinv = ctx->kinv1.as<double>(); s1.params = ctx->w_params.as<double>(); s1.bscene = ctx->bscene.as<double>();
     s1.xi_bar = ctx->w_xibar.as<double>(); s1.mu = nullptr; s1.b_out = db; s1.err = ctx->w_err.as<int>();
     const size_t s1smem = (size_t)(2 * s1.nr * s1_ld(s1.nr) + 2 * NC * s1.m_seg + 8 * MAX_DIM + 8 * S1_VEC) * 8;
-    raise_smem(sample_stage1_kernel, s1smem);
+    const bool s1def = s1.nr == S1_DEF_NR && dim == S1_DEF_DIM && ctx->m_seg == S1_DEF_MS && !ctx->with_goal;
+    raise_smem(sample_stage1_kernel<true>, s1smem);
+    raise_smem(sample_stage1_kernel<false>, s1smem);
     for (int it = it0; it < it1; ++it) {
         const double* zi = dz ? dz + (size_t)(it - it0) * tot * dim : nullptr;
-        sample_stage1_kernel<<<(unsigned)((tot + 7) / 8), 256, s1smem, ctx->stream>>>(
+        auto s1k = s1def ? sample_stage1_kernel<true> : sample_stage1_kernel<false>;
+        s1k<<<(unsigned)((tot + 7) / 8), 256, s1smem, ctx->stream>>>(
             s, it, zi, it == 0 ? dwarm : nullptr, cfg->seed, cfg->scene_offset, ctx->w_params.as<double>(), s1);
         ctx->launches++;
         if ((rc = run_projection(ctx, B, ctx->w_xibar.as<double>(), db, cfg->am_iters, cfg->tol,

@@ -101,8 +101,8 @@ __device__ void philox_normals(uint64_t seed, uint32_t scene, uint32_t it, uint3
 // Warp-cooperative form for one sample per warp: lane l draws Box-Muller pair l (the same
 // counter block and arithmetic as philox_normals, so bit-identical values) and the d normals are
 // broadcast to every lane.  Must be called by all 32 lanes.
-__device__ void philox_normals_warp(uint64_t seed, uint32_t scene, uint32_t it, uint32_t sample, double* z, int d,
-                                    int lane) {
+__device__ __forceinline__ void philox_normals_warp(uint64_t seed, uint32_t scene, uint32_t it, uint32_t sample,
+                                                    double* z, int d, int lane) {
     double a = 0.0, b = 0.0;
     if (lane < (d + 1) / 2) {
         uint32_t c[4] = {sample, it, scene, (uint32_t)(lane / 2)};
