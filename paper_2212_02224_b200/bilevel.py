@@ -51,7 +51,7 @@ class SamplingDistribution:
         cov = np.asarray(self.cov, dtype=float)
         if cov.shape != (mean.shape[0], mean.shape[0]):
             raise ValueError(f"cov shape {cov.shape} does not match mean dim {mean.shape[0]}")
-        if not np.allclose(cov, cov.T):
+        if not (np.array_equal(cov, cov.T) or np.allclose(cov, cov.T)):   # exact symmetry: the common, fast case
             raise ValueError("covariance must be symmetric")
         object.__setattr__(self, "mean", mean)
         object.__setattr__(self, "cov", cov)
