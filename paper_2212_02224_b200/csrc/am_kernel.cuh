@@ -154,10 +154,12 @@ __device__ __forceinline__ void group_reduce_scatter(float (&v)[NV], int lane) {
 // The x/y pairs run as packed fp32x2 (FFMA2 with the basis value broadcast).
 constexpr int SORT_MIN_PAIRS = 8;     // >= 16 obstacles: sorted-window obstacle pass (dense scenes)
 constexpr int SORT_MAX_OBS = 128;     // the binary search covers up to 128 obstacles per timestep
+constexpr int SCAN_W = 2;             // sorted-window scan: candidates loaded per step
 
 #ifndef BD_AM_OBS_EARLY
 #define BD_AM_OBS_EARLY 1
 #endif
+
 template <int P, bool CURV, bool INIT, int NV, int MT, int NPT, int TPB>
 __device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float4* __restrict__ osm,
                                       const float* __restrict__ csm, const float2 (&cxy)[NC], float (&v)[NV],
@@ -285,21 +287,31 @@ __device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float
 #pragma unroll
             for (int step = 64; step > 0; step >>= 1)
                 if (k + step <= nob && row[k + step - 1].x <= lo_key) k += step;
-            for (; k < nob; ++k) {
-                const float2 ob = row[k];
-                if (!(ob.x < hi_key)) break;
-                const float wc = xs + ob.x, ws = ys + ob.y;
-                const float q = fmaf(wc, wc, ws * ws);
-                if (q < 1.f) {
-                    coll += 1.f - q;
-                    if (q > 0.f) {
-                        const float f = 1.f - rsqrtf(q);
-                        rox = fmaf(wc, f, rox);
-                        roy = fmaf(ws, f, roy);
-                    } else {
-                        rox -= 1.f;
+            // SCAN_W candidates per step, loaded together (rows are sorted, so "inside the window"
+            // holds for a prefix of them); same obstacle order as a one-by-one scan, which waited
+            // on one dependent load per obstacle (2 per step: dense launch 2.31 -> 2.09 ms)
+            for (; k < nob; k += SCAN_W) {
+                float2 ob[SCAN_W];
+#pragma unroll
+                for (int u = 0; u < SCAN_W; ++u) ob[u] = row[min(k + u, nob - 1)];
+                bool inside = true;
+#pragma unroll
+                for (int u = 0; u < SCAN_W; ++u) {
+                    inside = inside && (k + u < nob) && (ob[u].x < hi_key);
+                    const float wc = xs + ob[u].x, ws = ys + ob[u].y;
+                    const float q = fmaf(wc, wc, ws * ws);
+                    if (inside && q < 1.f) {
+                        coll += 1.f - q;
+                        if (q > 0.f) {
+                            const float f = 1.f - rsqrtf(q);
+                            rox = fmaf(wc, f, rox);
+                            roy = fmaf(ws, f, roy);
+                        } else {
+                            rox -= 1.f;
+                        }
                     }
                 }
+                if (!inside) break;
             }
         } else if (qmin < 1.f) {
             for (int o = 0; o < npair; ++o) {
