@@ -153,12 +153,13 @@ __device__ __forceinline__ void group_reduce_scatter(float (&v)[NV], int lane) {
 // (v[2k] = g_x[k], v[2k+1] = g_y[k]), the direct residual (v[22]) and the upper cost (v[23]).
 // The x/y pairs run as packed fp32x2 (FFMA2 with the basis value broadcast).
 constexpr int SORT_MIN_PAIRS = 8;     // >= 16 obstacles: sorted-window obstacle pass (dense scenes)
-constexpr int SORT_MAX_OBS = 128;     // the binary search covers up to 128 obstacles per timestep
+constexpr int SORT_MAX_OBS = 256;     // the 4-ary window search reaches k <= 255
 constexpr int SCAN_W = 2;             // sorted-window scan: candidates loaded per step
 
 #ifndef BD_AM_OBS_EARLY
 #define BD_AM_OBS_EARLY 1
 #endif
+
 
 template <int P, bool CURV, bool INIT, int NV, int MT, int NPT, int TPB>
 __device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float4* __restrict__ osm,
@@ -284,9 +285,18 @@ __device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float
             const float win = 1.0f + fmaf(4e-6f, fabsf(xs), 1e-5f);
             const float lo_key = -xs - win, hi_key = -xs + win;
             int k = 0;
+            // 4-ary search: k = #keys <= lo_key, three independent loads per level (strides 64,
+            // 16, 4, 1 reach k <= 255); a binary search waited on one dependent load per level
 #pragma unroll
-            for (int step = 64; step > 0; step >>= 1)
-                if (k + step <= nob && row[k + step - 1].x <= lo_key) k += step;
+            for (int stride = 64; stride > 0; stride >>= 2) {
+                int cnt = 0;
+#pragma unroll
+                for (int u = 1; u < 4; ++u) {
+                    const int idx = k + u * stride - 1;
+                    cnt += (idx < nob && row[min(idx, nob - 1)].x <= lo_key) ? 1 : 0;
+                }
+                k += cnt * stride;
+            }
             // SCAN_W candidates per step, loaded together (rows are sorted, so "inside the window"
             // holds for a prefix of them); same obstacle order as a one-by-one scan, which waited
             // on one dependent load per obstacle (2 per step: dense launch 2.31 -> 2.09 ms)
