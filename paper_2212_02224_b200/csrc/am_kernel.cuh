@@ -97,7 +97,7 @@ __device__ __noinline__ void exit_scan_block(unsigned* base, int max_iters, doub
 
 // Shared-memory carve-up, identical on host and device.
 struct AmSmem {
-    size_t w, obs, k, kb, a, curv, scr, dap, kap, total;
+    size_t w, obs, k, kb, a, curv, scr, dap, kap, kix, total;
     __host__ __device__ AmSmem(int m, int n_obs, int neq, int n_curv, int s_cta, int threads, int P, bool curv_on) {
         const int J = (m + P - 1) / P;
         size_t o = 0;
@@ -110,6 +110,8 @@ struct AmSmem {
         scr = o;  o = align_up(o + (size_t)s_cta * SCR_BYTES, 16);
         dap = o;  o = align_up(o + (size_t)J * threads * 4, 16);
         kap = o;  o = align_up(o + (curv_on ? (size_t)J * threads * 4 : 0), 16);
+        // dense scenes: each (timestep slot, thread)'s window start of the previous iteration
+        kix = o;  o = align_up(o + (n_obs >= 2 * 8 ? (size_t)J * threads * 2 : 0), 16);   // 8 = SORT_MIN_PAIRS
         total = o;
     }
     // per-sample scratch: u (24 doubles) | c32 (24 floats) | lambda-state l (24 doubles) | first-step
@@ -164,7 +166,8 @@ constexpr int SCAN_W = 2;             // sorted-window scan: candidates loaded p
 template <int P, bool CURV, bool INIT, int NV, int MT, int NPT, int TPB>
 __device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float4* __restrict__ osm,
                                       const float* __restrict__ csm, const float2 (&cxy)[NC], float (&v)[NV],
-                                      float* dap, float* kap, int dstride_rt, int p, int m_rt, int npair_rt,
+                                      float* dap, float* kap, unsigned short* kix, int dstride_rt, int p, int m_rt,
+                                      int npair_rt,
                                       int n_curv, const SceneLim& L, int& conf, bool sorted_rt,
                                       bool want_cost = true) {
     // MT / NPT / TPB > 0: timesteps, obstacle pairs and CTA size fixed at compile time (the
@@ -285,18 +288,30 @@ __device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float
             const float win = 1.0f + fmaf(4e-6f, fabsf(xs), 1e-5f);
             const float lo_key = -xs - win, hi_key = -xs + win;
             int k = 0;
-            // 4-ary search: k = #keys <= lo_key, three independent loads per level (strides 64,
-            // 16, 4, 1 reach k <= 255); a binary search waited on one dependent load per level
-#pragma unroll
-            for (int stride = 64; stride > 0; stride >>= 2) {
-                int cnt = 0;
-#pragma unroll
-                for (int u = 1; u < 4; ++u) {
-                    const int idx = k + u * stride - 1;
-                    cnt += (idx < nob && row[min(idx, nob - 1)].x <= lo_key) ? 1 : 0;
-                }
-                k += cnt * stride;
+            bool hit = false;
+            if (!INIT) {
+                // last iteration's window start is usually still right: two independent checks
+                const int k0 = kix[di];
+                const bool okl = k0 == 0 || row[max(k0 - 1, 0)].x <= lo_key;
+                const bool okr = k0 >= nob || row[min(k0, nob - 1)].x > lo_key;
+                hit = okl && okr;
+                k = hit ? k0 : 0;
             }
+            if (!hit) {
+                // 4-ary search: k = #keys <= lo_key, three independent loads per level (strides 64,
+                // 16, 4, 1 reach k <= 255); a binary search waited on one dependent load per level
+#pragma unroll
+                for (int stride = 64; stride > 0; stride >>= 2) {
+                    int cnt = 0;
+#pragma unroll
+                    for (int u = 1; u < 4; ++u) {
+                        const int idx = k + u * stride - 1;
+                        cnt += (idx < nob && row[min(idx, nob - 1)].x <= lo_key) ? 1 : 0;
+                    }
+                    k += cnt * stride;
+                }
+            }
+            kix[di] = (unsigned short)k;
             // SCAN_W candidates per step, loaded together (rows are sorted, so "inside the window"
             // holds for a prefix of them); same obstacle order as a one-by-one scan, which waited
             // on one dependent load per obstacle (2 per step: dense launch 2.31 -> 2.09 ms)
@@ -454,6 +469,7 @@ __global__ void __launch_bounds__(256, BD_AM_MINB) am_kernel(const AmArgs a) {
     float* sc = reinterpret_cast<float*>(su + 24);
     float* dap = reinterpret_cast<float*>(smem + lay.dap) + threadIdx.x;
     float* kap = reinterpret_cast<float*>(smem + lay.kap) + threadIdx.x;
+    unsigned short* kix = reinterpret_cast<unsigned short*>(smem + lay.kix) + threadIdx.x;
     const SceneLim L = a.lim[scene];
     const double rho = a.rho;
 
@@ -511,7 +527,7 @@ __global__ void __launch_bounds__(256, BD_AM_MINB) am_kernel(const AmArgs a) {
             if (!(threadIdx.x & 32) && lane < NX + 2) v[0] += xbuf[lane];
         }
     };
-    sweep<P, CURV, true, NV, MT, NPT, TPB>(wsm, osm, csm, cxy, v, dap, kap, threads, p, m, n_obs / 2, a.n_curv, L,
+    sweep<P, CURV, true, NV, MT, NPT, TPB>(wsm, osm, csm, cxy, v, dap, kap, kix, threads, p, m, n_obs / 2, a.n_curv, L,
                                            conf, a.sorted != 0);
     reduce();
 
@@ -566,7 +582,7 @@ __global__ void __launch_bounds__(256, BD_AM_MINB) am_kernel(const AmArgs a) {
 #pragma unroll
         for (int q = 0; q < NC; ++q) cxy[q] = reinterpret_cast<const float2*>(sc)[q];
         // ---- projections, back-projection, residual at the new iterate
-        sweep<P, CURV, false, NV, MT, NPT, TPB>(wsm, osm, csm, cxy, v, dap, kap, threads, p, m, n_obs / 2, a.n_curv,
+        sweep<P, CURV, false, NV, MT, NPT, TPB>(wsm, osm, csm, cxy, v, dap, kap, kix, threads, p, m, n_obs / 2, a.n_curv,
                                                 L, conf, a.sorted != 0, it == iters - 1);   // cost: last sweep only
         reduce();
         resid = v[r_slot];
