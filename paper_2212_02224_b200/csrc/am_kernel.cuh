@@ -95,6 +95,11 @@ __device__ __noinline__ void exit_scan_block(unsigned* base, int max_iters, doub
     }
 }
 
+#ifndef BD_SORT_MIN_PAIRS
+#define BD_SORT_MIN_PAIRS 8
+#endif
+constexpr int SORT_MIN_PAIRS = BD_SORT_MIN_PAIRS;   // >= 16 obstacles: sorted-window obstacle pass (dense scenes)
+
 // Shared-memory carve-up, identical on host and device.
 struct AmSmem {
     size_t w, obs, k, kb, a, curv, scr, dap, kap, kix, total;
@@ -111,7 +116,7 @@ struct AmSmem {
         dap = o;  o = align_up(o + (size_t)J * threads * 4, 16);
         kap = o;  o = align_up(o + (curv_on ? (size_t)J * threads * 4 : 0), 16);
         // dense scenes: each (timestep slot, thread)'s window start of the previous iteration
-        kix = o;  o = align_up(o + (n_obs >= 2 * 8 ? (size_t)J * threads * 2 : 0), 16);   // 8 = SORT_MIN_PAIRS
+        kix = o;  o = align_up(o + (n_obs >= 2 * SORT_MIN_PAIRS ? (size_t)J * threads * 2 : 0), 16);
         total = o;
     }
     // per-sample scratch: u (24 doubles) | c32 (24 floats) | lambda-state l (24 doubles) | first-step
@@ -154,7 +159,6 @@ __device__ __forceinline__ void group_reduce_scatter(float (&v)[NV], int lane) {
 // forward evaluation, polar split + coupled clips, back-projection of the residuals
 // (v[2k] = g_x[k], v[2k+1] = g_y[k]), the direct residual (v[22]) and the upper cost (v[23]).
 // The x/y pairs run as packed fp32x2 (FFMA2 with the basis value broadcast).
-constexpr int SORT_MIN_PAIRS = 8;     // >= 16 obstacles: sorted-window obstacle pass (dense scenes)
 constexpr int SORT_MAX_OBS = 256;     // the 4-ary window search reaches k <= 255
 constexpr int SCAN_W = 2;             // sorted-window scan: candidates loaded per step
 
