@@ -47,6 +47,21 @@ class FleetResult:
     iterations_done: np.ndarray  # S  (< N: degraded; <= 0: failed in iteration 1)
 
 
+def initial_means(road: np.ndarray, b0: np.ndarray, m_seg: int) -> np.ndarray:
+    """BasePlanner.initial_distribution's mean (pkg/planners.py:218-231) for S worlds at once:
+    lateral set-points at the lane centre nearest to y0 (first on ties; y0 itself on a road
+    without lanes), speed set-points at hypot(xdot0, ydot0).  road: S x (lanes, width, ...)."""
+    S = b0.shape[0]
+    lanes = road[:, 0].astype(np.int64)
+    centres = np.arange(max(int(lanes.max(initial=0)), 1))[None, :] * road[:, 1:2]   # k * width, per world
+    dist = np.abs(centres - b0[:, 1:2])
+    dist[np.arange(centres.shape[1])[None, :] >= lanes[:, None]] = np.inf
+    lane_y = np.where(lanes > 0, centres[np.arange(S), np.argmin(dist, axis=1)], b0[:, 1])
+    speed = np.hypot(b0[:, 2], b0[:, 3])
+    return np.concatenate([np.repeat(lane_y[:, None], m_seg, axis=1), np.repeat(speed[:, None], m_seg, axis=1)],
+                          axis=1)
+
+
 class FleetPlanner:
     """Batched solve_bilevel over a list of scenes sharing one basis / QP / obstacle count."""
 
@@ -108,11 +123,7 @@ class FleetPlanner:
         ms = self.layout.m_seg
         S = b0.shape[0]
         road = np.asarray(worlds.road.cpu() if hasattr(worlds.road, "cpu") else worlds.road)
-        mean = np.empty((S, 2 * ms))
-        for s in range(S):
-            c = np.arange(int(road[s, 0])) * road[s, 1]
-            lane_y = float(c[np.argmin(np.abs(c - b0[s, 1]))]) if c.size else b0[s, 1]
-            mean[s] = np.concatenate([np.full(ms, lane_y), np.full(ms, float(np.hypot(b0[s, 2], b0[s, 3])))])
+        mean = initial_means(road, b0, ms)
         cov = np.repeat(np.diag(np.concatenate([np.full(ms, sigma_offset ** 2), np.full(ms, sigma_speed ** 2)]))[None],
                         S, axis=0)
         dim, N, n2 = self.layout.dim, self.config.iterations, 2 * self.solver.basis.num_coeffs

@@ -89,3 +89,21 @@ def test_footprint_overlap_is_symmetric(pa, pb, la, wa, lb, wb):
     a = (pa[0], pa[1] / 4.0, pa[2] / 10.0, la, wa)
     b = (pb[0], pb[1] / 4.0, pb[2] / 10.0, lb, wb)
     assert overlap(a, b) == overlap(b, a)
+
+
+@settings(max_examples=60, deadline=None)
+@given(st.integers(1, 40), st.integers(0, 2**31 - 1))
+def test_fleet_initial_means_match_per_world_rule(S, seed):
+    """FleetPlanner.plan_cycle's vectorised initial mean equals the per-world rule of
+    BasePlanner.initial_distribution (pkg/planners.py:218-231), bit for bit."""
+    from paper_2212_02224_b200.fleet import initial_means
+    rng = np.random.default_rng(seed)
+    road = np.stack([rng.integers(0, 6, S).astype(float), rng.uniform(3.0, 5.0, S)], axis=1)
+    b0 = rng.normal(size=(S, 6)) * 5.0
+    b0[: S // 3, 1] = np.round(b0[: S // 3, 1])          # exact ties between two lane centres
+    ref = np.empty((S, 8))
+    for s in range(S):
+        c = np.arange(int(road[s, 0])) * road[s, 1]
+        lane_y = float(c[np.argmin(np.abs(c - b0[s, 1]))]) if c.size else b0[s, 1]
+        ref[s] = np.concatenate([np.full(4, lane_y), np.full(4, float(np.hypot(b0[s, 2], b0[s, 3])))])
+    np.testing.assert_array_equal(initial_means(road, b0, 4), ref)
