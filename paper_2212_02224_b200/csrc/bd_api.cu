@@ -325,9 +325,13 @@ int finish_call(bd_ctx* ctx, bool check_err, int n_err) {
     return 0;
 }
 
+// Opt in to more than the default 48 KB when dynamic + static shared memory exceed it.
 template <class K>
 void raise_smem(K kernel, size_t bytes) {
-    if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (bytes <= 36 * 1024) return;          // every kernel here has < 12 KB of static shared memory
+    cudaFuncAttributes fa{};
+    const size_t stat = cudaFuncGetAttributes(&fa, kernel) == cudaSuccess ? fa.sharedSizeBytes : 0;
+    if (bytes + stat > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
 template <int P, bool CURV, int MT = 0, int NPT = 0, int TPB = 0>

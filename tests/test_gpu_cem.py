@@ -229,3 +229,32 @@ def test_absurd_warm_start_rows_do_not_degrade():
     # iteration 1 holds the absurd rows: the reference's max is huge, the device's +inf
     assert np.isinf(st[0, 5]) and g["cem_stats"][0, 5] > 1e15
     np.testing.assert_allclose(st[1:, 5], g["cem_stats"][1:, 5], rtol=1e-3, atol=1e-3)
+
+
+@pytest.mark.parametrize("B,n,q,seed", [(37, 20, 7, 0), (1000, 150, 100, 1), (4096, 600, 50, 2), (13000, 1024, 64, 3)])
+def test_rank_refit_random_with_ties(B, n, q, seed):
+    """rank_samples + update_distribution (pkg/bilevel.py:129-194) on random keys with many exact
+    ties, against the oracle: constraint-elite and elite sets and order exactly, refit to 1e-12.
+    B = 13000 takes the global (non-shared-memory) counting rank."""
+    from paper_2212_02224_b200._native import ptr
+    g = load("cem_c2")
+    ctx = _solver_c2(g).context
+    rng = np.random.default_rng(seed)
+    r = np.round(rng.exponential(1.0, B), 2)                 # residual ties
+    c = np.round(rng.normal(200.0, 30.0, B), 1)              # augmented-cost ties
+    r[rng.random(B) < 0.05] = 0.0
+    P = np.ascontiguousarray(rng.normal(size=(B, 8)))
+    mean, cov = rng.normal(size=8), np.eye(8) * 2.0 + 0.1
+    m_dev, c_dev = mean.copy(), cov.copy()
+    cons, el, ea, st = np.empty(n, np.int64), np.empty(q, np.int64), np.empty(q), np.empty(6)
+    ctx.call("bd_rank_refit", 1, B, 8, ptr(r), ptr(c), ptr(P), n, q, 1.0, 0.7, 0.9, ptr(m_dev), ptr(c_dev),
+             ptr(cons), ptr(el), ptr(ea), ptr(st))
+    rc, re, ra = O.rank_two_stage(r, c, n, q, 1.0)
+    np.testing.assert_array_equal(cons, rc)
+    np.testing.assert_array_equal(el, re)
+    np.testing.assert_array_equal(ea, ra)
+    mu, C = O.refit_gaussian(mean, cov, P[re], ra, 0.7, 0.9)
+    np.testing.assert_allclose(m_dev, mu, rtol=1e-12, atol=1e-13)
+    np.testing.assert_allclose(c_dev, C, rtol=1e-11, atol=1e-13)
+    np.testing.assert_allclose(st[[3, 4, 5]], [r.min(), np.median(r), r.max()], rtol=0, atol=0)
+    assert st[1] == ra[0]
