@@ -258,3 +258,27 @@ def test_rank_refit_random_with_ties(B, n, q, seed):
     np.testing.assert_allclose(c_dev, C, rtol=1e-11, atol=1e-13)
     np.testing.assert_allclose(st[[3, 4, 5]], [r.min(), np.median(r), r.max()], rtol=0, atol=0)
     assert st[1] == ra[0]
+
+
+@pytest.mark.parametrize("dim,seed", [(4, 10), (10, 11), (16, 12)])
+def test_rank_refit_random_other_dims(dim, seed):
+    """The refit for behaviour vectors of 4 (two segments), 10 (goal layout) and 16 (the maximum)."""
+    from paper_2212_02224_b200._native import ptr
+    g = load("cem_c2")
+    ctx = _solver_c2(g).context
+    rng = np.random.default_rng(seed)
+    B, n, q = 500, 120, 40
+    r = np.round(rng.exponential(1.0, B), 2)
+    c = np.round(rng.normal(200.0, 30.0, B), 1)
+    P = np.ascontiguousarray(rng.normal(size=(B, dim)))
+    A = rng.normal(size=(dim, dim))
+    mean, cov = rng.normal(size=dim), A @ A.T + dim * np.eye(dim)
+    m_dev, c_dev = mean.copy(), cov.copy()
+    cons, el, ea, st = np.empty(n, np.int64), np.empty(q, np.int64), np.empty(q), np.empty(6)
+    ctx.call("bd_rank_refit", 1, B, dim, ptr(r), ptr(c), ptr(P), n, q, 1.0, 0.6, 1.3, ptr(m_dev), ptr(c_dev),
+             ptr(cons), ptr(el), ptr(ea), ptr(st))
+    rc, re, ra = O.rank_two_stage(r, c, n, q, 1.0)
+    np.testing.assert_array_equal(el, re)
+    mu, C = O.refit_gaussian(mean, cov, P[re], ra, 0.6, 1.3)
+    np.testing.assert_allclose(m_dev, mu, rtol=1e-12, atol=1e-13)
+    np.testing.assert_allclose(c_dev, C, rtol=1e-11, atol=1e-12)
