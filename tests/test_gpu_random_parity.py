@@ -68,3 +68,6 @@ def test_random_scene_matches_oracle(seed):
     assert rel_err_per_sample_axis(proj.xi, out["xi"]) <= XI_TOL
     assert np.all(np.abs(proj.residuals - out["residuals"]) <= RES_TOL * (1.0 + out["residuals"]))
     assert np.all(np.abs(costs - ref_cost) <= COST_TOL * np.maximum(ref_cost, 1.0))
+    hist = np.asarray(proj.residual_history)                # (iterations, B) per-iteration residuals
+    assert hist.shape == out["history"].shape
+    assert np.all(np.abs(hist - out["history"]) <= RES_TOL * (1.0 + out["history"]))
