@@ -71,3 +71,28 @@ def test_random_scene_matches_oracle(seed):
     hist = np.asarray(proj.residual_history)                # (iterations, B) per-iteration residuals
     assert hist.shape == out["history"].shape
     assert np.all(np.abs(hist - out["history"]) <= RES_TOL * (1.0 + out["history"]))
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_random_goal_layout_matches_oracle(seed):
+    """Goal layout (pkg/batch_qp.py:189-192, 236-238): per-sample b with the terminal rows, the
+    generic stage-1 path, behaviour vectors of 10."""
+    import paper_2212_02224_b200 as bd
+    n_obs, ox, oy, lim, curv, b0, P8 = _random_case(100 + seed)
+    rng = np.random.default_rng(seed)
+    P = np.concatenate([P8, np.stack([rng.uniform(40.0, 90.0, B), rng.uniform(-2.0, 10.0, B)], axis=1)], axis=1)
+    basis = bd.build_basis(10, M, T, "bernstein")
+    solver = bd.LowerLevelSolver(basis, bd.TrackingWeights(), bd.ParamLayout(4, with_goal=True),
+                                 bd.ProjectionConfig(1.0, ITERS, 1e-30), n_obs)
+    spec = bd.ConstraintSpec(ox, oy, lim["a"], lim["b"], lim["v_max"], lim["a_max"], lim["kappa_max"], lim["c_max"],
+                             lim["y_lb"], lim["y_ub"], lim["v_min"], curv)
+    _, proj = solver.solve(P, bd.PlanningScene(b0, spec))
+    _, W, Wd, Wdd = O.basis_matrices(10, M, T)
+    qp = O.tracking_qp(W, Wd, Wdd, 4, True)
+    ol = O.Limits(ox.reshape(n_obs, M), oy.reshape(n_obs, M), lim["a"], lim["b"], lim["v_max"], lim["a_max"],
+                  lim["kappa_max"], lim["c_max"], lim["y_lb"], lim["y_ub"], lim["v_min"], curv)
+    xb, _, bb = O.stage1(qp, P, b0)
+    aug = O.aug_qp(W, Wd, Wdd, qp.A_eq, n_obs, 1.0)
+    out = O.am_project(aug, W, Wd, Wdd, xb, bb, ol, 1.0, ITERS, 1e-30)
+    assert rel_err_per_sample_axis(proj.xi, out["xi"]) <= XI_TOL
+    assert np.all(np.abs(proj.residuals - out["residuals"]) <= RES_TOL * (1.0 + out["residuals"]))
