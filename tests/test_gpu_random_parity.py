@@ -15,11 +15,11 @@ XI_TOL, COST_TOL, RES_TOL = 1e-4, 1e-4, 1e-3
 M, T, B, ITERS = 100, 5.0, 24, 40
 
 
-def _random_case(seed):
+def _random_case(seed, m=M, horizon=T, n_obs=None):
     rng = np.random.default_rng(seed)
-    n_obs = [0, 3, 10, 20, 50][seed % 5]
+    n_obs = [0, 3, 10, 20, 50][seed % 5] if n_obs is None else n_obs
     lanes = int(rng.integers(2, 5))
-    t = np.linspace(0.0, T, M)
+    t = np.linspace(0.0, horizon, m)
     x0 = rng.uniform(10.0, 160.0, n_obs)
     vx = np.where(rng.random(n_obs) < 0.3, 0.0, rng.uniform(4.0, 18.0, n_obs))
     lane = rng.integers(0, lanes, n_obs) * 4.0
@@ -91,6 +91,30 @@ def test_random_goal_layout_matches_oracle(seed):
     qp = O.tracking_qp(W, Wd, Wdd, 4, True)
     ol = O.Limits(ox.reshape(n_obs, M), oy.reshape(n_obs, M), lim["a"], lim["b"], lim["v_max"], lim["a_max"],
                   lim["kappa_max"], lim["c_max"], lim["y_lb"], lim["y_ub"], lim["v_min"], curv)
+    xb, _, bb = O.stage1(qp, P, b0)
+    aug = O.aug_qp(W, Wd, Wdd, qp.A_eq, n_obs, 1.0)
+    out = O.am_project(aug, W, Wd, Wdd, xb, bb, ol, 1.0, ITERS, 1e-30)
+    assert rel_err_per_sample_axis(proj.xi, out["xi"]) <= XI_TOL
+    assert np.all(np.abs(proj.residuals - out["residuals"]) <= RES_TOL * (1.0 + out["residuals"]))
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_random_planner_default_shape_matches_oracle(seed):
+    """The reference planner's default shape (PlannerEnvConfig: m = 50 over 10 s, 6 obstacles),
+    which runs on its own compile-time specialisation of the AM kernel."""
+    import paper_2212_02224_b200 as bd
+    m, horizon = 50, 10.0
+    n_obs, ox, oy, lim, curv, b0, P = _random_case(200 + seed, m, horizon, n_obs=6)
+    basis = bd.build_basis(10, m, horizon, "bernstein")
+    solver = bd.LowerLevelSolver(basis, bd.TrackingWeights(), bd.ParamLayout(4),
+                                 bd.ProjectionConfig(1.0, ITERS, 1e-30), n_obs)
+    spec = bd.ConstraintSpec(ox, oy, lim["a"], lim["b"], lim["v_max"], lim["a_max"], lim["kappa_max"], lim["c_max"],
+                             lim["y_lb"], lim["y_ub"], lim["v_min"], None)
+    _, proj = solver.solve(P, bd.PlanningScene(b0, spec))
+    _, W, Wd, Wdd = O.basis_matrices(10, m, horizon)
+    qp = O.tracking_qp(W, Wd, Wdd, 4)
+    ol = O.Limits(ox, oy, lim["a"], lim["b"], lim["v_max"], lim["a_max"], lim["kappa_max"], lim["c_max"],
+                  lim["y_lb"], lim["y_ub"], lim["v_min"], None)
     xb, _, bb = O.stage1(qp, P, b0)
     aug = O.aug_qp(W, Wd, Wdd, qp.A_eq, n_obs, 1.0)
     out = O.am_project(aug, W, Wd, Wdd, xb, bb, ol, 1.0, ITERS, 1e-30)
