@@ -413,7 +413,7 @@ __device__ __forceinline__ void pair_sync() {
 #define BD_AM_MINB 2       // x 256 threads: 128 registers per thread
 #endif
 template <int P, bool CURV, int MT = 0, int NPT = 0, int TPB = 0>
-__global__ void __launch_bounds__(256, BD_AM_MINB) am_kernel(const AmArgs a) {
+__global__ void __launch_bounds__(TPB > 256 ? TPB : 256, TPB > 256 ? 1 : BD_AM_MINB) am_kernel(const AmArgs a) {
     // P <= 32: a sample is a group of P lanes of one warp.  P == 64: a sample spans two warps
     // (latency mapping for small batches); each warp reduce-scatters its partial sums, the second
     // warp hands them to the first through shared memory and the first warp owns the update.

@@ -390,6 +390,16 @@ int dispatch_am(bd_ctx* ctx, AmArgs a, int P, int threads, bool replay_pass, int
             return launch_am_t<PP, false, 100, 25, (PP == 32 ? 64 : 128)>(ctx, a, threads, replay_pass, occ); \
         return curv ? launch_am_t<PP, true>(ctx, a, threads, replay_pass, occ)                               \
                     : launch_am_t<PP, false>(ctx, a, threads, replay_pass, occ);
+    // single-scene latency shape: one CTA of 5-8 two-warp samples per SM (see default_threads)
+    if (P == 64 && !curv && a.m == 100 && a.n_obs == 10 && threads > 256) {
+        switch (threads) {
+            case 320: return launch_am_t<64, false, 100, 5, 320>(ctx, a, threads, replay_pass, occ);
+            case 384: return launch_am_t<64, false, 100, 5, 384>(ctx, a, threads, replay_pass, occ);
+            case 448: return launch_am_t<64, false, 100, 5, 448>(ctx, a, threads, replay_pass, occ);
+            case 512: return launch_am_t<64, false, 100, 5, 512>(ctx, a, threads, replay_pass, occ);
+            default: return fail(ctx, BD_ERR_VALUE, "unsupported CTA size %d", threads);
+        }
+    }
     switch (P) {
         AM_CASE(4)
         AM_CASE(8)
@@ -401,9 +411,18 @@ int dispatch_am(bd_ctx* ctx, AmArgs a, int P, int threads, bool replay_pass, int
 #undef AM_CASE
 }
 
-int default_threads(bd_ctx* ctx, int P) {
+int default_threads(bd_ctx* ctx, int P, const AmArgs& a) {
     int threads = ctx->opt_spc ? ctx->opt_spc * P : (P == 32 ? 64 : 128);
     if (P == 64 && threads % 64) threads = 128;
+    if (P == 64 && !ctx->opt_spc && a.n_curv == 0 && a.m == 100 && a.n_obs == 10) {
+        // two-warp mapping on the BASELINE shape: give every SM one CTA of ceil(samples / SMs)
+        // samples when that is 5-8, instead of 3-4 two-sample CTAs whose count differs by one
+        // between SMs (B = 1000: 0.257 -> 0.246 ms per AM launch)
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+        const long long per_sm = ((long long)a.B * ctx->S + sms - 1) / sms;
+        if (per_sm >= 5 && per_sm <= 8) threads = 64 * (int)per_sm;
+    }
     return threads;
 }
 
@@ -423,7 +442,7 @@ int pick_lanes(bd_ctx* ctx, const AmArgs& a) {
     double best_cost = 1e300;
     for (int i = 0; i < 4; ++i) {
         const int P = cands[i];
-        const int threads = default_threads(ctx, P);
+        const int threads = default_threads(ctx, P, a);
         int occ = 0;
         if (dispatch_am(ctx, a, P, threads, false, &occ) != 0 || occ <= 0) continue;
         const double slots = (double)occ * sms * (threads / 32);
@@ -437,8 +456,9 @@ int pick_lanes(bd_ctx* ctx, const AmArgs& a) {
 
 int launch_am(bd_ctx* ctx, AmArgs a, bool replay_pass) {
     const int P = pick_lanes(ctx, a);
-    const int threads = default_threads(ctx, P);
-    if (threads % 32 || threads > 256 || threads < 32) return fail(ctx, BD_ERR_VALUE, "bad samples_per_cta");
+    const int threads = default_threads(ctx, P, a);
+    if (threads % 32 || threads > 512 || threads < 32 || (threads > 256 && P != 64))
+        return fail(ctx, BD_ERR_VALUE, "bad samples_per_cta");
     return dispatch_am(ctx, a, P, threads, replay_pass, nullptr);
 }
 
