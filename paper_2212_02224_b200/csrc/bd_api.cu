@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <unordered_map>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -326,12 +327,24 @@ int finish_call(bd_ctx* ctx, bool check_err, int n_err) {
 }
 
 // Opt in to more than the default 48 KB when dynamic + static shared memory exceed it.
+// Per kernel and device: its static shared memory and the dynamic size it was opted in to (the
+// driver calls are made once per kernel, device and size, not per launch).
 template <class K>
 void raise_smem(K kernel, size_t bytes) {
     if (bytes <= 36 * 1024) return;          // every kernel here has < 12 KB of static shared memory
-    cudaFuncAttributes fa{};
-    const size_t stat = cudaFuncGetAttributes(&fa, kernel) == cudaSuccess ? fa.sharedSizeBytes : 0;
-    if (bytes + stat > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    struct Seen { size_t stat = 0, raised = 0; bool known = false; };
+    thread_local std::unordered_map<uintptr_t, Seen> seen;    // keyed by (kernel, device)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    Seen& e = seen[reinterpret_cast<uintptr_t>(reinterpret_cast<const void*>(kernel)) * 64 + (uintptr_t)dev];
+    if (!e.known) {
+        cudaFuncAttributes fa{};
+        e.stat = cudaFuncGetAttributes(&fa, kernel) == cudaSuccess ? fa.sharedSizeBytes : 0;
+        e.known = true;
+    }
+    if (bytes + e.stat > 48 * 1024 && bytes > e.raised &&
+        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) == cudaSuccess)
+        e.raised = bytes;
 }
 
 template <int P, bool CURV, int MT = 0, int NPT = 0, int TPB = 0>
