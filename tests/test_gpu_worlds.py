@@ -37,6 +37,23 @@ def test_build_scene_and_observe_match_reference(k):
     np.testing.assert_allclose(obs[0], g[f"w{k}_obs"], rtol=1e-13, atol=1e-13)
 
 
+@pytest.mark.parametrize("k", range(24))
+def test_build_scene_randomised_worlds_match_reference(k):
+    """24 randomised worlds (2-5 lanes, 0-90 vehicles, 0-40 simulator steps, 1-50 obstacle rows,
+    30-300 m range; tests/golden/worlds_random.npz from the reference) through the device builder."""
+    from paper_2212_02224_b200.worlds import PlannerEnv, build_scenes
+    g = load("worlds_random")
+    nobs, rng_, wb = g[f"w{k}_env"]
+    solver = _solver(int(nobs))
+    env = PlannerEnv(max_obstacles=int(nobs), obstacle_range=float(rng_), wheelbase=float(wb))
+    ox, oy, b0, lim, obs = build_scenes(solver.context, solver.basis, _world(g, k), env, outputs=True)
+    np.testing.assert_array_equal(ox[0], g[f"w{k}_ox"])
+    np.testing.assert_array_equal(oy[0], g[f"w{k}_oy"])
+    np.testing.assert_allclose(b0[0], g[f"w{k}_b0"], rtol=1e-14, atol=1e-14)
+    np.testing.assert_array_equal(lim[0], g[f"w{k}_lim"])
+    np.testing.assert_allclose(obs[0], g[f"w{k}_obs"], rtol=1e-13, atol=1e-13)
+
+
 def test_device_built_scene_drives_the_solver():
     """Scenes built on the device give the same projection as the host-uploaded reference scene."""
     import paper_2212_02224_b200 as bd

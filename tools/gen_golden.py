@@ -609,6 +609,41 @@ def gen_absurd():
     print(f"absurd written: lower resid {proj.residuals[[3, 7, 9, 10]]}, cem best {res.best.index}")
 
 
+def gen_worlds_random():
+    """24 randomised worlds (lanes, density, vehicle count incl. none, simulator steps, obstacle
+    count and range) with the reference's build_scene / ego_flat_state / observe outputs."""
+    from bilevel_drive.highway import observe, step
+    rng = np.random.default_rng(2026)
+    out = {}
+    n = 24
+    for k in range(n):
+        lanes = int(rng.integers(2, 6))
+        dens = float(rng.uniform(0.3, 3.5))
+        veh = int(rng.choice([0, 1, 2, 5, 12, 24, 40, 80, 90]))
+        seed = int(rng.integers(0, 10_000))
+        nsteps = int(rng.integers(0, 40))
+        nobs = int(rng.choice([1, 6, 10, 25, 50]))
+        rng_ = float(rng.uniform(30.0, 300.0))
+        world = spawn_world(ScenarioConfig(RoadSpec(lane_count=lanes), density=dens, vehicle_count=veh, seed=seed))
+        for t in range(nsteps):
+            step(world, 1.2 * np.sin(0.37 * t + k), 0.05 * np.cos(0.23 * t + k))
+        env = env_for(n_obs=nobs, obstacle_range=rng_)
+        basis = build_basis(10, 100, 5.0, "bernstein")
+        sc = build_scene(world, env, basis.times)
+        e = world.ego
+        out[f"w{k}_ego"] = np.array([e.x, e.y, e.psi, e.v, e.accel, e.steer, e.length, e.width])
+        out[f"w{k}_veh"] = np.array([[v.x, v.y, v.psi, v.v, v.lateral_rate] for v in world.neighbors]).reshape(-1, 5)
+        out[f"w{k}_road"] = np.array([world.road.lane_count, world.road.lane_width])
+        out[f"w{k}_env"] = np.array([nobs, rng_, env.wheelbase])
+        out[f"w{k}_ox"], out[f"w{k}_oy"] = sc.spec.obstacles_x, sc.spec.obstacles_y
+        out[f"w{k}_b0"] = sc.initial_state
+        out[f"w{k}_lim"] = scene_arrays(sc)["limits"]
+        out[f"w{k}_obs"] = observe(world)
+    out["n_worlds"] = n
+    np.savez_compressed(os.path.join(OUT, "worlds_random.npz"), **out)
+    print(f"worlds_random written ({n} worlds)")
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", nargs="*", default=None)
@@ -616,7 +651,7 @@ if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
     jobs = {"basis": gen_basis, "lower": gen_lower, "scenes": gen_scenes, "cem_small": gen_cem_small,
             "cem_c2": gen_cem_c2, "worlds": gen_worlds, "sim": gen_sim, "episodes": gen_episodes, "cem_variants": gen_cem_variants, "planners": gen_planners,
-            "harness": gen_harness, "absurd": gen_absurd}
+            "harness": gen_harness, "absurd": gen_absurd, "worlds_random": gen_worlds_random}
     for name, fn in jobs.items():
         if a.only is None or name in a.only:
             fn()
