@@ -89,6 +89,20 @@ def test_control_emission_matches_reference():
     np.testing.assert_allclose(ste[ok], g["ctrl_steer"][ok], rtol=1e-10, atol=1e-12)
 
 
+def test_control_emission_randomised_trajectories():
+    """96 randomised trajectories (incl. stopping / reversing ones that hit SpeedSingularity)
+    against the reference's flat_to_controls (tests/golden/worlds_random.npz)."""
+    from paper_2212_02224_b200.worlds import ControlEmitter, PlannerEnv
+    g = load("worlds_random")
+    solver = _solver(10)
+    em = ControlEmitter(solver.context, solver.basis, 5.0, 0.1, PlannerEnv())
+    acc, ste, sing = em.emit(g["ctrl_xi"])
+    np.testing.assert_array_equal(sing, g["ctrl_singular"].astype(bool))
+    ok = ~sing
+    np.testing.assert_allclose(acc[ok], g["ctrl_accel"][ok], rtol=1e-10, atol=1e-10)
+    np.testing.assert_allclose(ste[ok], g["ctrl_steer"][ok], rtol=1e-10, atol=1e-12)
+
+
 def test_fleet_plan_cycle_from_worlds():
     import paper_2212_02224_b200 as bd
     from paper_2212_02224_b200.fleet import FleetPlanner

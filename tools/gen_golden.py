@@ -640,6 +640,32 @@ def gen_worlds_random():
         out[f"w{k}_lim"] = scene_arrays(sc)["limits"]
         out[f"w{k}_obs"] = observe(world)
     out["n_worlds"] = n
+    # control emission (flat_to_controls on the 0.1 s grid) of 96 randomised trajectories:
+    # forward motion at 0-25 m/s with lateral wiggles, some stopping or reversing (singular)
+    from bilevel_drive.basis import SpeedSingularity, TrajectoryCoeffs, flat_to_controls
+    basis = build_basis(10, 100, 5.0, "bernstein")
+    times = np.arange(int(5.0 / 0.1)) * 0.1
+    env = env_for()
+    u = np.linspace(0.0, 1.0, 11)
+    xis, acc, ste, sing = [], [], [], []
+    for j in range(96):
+        v = rng.uniform(-3.0, 25.0) if j % 8 else rng.uniform(-0.5, 0.5)
+        cx = v * 5.0 * u + rng.normal(0.0, 1.0 + 0.2 * abs(v), 11) * (u * (1 - u) * 4)
+        cy = rng.uniform(-2.0, 10.0) + rng.normal(0.0, 1.5, 11)
+        if j % 16 == 0:                              # standing still: SpeedSingularity
+            cx, cy = np.full(11, cx[0]), np.full(11, cy[0])
+        xi = np.concatenate([cx, cy])
+        xis.append(xi)
+        try:
+            c = flat_to_controls(basis, TrajectoryCoeffs.from_stacked(xi), env.wheelbase, times=times)
+            acc.append(np.clip(c.accel, -env.a_max, env.a_max))
+            ste.append(np.clip(c.delta, -env.steer_limit, env.steer_limit))
+            sing.append(0)
+        except SpeedSingularity:
+            acc.append(np.full(len(times), np.nan))
+            ste.append(np.full(len(times), np.nan))
+            sing.append(1)
+    out.update(ctrl_xi=np.array(xis), ctrl_accel=np.array(acc), ctrl_steer=np.array(ste), ctrl_singular=np.array(sing))
     np.savez_compressed(os.path.join(OUT, "worlds_random.npz"), **out)
     print(f"worlds_random written ({n} worlds)")
 
