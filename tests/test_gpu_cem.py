@@ -282,3 +282,47 @@ def test_rank_refit_random_other_dims(dim, seed):
     mu, C = O.refit_gaussian(mean, cov, P[re], ra, 0.6, 1.3)
     np.testing.assert_allclose(m_dev, mu, rtol=1e-12, atol=1e-13)
     np.testing.assert_allclose(c_dev, C, rtol=1e-11, atol=1e-12)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_random_teacher_forced_cem_matches_oracle(seed):
+    """Teacher-forced CEM on randomised scenes (tests/test_gpu_random_parity.py's generator):
+    every iteration the device solves the oracle's samples; residuals and costs within the §8c
+    tolerances, constraint-elite and elite sets exact outside the residual tie band, refit mean
+    to 1e-4 when the sets agree."""
+    import paper_2212_02224_b200 as bd
+    from paper_2212_02224_b200._native import ptr
+    from tests.test_gpu_random_parity import M, T, _random_case
+    n_obs, ox, oy, lim, curv, b0, _ = _random_case(300 + seed, n_obs=10)
+    B, n, q, N, am = 300, 90, 30, 3, 40
+    _, W, Wd, Wdd = O.basis_matrices(10, M, T)
+    qp = O.tracking_qp(W, Wd, Wdd, 4)
+    aug = O.aug_qp(W, Wd, Wdd, qp.A_eq, n_obs, 1.0)
+    ol = O.Limits(ox, oy, lim["a"], lim["b"], lim["v_max"], lim["a_max"], lim["kappa_max"], lim["c_max"],
+                  lim["y_lb"], lim["y_ub"], lim["v_min"], curv)
+    mean0 = np.concatenate([np.full(4, b0[1]), np.full(4, np.hypot(b0[2], b0[3]))])
+    cov0 = np.diag(np.concatenate([np.full(4, 1.5 ** 2), np.full(4, 3.0 ** 2)]))
+    tr = O.cem_cycle(qp, aug, W, Wd, Wdd, b0, ol, mean0, cov0, batch=B, n_cons=n, n_elite=q, iters=N, eta=0.7,
+                     gamma=0.9, w_res=1.0, rng=np.random.default_rng(seed), am_iters=am, tol=1e-30)
+    basis = bd.build_basis(10, M, T, "bernstein")
+    solver = bd.LowerLevelSolver(basis, bd.TrackingWeights(), bd.ParamLayout(4), bd.ProjectionConfig(1.0, am, 1e-30),
+                                 n_obs)
+    spec = bd.ConstraintSpec(ox, oy, lim["a"], lim["b"], lim["v_max"], lim["a_max"], lim["kappa_max"], lim["c_max"],
+                             lim["y_lb"], lim["y_ub"], lim["v_min"], curv)
+    scene = bd.PlanningScene(b0, spec)
+    mean, cov = mean0, cov0
+    for it in range(N):
+        P = np.ascontiguousarray(tr.params[it])
+        _, proj = solver.solve(P, scene)
+        r, c = np.asarray(proj.residuals), np.asarray(solver.last_costs)
+        assert np.all(np.abs(r - tr.residuals[it]) <= RES_TOL * (1.0 + tr.residuals[it]))
+        assert np.all(np.abs(c - tr.costs[it]) <= COST_TOL * np.maximum(tr.costs[it], 1.0))
+        m_dev, c_dev = mean.copy(), cov.copy()
+        cons, el, ea, st = np.empty(n, np.int64), np.empty(q, np.int64), np.empty(q), np.empty(6)
+        solver.context.call("bd_rank_refit", 1, B, 8, ptr(np.ascontiguousarray(r)), ptr(np.ascontiguousarray(c)),
+                            ptr(P), n, q, 1.0, 0.7, 0.9, ptr(m_dev), ptr(c_dev), ptr(cons), ptr(el), ptr(ea), ptr(st))
+        ok, diff = band_ok(cons, tr.cons_idx[it], tr.residuals[it], n)
+        assert ok, f"iteration {it}: constraint elites differ outside the tie band: {sorted(diff)}"
+        if not diff and set(el.tolist()) == set(tr.elite_idx[it].tolist()):
+            np.testing.assert_allclose(m_dev, tr.mean[it], rtol=1e-4, atol=1e-6)
+        mean, cov = tr.mean[it], tr.cov[it]                   # teacher forcing: continue from the oracle
