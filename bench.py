@@ -145,7 +145,7 @@ def make_planner(device: int):
                         N_OBS, cfg, device=device)
 
 
-def cem_latency(device: int, cycles: int = 30):
+def cem_latency(device: int, cycles: int = 120):
     """Single-scene config-2 cycle through the public drop-in solve_bilevel (host numpy in/out)."""
     import paper_2212_02224_b200 as bd
     from paper_2212_02224_b200.fleet import initial_distribution
@@ -184,7 +184,7 @@ def cem_latency(device: int, cycles: int = 30):
                            "api": "FleetPlanner.plan (device Philox draws), host call to host-visible results"}}
 
 
-def cvae_config3(device: int, cycles: int = 20):
+def cvae_config3(device: int, cycles: int = 120):
     """BASELINE config 3: CVAE decoder draws 1000 set-points from a scene embedding (the 55-entry
     observation), which warm-start iteration 1 of the config-2 CEM cycle; p50 of decode + cycle
     through the public API (tcgen05 decoder, synthetic seeded weights: the reference ships none)."""
