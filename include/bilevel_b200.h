@@ -212,6 +212,12 @@ int bd_cem_cycle(bd_ctx* ctx, int n_scenes, const bd_cem_config* cfg, const doub
                  double* best_params, double* best_xi, double* best_cost, double* best_residual,
                  double* best_aug, double* stats, double* final_mean, double* final_cov, int* iterations_done);
 
+/* The last CEM iteration's batch of the preceding bd_cem_cycle on this context (the arguments of the
+ * reference's trace_hook, pkg/bilevel.py:269-270): set-points S x B x dim, projected coefficients
+ * S x B x 2n, residuals S x B, upper costs S x B (each may be NULL). */
+int bd_cem_last_batch(bd_ctx* ctx, int n_scenes, int batch, double* params, double* xi, double* residuals,
+                      double* cost);
+
 /* ------------------------------------------------------------------ scene construction / control emission
  * the steps either side of the path, on the device.                          */
 

@@ -53,6 +53,7 @@ SIGNATURES = {
     "bd_rank_refit": (c_int, [_P, c_int, c_int, c_int, _P, _P, _P, c_int, c_int, c_double, c_double, c_double, _P, _P,
                               _P, _P, _P, _P]),
     "bd_cem_cycle": (c_int, [_P, c_int, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "bd_cem_last_batch": (c_int, [_P, c_int, c_int, _P, _P, _P, _P]),
     "bd_build_scenes": (c_int, [_P, c_int, c_int, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "bd_set_curvature": (c_int, [_P, c_int, c_int, _P, _P]),
     "bd_set_control_grid": (c_int, [_P, c_int, _P, _P, c_double, c_double, c_double, c_double]),

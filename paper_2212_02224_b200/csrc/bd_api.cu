@@ -111,6 +111,8 @@ struct bd_ctx {
     std::vector<DevBuf*> cvae_w, cvae_b, cvae_w16;
     DevBuf cvae_h0, cvae_h1, cvae_obs, cvae_z, cvae_a0, cvae_a1;
     int cvae_tc = 1;            // option "cvae_tensor_cores": bf16 tcgen05 hidden layers (1) or fp32 SIMT (0)
+    bool err_sticky = false;    // option "sticky_errors": entry points accumulate into the error word
+                                // instead of clearing it (multi-call loops read it once at the end)
     ~bd_ctx() {
         for (auto& e : ev_used) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
         for (auto& e : ev_free) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
@@ -238,6 +240,12 @@ int stage_inout(bd_ctx* ctx, T* user, size_t count, DevBuf& ws, T** out) {
     return 0;
 }
 
+// Clear the per-scene error word at the start of a call, unless the caller asked for sticky errors.
+cudaError_t clear_err(bd_ctx* ctx, size_t bytes) {
+    if (ctx->err_sticky) return cudaSuccess;
+    return cudaMemsetAsync(ctx->w_err.p, 0, bytes, ctx->stream);
+}
+
 void begin_call(bd_ctx* ctx) {
     ctx->n_stage = 0;
     ctx->pending.clear();
@@ -331,7 +339,6 @@ int finish_call(bd_ctx* ctx, bool check_err, int n_err) {
 // driver calls are made once per kernel, device and size, not per launch).
 template <class K>
 void raise_smem(K kernel, size_t bytes) {
-    if (bytes <= 36 * 1024) return;          // every kernel here has < 12 KB of static shared memory
     struct Seen { size_t stat = 0, raised = 0; bool known = false; };
     thread_local std::unordered_map<uintptr_t, Seen> seen;    // keyed by (kernel, device)
     int dev = 0;
@@ -470,8 +477,11 @@ int pick_lanes(bd_ctx* ctx, const AmArgs& a) {
 int launch_am(bd_ctx* ctx, AmArgs a, bool replay_pass) {
     const int P = pick_lanes(ctx, a);
     const int threads = default_threads(ctx, P, a);
-    if (threads % 32 || threads > 512 || threads < 32 || (threads > 256 && P != 64))
-        return fail(ctx, BD_ERR_VALUE, "bad samples_per_cta");
+    // > 256 threads only for the latency-shape instances (dispatch_am: P = 64, m = 100, 10 obstacles)
+    const bool big_ok = P == 64 && a.n_curv == 0 && a.m == 100 && a.n_obs == 10;
+    if (threads % 32 || threads > 512 || threads < 32 || (threads > 256 && !big_ok))
+        return fail(ctx, BD_ERR_VALUE, "bad samples_per_cta (more than 256 threads only for the 10-obstacle "
+                    "m=100 two-warp mapping)");
     return dispatch_am(ctx, a, P, threads, replay_pass, nullptr);
 }
 
@@ -641,6 +651,12 @@ int bd_set_option(bd_ctx* ctx, const char* key, int value) {
     }
     if (!strcmp(key, "timing")) {
         ctx->timing = value != 0;
+        return 0;
+    }
+    if (!strcmp(key, "sticky_errors")) {      // set (1) or leave (0) sticky mode; both reset the word
+        cudaSetDevice(ctx->device);
+        if (ctx->w_err.p) CU(cudaMemsetAsync(ctx->w_err.p, 0, ctx->w_err.bytes, ctx->stream));
+        ctx->err_sticky = value != 0;
         return 0;
     }
     if (!strcmp(key, "samples_per_cta")) {
@@ -923,7 +939,7 @@ int bd_stage1(bd_ctx* ctx, int S, int B, const double* params, double* xi_bar, d
     if ((rc = stage_out(ctx, xi_bar, tot * NX, ctx->w_xibar, &dx))) return rc;
     if ((rc = stage_out(ctx, mu, tot * ctx->neq1, ctx->w_mu, &dm))) return rc;
     if ((rc = stage_out(ctx, b_out, tot * ctx->neq1, ctx->w_b, &db))) return rc;
-    CU(cudaMemsetAsync(ctx->w_err.p, 0, (size_t)S * 4, ctx->stream));
+    CU(clear_err(ctx, (size_t)S * 4));
     if ((rc = run_stage1(ctx, B, dp, dx, dm, db))) return rc;
     return finish_call(ctx, ctx->host_out, S);
 }
@@ -952,7 +968,7 @@ int bd_project(bd_ctx* ctx, int S, int B, const double* xi_bar, const double* b,
     if ((rc = stage_out_req(ctx, iters_used, (size_t)S, ctx->w_iters, &dit))) return rc;
     if ((rc = stage_out_req(ctx, reinterpret_cast<unsigned long long*>(conflicts), (size_t)S, ctx->w_conf, &dconf)))
         return rc;
-    CU(cudaMemsetAsync(ctx->w_err.p, 0, (size_t)S * 4, ctx->stream));
+    CU(clear_err(ctx, (size_t)S * 4));
     if ((rc = run_projection(ctx, B, dxb, dbb, iters, tol, dxi, dres, dcost, dh, dit, dconf))) return rc;
     return finish_call(ctx, ctx->host_out, S);
 }
@@ -987,7 +1003,7 @@ int bd_solve_lower(bd_ctx* ctx, int S, int B, const double* params, int iters, d
         CU(ctx->w_b.ensure(tot * ctx->neq * 8));
         db = ctx->w_b.as<double>();
     }
-    CU(cudaMemsetAsync(ctx->w_err.p, 0, (size_t)S * 4, ctx->stream));
+    CU(clear_err(ctx, (size_t)S * 4));
     if ((rc = run_stage1(ctx, B, dp, dxb, dmu, db))) return rc;
     if ((rc = run_projection(ctx, B, dxb, db, iters, tol, dxi, dres, dcost, dh, dit, dconf))) return rc;
     return finish_call(ctx, ctx->host_out, S);
@@ -1058,7 +1074,7 @@ int bd_solve_lower_shard(bd_ctx* ctx, int B, const double* params, int iters, do
     if ((rc = stage_out(ctx, iter_max, (size_t)iters, ctx->stage[7], &dmax))) return rc;
     CU(ctx->w_iters.ensure(4));
     CU(ctx->w_conf.ensure(8));
-    CU(cudaMemsetAsync(ctx->w_err.p, 0, 4, ctx->stream));
+    CU(clear_err(ctx, 4));
     if ((rc = run_stage1(ctx, B, dp, dxb, nullptr, nullptr))) return rc;
     if ((rc = run_projection(ctx, B, dxb, nullptr, iters, 1.0, dxi, dres, dcost, nullptr, ctx->w_iters.as<int>(),
                              ctx->w_conf.as<unsigned long long>(), true)))
@@ -1084,7 +1100,7 @@ int bd_replay_shard(bd_ctx* ctx, int B, const double* xi_bar, int iters, double*
     if ((rc = ensure_itmax(ctx, (size_t)iters * ITMAX_SLOTS * 4))) return rc;
     CU(ctx->w_replay.ensure(4));
     CU(ctx->w_conf.ensure(8));
-    CU(cudaMemsetAsync(ctx->w_err.p, 0, 4, ctx->stream));
+    CU(clear_err(ctx, 4));
     CU(cudaMemcpyAsync(ctx->w_replay.p, &iters, 4, cudaMemcpyHostToDevice, ctx->stream));
     AmArgs a = projection_args(ctx, B, dxb, iters, dxi, dres, dcost);
     if ((rc = launch_am(ctx, a, true))) return rc;
@@ -1155,7 +1171,7 @@ int bd_solve_lower_shard_p2p(bd_ctx* ctx, int B, const double* params, int iters
     CU(ctx->stage[7].ensure((size_t)iters * 4));
     P2PArgs pa = ctx->p2p;
     pa.err = ctx->w_err.as<int>();
-    CU(cudaMemsetAsync(ctx->w_err.p, 0, 4, ctx->stream));
+    CU(clear_err(ctx, 4));
     if ((rc = run_stage1(ctx, B, dp, dxb, nullptr, nullptr))) return rc;
     ctx->p2p_epilogue = true;                 // AM epilogues store (res, cost) into every rank's buffer
     ctx->p2p_row0 = row0;
@@ -1238,7 +1254,7 @@ int bd_kkt_solve(bd_ctx* ctx, int nvar, int neq, const double* kkt, const double
     if ((rc = stage_in(ctx, rhs, (size_t)count * nr, &dr))) return rc;
     if ((rc = stage_out(ctx, sol, (size_t)count * nr, ctx->w_xibar, &ds))) return rc;
     CU(ctx->w_err.ensure(4 * (size_t)(ctx->S > 1 ? ctx->S : 1)));
-    CU(cudaMemsetAsync(ctx->w_err.p, 0, 4, ctx->stream));
+    CU(clear_err(ctx, 4));
     S1Args s{};
     s.total = count; s.B = count; s.nr = nr; s.nvar = nvar; s.neq = neq;
     s.kkt = dk; s.kinv = dki; s.rhs_in = dr; s.sol_out = ds; s.err = ctx->w_err.as<int>();
@@ -1298,7 +1314,7 @@ int bd_rank_refit(bd_ctx* ctx, int S, int B, int dim, const double* resid, const
     CU(ctx->w_xi.ensure(tot * NX * 8));
     CU(cudaMemcpyAsync(ctx->c_mean.p, mean, (size_t)S * dim * 8, cudaMemcpyDefault, ctx->stream));
     CU(cudaMemcpyAsync(ctx->c_cov.p, cov, (size_t)S * dim * dim * 8, cudaMemcpyDefault, ctx->stream));
-    CU(cudaMemsetAsync(ctx->w_err.p, 0, (size_t)S * 4, ctx->stream));
+    CU(clear_err(ctx, (size_t)S * 4));
     CU(cudaMemsetAsync(ctx->c_done.p, 0, (size_t)S * 4, ctx->stream));
     int64_t *dci, *dei;
     double *dea, *dst;
@@ -1450,6 +1466,32 @@ int bd_cem_cycle(bd_ctx* ctx, int S, const bd_cem_config* cfg, const double* ini
     return finish_call(ctx, false, 0);
 }
 
+// The last CEM iteration's batch of the preceding bd_cem_cycle call on this context: the arguments
+// the reference hands its trace_hook(it, params, proj, costs, elite_idx) (pkg/bilevel.py:269-270).
+int bd_cem_last_batch(bd_ctx* ctx, int S, int B, double* params, double* xi, double* residuals, double* cost) {
+    NvtxRange nvtx_("bd_cem_last_batch");
+    if (!ctx) return BD_ERR_VALUE;
+    if (S != ctx->S || B < 1 || !ctx->dim) return fail(ctx, BD_ERR_VALUE, "bad batch (S=%d, B=%d)", S, B);
+    const size_t tot = (size_t)S * B;
+    if (ctx->w_params.bytes < tot * ctx->dim * 8 || ctx->w_xi.bytes < tot * NX * 8 || ctx->w_res.bytes < tot * 8 ||
+        ctx->w_cost.bytes < tot * 8)
+        return fail(ctx, BD_ERR_STATE, "no CEM batch of this size on the context (run bd_cem_cycle first)");
+    begin_call(ctx);
+    struct Out { void* dst; const void* src; size_t bytes; };
+    const Out outs[] = {{params, ctx->w_params.p, tot * ctx->dim * 8}, {xi, ctx->w_xi.p, tot * NX * 8},
+                        {residuals, ctx->w_res.p, tot * 8}, {cost, ctx->w_cost.p, tot * 8}};
+    for (const Out& o : outs)
+        if (o.dst) {
+            if (is_device_ptr(o.dst)) {
+                CU(cudaMemcpyAsync(o.dst, o.src, o.bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+            } else {
+                ctx->pending.push_back({o.dst, o.src, o.bytes});
+                ctx->host_out = true;
+            }
+        }
+    return finish_call(ctx, false, 0);
+}
+
 // ------------------------------------------------------------------ scenes from worlds, controls
 int bd_build_scenes(bd_ctx* ctx, int S, int n_veh_max, const double* ego, const double* veh, const int* n_veh,
                     const double* road, const bd_env* env, const double* times, double* ox_out, double* oy_out,
@@ -1480,7 +1522,7 @@ int bd_build_scenes(bd_ctx* ctx, int S, int n_veh_max, const double* ego, const 
     CU(ctx->ox64.ensure(no ? no * 8 : 8));
     CU(ctx->oy64.ensure(no ? no * 8 : 8));
     CU(ctx->w_err.ensure((size_t)S * 4));
-    CU(cudaMemsetAsync(ctx->w_err.p, 0, (size_t)S * 4, ctx->stream));
+    CU(clear_err(ctx, (size_t)S * 4));
     double *db0, *dobs;
     if ((rc = stage_out(ctx, b0_out, (size_t)S * 6, ctx->stage[6], &db0))) return rc;
     if ((rc = stage_out(ctx, observations, (size_t)S * OBS_DIM, ctx->stage[7], &dobs))) return rc;

@@ -70,20 +70,24 @@ class FleetPlanner:
         self.solver = LowerLevelSolver(basis, weights, layout, proj_config, num_obstacles, device=device)
         self.config = config
         self.layout = layout
-        self._scenes_key = None
+        self._scenes = None            # the scene objects last uploaded (strong references)
 
     @property
     def context(self):
         return self.solver.context
 
     def set_scenes(self, scenes: list[PlanningScene]):
-        key = tuple(id(s) for s in scenes)
-        if key != self._scenes_key:
+        """Upload the scenes unless they are the very objects uploaded last.  Scenes are immutable
+        values; the planner keeps strong references to the uploaded ones, so an
+        identity match cannot come from a recycled id() of a freed scene."""
+        prev = self._scenes
+        stale = self.solver.projector._scene_key is not None      # a single-scene upload since ours
+        if stale or prev is None or len(prev) != len(scenes) or any(a is not b for a, b in zip(prev, scenes)):
             for sc in scenes:
                 self.solver.projector._check_spec(sc.spec)
             upload_scenes(self.context, scenes, self.solver.basis.num_samples)
             self.solver.projector._scene_key = None
-            self._scenes_key = key
+            self._scenes = list(scenes)
 
     def cem_config(self, seed: int, scene_offset: int = 0) -> CemConfig:
         c, p = self.config, self.solver.projector.config
@@ -116,7 +120,7 @@ class FleetPlanner:
         Returns (accels, steers, singular, FleetResult); world arrays in, controls out."""
         from .worlds import build_scenes
         b0 = build_scenes(self.context, self.solver.basis, worlds, env, b0_only=True)
-        self._scenes_key = ("worlds", id(worlds))
+        self._scenes = None              # device scenes now come from the worlds
         self.solver.projector._scene_key = None
         # BasePlanner.initial_distribution (pkg/planners.py:218-231) on the device-built initial
         # states: nearest lane centre to y0, speed = hypot(xdot0, ydot0)

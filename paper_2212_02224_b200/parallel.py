@@ -111,6 +111,8 @@ class ShardedCEM:
         rec = torch.zeros(5, dtype=torch.float64, device=dev)        # index, cost, residual, aug (last iteration)
         xi_best = torch.zeros(22, dtype=torch.float64, device=dev)
         ks = None
+        if hasattr(self.b, "begin"):
+            self.b.begin()                  # device errors accumulate over the loop (read by check())
         for it in range(N):
             P = self.b.sample(mean, cov, self.seed, it, self.B)                 # full batch, every rank
             if self.exchange is not None:
@@ -243,9 +245,20 @@ class CudaShardBackend:
                       shard["residuals"], shard["cost"])
         return shard
 
+    def begin(self):
+        """Sticky error word for the loop: the shard / replay / refit calls OR into it instead of
+        clearing it, so a non-finite iterate, a bad right-hand side or a peer-exchange timeout in
+        any iteration survives to check()."""
+        self.ctx.set_option("sticky_errors", 1)
+
     def check(self):
         """Raise for any device error of the loop (checked once, after it)."""
-        bits = self.ctx.error_bits() if hasattr(self.ctx, "error_bits") else 0
+        bits = self.ctx.error_bits()
+        self.ctx.set_option("sticky_errors", 0)
+        if bits & 16:                       # ERR_P2P_TIMEOUT: a rank never signalled
+            raise RuntimeError(f"sharded CEM: peer exchange timed out (device error bits {bits:#x})")
+        if bits & 4:                        # ERR_BAD_RHS
+            raise ValueError(f"sharded CEM: right-hand sides must be finite (device error bits {bits:#x})")
         if bits:
             from .batch_qp import NumericalFailure
             raise NumericalFailure(f"sharded CEM: device error bits {bits:#x}")
@@ -253,9 +266,11 @@ class CudaShardBackend:
     def rank_refit(self, resid, cost, P, mean, cov, n, q, w, eta, gamma):
         B = resid.shape[0]
         mean, cov = mean.clone(), cov.clone()
-        el = torch.empty(q, dtype=torch.int64, device=self.dev)
-        ea = torch.empty(q, dtype=torch.float64, device=self.dev)
-        st = torch.empty(6, dtype=torch.float64, device=self.dev)
+        # zero-filled: a failed iteration (device error word set) leaves them unwritten, and the loop
+        # still indexes with elite 0 until check() raises after it
+        el = torch.zeros(q, dtype=torch.int64, device=self.dev)
+        ea = torch.zeros(q, dtype=torch.float64, device=self.dev)
+        st = torch.zeros(6, dtype=torch.float64, device=self.dev)
         self.ctx.call("bd_rank_refit", 1, B, self.dim, resid, cost, P.contiguous(), n, q, float(w), float(eta),
                       float(gamma), mean, cov, None, el, ea, st)
         return {"mean": mean, "cov": cov, "elite_idx": el, "elite_aug": ea, "stats": st}

@@ -202,7 +202,7 @@ class BatchMPCBiLevelPlanner(_BatchPlanner):
         self._warm = None
 
     def _invalidate_scene_cache(self):
-        self.fleet._scenes_key = ("sim", self.cycle)
+        self.fleet._scenes = None
         self.fleet.solver.projector._scene_key = None
 
     def reset(self):

@@ -231,11 +231,14 @@ def test_absurd_warm_start_rows_do_not_degrade():
     np.testing.assert_allclose(st[1:, 5], g["cem_stats"][1:, 5], rtol=1e-3, atol=1e-3)
 
 
-@pytest.mark.parametrize("B,n,q,seed", [(37, 20, 7, 0), (1000, 150, 100, 1), (4096, 600, 50, 2), (13000, 1024, 64, 3)])
+@pytest.mark.parametrize("B,n,q,seed", [(37, 20, 7, 0), (1000, 150, 100, 1), (4096, 600, 50, 2), (13000, 1024, 64, 3),
+                                        (2000, 700, 100, 4), (3000, 850, 160, 5)])
 def test_rank_refit_random_with_ties(B, n, q, seed):
     """rank_samples + update_distribution (pkg/bilevel.py:129-194) on random keys with many exact
     ties, against the oracle: constraint-elite and elite sets and order exactly, refit to 1e-12.
-    B = 13000 takes the global (non-shared-memory) counting rank."""
+    B = 13000 takes the global (non-shared-memory) counting rank.  (700, 100) and (850, 160) put
+    the refit kernel's dynamic shared memory in (32 KB, 36 KB], where dynamic + static exceed the
+    default 48 KB (the opt-in must not be skipped there)."""
     from paper_2212_02224_b200._native import ptr
     g = load("cem_c2")
     ctx = _solver_c2(g).context

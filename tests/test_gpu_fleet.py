@@ -117,3 +117,32 @@ def test_sharded_p2p_exchange_world1_equals_nccl_path(tol):
         assert ex.epoch == 6
     finally:
         dist.destroy_process_group()
+
+
+def test_sharded_loop_keeps_device_errors():
+    """The sharded loop's device error word is sticky: a non-finite set-point drawn in
+    CEM iteration 2 is still reported after the loop although the later shard / refit calls of
+    the loop would each have cleared it (pkg/batch_qp.py:105-106 -> ValueError), and the context
+    is usable again afterwards."""
+    import torch
+    from paper_2212_02224_b200.fleet import initial_distribution
+    from paper_2212_02224_b200.parallel import CudaShardBackend, ShardedCEM
+    from paper_2212_02224_b200.scenes import highway_scene
+    fp = _fleet(batch=256, n=64, q=16, N=3, am_iters=20)
+    sc = highway_scene(4)
+    mean, cov = initial_distribution(sc)
+
+    class Inject(CudaShardBackend):
+        def sample(self, mean, cov, seed, it, count):
+            P = super().sample(mean, cov, seed, it, count)
+            if it == 1:
+                P[5, 0] = float("nan")
+            return P
+
+    kw = dict(batch=256, n_cons=64, n_elite=16, iterations=3, eta=0.7, gamma=0.9, residual_weight=1.0, am_iters=20,
+              tol=1e-3, seed=3)
+    with pytest.raises(ValueError, match="finite"):
+        ShardedCEM(Inject(fp.solver, sc), **kw).run(mean, cov)
+    torch.cuda.synchronize()
+    res = ShardedCEM(CudaShardBackend(fp.solver, sc), **kw).run(mean, cov)
+    assert np.isfinite(res.best_cost)

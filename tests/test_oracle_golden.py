@@ -91,6 +91,31 @@ def test_cem_c2_teacher_forced_iteration1():
     np.testing.assert_allclose(tr.mean[0], g["mean"][0], rtol=1e-10)
 
 
+def test_dense_config4_oracle_matches_reference_subset():
+    """Config 4 (tests/golden/dense_c4.npz, B = 10 000 x 50 obstacles run by the reference): the
+    oracle reproduces a subset of the batch (per-sample independent: the reference's shards all
+    ran the full 100 iterations) and the reference's ranking + refit on the whole batch."""
+    g = load("dense_c4")
+    _, W, Wd, Wdd = O.basis_matrices(10, 100, 5.0)
+    qp = O.tracking_qp(W, Wd, Wdd, 4)
+    lim = oracle_limits(g)
+    sub = np.array([0, 1, 2, 3, 990, 4097, 9999])
+    xb, _, b = O.stage1(qp, g["params"][sub], g["b0"])
+    out = O.am_project(O.aug_qp(W, Wd, Wdd, qp.A_eq, 50, 1.0), W, Wd, Wdd, xb, b, lim, 1.0, 100, -1.0)
+    np.testing.assert_allclose(out["residuals"], g["residuals"][sub], rtol=1e-9, atol=1e-9)
+    keep = {int(k): j for j, k in enumerate(g["xi_keep_idx"])}
+    have = [i for i, s in enumerate(sub) if int(s) in keep]
+    assert rel_err_per_sample_axis(out["xi"][:, have], g["xi_keep"][:, [keep[int(sub[i])] for i in have]]) <= 1e-9
+    n, q, w = int(g["cfg"][1]), int(g["cfg"][2]), float(g["cfg"][6])
+    cons, el, ea = O.rank_two_stage(g["residuals"], g["costs"], n, q, w)
+    np.testing.assert_array_equal(cons, g["cons_idx"])
+    np.testing.assert_array_equal(el, g["elite_idx"])
+    mu, C = O.refit_gaussian(g["init_mean"], g["init_cov"], g["params"][el], ea, float(g["cfg"][4]),
+                             float(g["cfg"][5]))
+    np.testing.assert_allclose(mu, g["mean"], rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(C, g["cov"], rtol=1e-12, atol=1e-12)
+
+
 def test_spec_examples():
     # polar identity (SPEC.md:180-182): xdot=3, ydot=4 -> alpha=atan2(4,3), d=5
     _, av, _, _, dv, _ = O.polar_split(np.array([[3.0]]), np.array([[4.0]]), np.zeros((1, 1)), np.zeros((1, 1)))

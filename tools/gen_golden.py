@@ -18,6 +18,9 @@ Cases:
   episodes         run_episode with scripted planners (EpisodeLog JSONL) + suite output files
   cem_variants     solve_bilevel with the goal layout and with a warm-start source
   planners         baseline planners' plan_cycle (vanilla, grid, goal, random) on a few worlds
+  dense_c4         BASELINE config 4 at its stated size: one teacher-forced CEM iteration at B = 10 000
+                   x 50 obstacles (LowerLevelSolver.solve sharded over CPU processes, then the
+                   reference's rank_samples + update_distribution on the whole batch)
 """
 
 from __future__ import annotations
@@ -670,6 +673,63 @@ def gen_worlds_random():
     print(f"worlds_random written ({n} worlds)")
 
 
+def _c4_solve(args):
+    """One shard of the config-4 batch through the reference's LowerLevelSolver.solve."""
+    params, seed_scene = args
+    env50 = env_for(n_obs=50, obstacle_range=250.0)
+    basis = build_basis(10, 100, 5.0, "bernstein")
+    sc = highway_scene(env50, basis, 4, 3.0, 80, seed_scene)
+    solver = LowerLevelSolver(basis, TrackingWeights(), ParamLayout(4), ProjectionConfig(1.0, 100, 1e-3), 50)
+    _, proj = solver.solve(params, sc)
+    xd, yd = solver.velocities(proj.xi)
+    return (proj.xi, proj.residuals, upper_cost_batch(xd, yd, sc.spec.v_max), proj.iterations_used,
+            proj.residual_history.max(axis=1))
+
+
+def gen_dense_c4(B=10_000, shards=40, keep_xi=1000):
+    """BASELINE config 4 (B = 10 000 samples x 50 obstacles x 100 timesteps, 100 AM iterations):
+    one CEM iteration of solve_bilevel (pkg/bilevel.py:249-292), teacher-forced from the initial
+    distribution of bilevel_config_for (pkg/bench.py:245-261) drawn with default_rng(4).
+
+    The batch is split over CPU processes.  A split solve equals the unsplit one exactly when no
+    shard takes the batch-global early exit (pkg/projection.py:329): every shard then runs all
+    100 iterations, so the whole batch would too, and every other operation is per sample.  This
+    is checked twice: each shard's iterations_used == 100, and at B = 64 a 2-way split is
+    compared with the unsplit solve (max |diff| recorded)."""
+    import multiprocessing as mp
+    env50 = env_for(n_obs=50, obstacle_range=250.0)
+    basis = build_basis(10, 100, 5.0, "bernstein")
+    sc = highway_scene(env50, basis, 4, 3.0, 80, 0)
+    env2 = PlannerEnvConfig(horizon=5.0, num_samples=100, max_obstacles=50, proj_iters=100, batch_size=B,
+                            constraint_elites=150, elites=100, iterations=1, obstacle_range=250.0)
+    cfg = bilevel_config_for(env2, sc, batch_size=B, iterations=1)
+    params = SamplingDistribution(cfg.init_mean, cfg.init_cov).sample(B, np.random.default_rng(4))
+    t0 = time.time()
+    with mp.get_context("fork").Pool(os.cpu_count()) as pool:
+        small = pool.map(_c4_solve, [(params[:64], 0), (params[:32], 0), (params[32:64], 0)])
+        parts = pool.map(_c4_solve, [(c, 0) for c in np.array_split(params, shards)])
+    dt = time.time() - t0
+    split_diff = max(float(np.abs(np.concatenate([small[1][0], small[2][0]], axis=1) - small[0][0]).max()),
+                     float(np.abs(np.concatenate([small[1][1], small[2][1]]) - small[0][1]).max()))
+    used = np.array([p[3] for p in parts])
+    assert np.all(used == 100) and small[0][3] == 100, used
+    xi = np.concatenate([p[0] for p in parts], axis=1)
+    res = np.concatenate([p[1] for p in parts])
+    costs = np.concatenate([p[2] for p in parts])
+    hist_max = np.max(np.stack([p[4] for p in parts]), axis=0)
+    cons, el, ea = rank_samples(res, costs, cfg.constraint_elites, cfg.elites, cfg.residual_weight)
+    nd = update_distribution(SamplingDistribution(cfg.init_mean, cfg.init_cov), params[el], ea, cfg.eta, cfg.gamma)
+    keep = np.unique(np.concatenate([np.arange(keep_xi), el]))
+    out = dict(params=params, residuals=res, costs=costs, xi_keep_idx=keep, xi_keep=xi[:, keep],
+               cons_idx=cons, elite_idx=el, elite_aug=ea, mean=nd.mean, cov=nd.cov, init_mean=cfg.init_mean,
+               init_cov=cfg.init_cov, iters_used=used, history_max=hist_max, split_check_maxdiff=split_diff,
+               cfg=np.array([B, cfg.constraint_elites, cfg.elites, 1, cfg.eta, cfg.gamma, cfg.residual_weight]),
+               ref_seconds=dt, ref_processes=os.cpu_count(), **scene_arrays(sc))
+    np.savez_compressed(os.path.join(OUT, "dense_c4.npz"), **out)
+    print(f"dense_c4 written: {dt:.0f}s on {os.cpu_count()} processes, split check {split_diff:.2e}, "
+          f"r=0: {int(np.sum(res == 0))}, best {el[0]}")
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", nargs="*", default=None)
@@ -677,7 +737,8 @@ if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
     jobs = {"basis": gen_basis, "lower": gen_lower, "scenes": gen_scenes, "cem_small": gen_cem_small,
             "cem_c2": gen_cem_c2, "worlds": gen_worlds, "sim": gen_sim, "episodes": gen_episodes, "cem_variants": gen_cem_variants, "planners": gen_planners,
-            "harness": gen_harness, "absurd": gen_absurd, "worlds_random": gen_worlds_random}
+            "harness": gen_harness, "absurd": gen_absurd, "worlds_random": gen_worlds_random,
+            "dense_c4": gen_dense_c4}
     for name, fn in jobs.items():
         if a.only is None or name in a.only:
             fn()
