@@ -26,7 +26,7 @@ from .basis import PolynomialBasis, TrajectoryCoeffs, eval_trajectory
 from .batch_qp import NumericalFailure, QPSolutionBatch, TrackingWeights, build_qp_structure
 from .behavior import BehaviorParams, ParamLayout, WarmStartSource
 from .constraints import PlanningScene
-from .projection import ProjectionBatchResult, ProjectionConfig, ProjectionOperator
+from .projection import ProjectionBatchResult, ProjectionConfig, ProjectionOperator, require_device_order
 
 __all__ = [
     "SamplingDistribution", "EliteRecord", "BiLevelConfig", "IterationStats", "BiLevelResult", "upper_cost",
@@ -183,6 +183,7 @@ class LowerLevelSolver:
 
     def __init__(self, basis: PolynomialBasis, weights: TrackingWeights, layout: ParamLayout,
                  proj_config: ProjectionConfig, num_obstacles: int, device: int = 0):
+        require_device_order(basis)
         self.basis = basis
         self.layout = layout
         self.qp = build_qp_structure(basis, weights, layout)

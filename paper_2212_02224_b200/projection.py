@@ -121,6 +121,20 @@ def clip_magnitudes(state: ProjectionState, spec: ConstraintSpec, kappa_abs=None
     return replace(state, d_o=d_o, d_v=d_v, d_a=d_a)
 
 
+DEVICE_ORDER = 10          # the kernels' compile-time coefficient count is order + 1 = 11 (csrc/bd_common.cuh NC)
+
+
+def require_device_order(basis: PolynomialBasis) -> None:
+    """The device path is built for the BASELINE basis order (10, i.e. 11 coefficients per axis);
+    the reference's build_basis accepts any order >= 2 (pkg/basis.py:156-179), so another order
+    is refused here, before any factorization or device work, with a message that names the limit."""
+    if basis.num_coeffs != DEVICE_ORDER + 1:
+        raise NotImplementedError(
+            f"the B200 path supports order-{DEVICE_ORDER} bases ({DEVICE_ORDER + 1} coefficients per axis, the "
+            f"BASELINE configuration); got order {basis.num_coeffs - 1}.  The reference accepts any order >= 2 "
+            "(pkg/basis.py:156-179): plan with order 10 or use the reference for other orders.")
+
+
 class ProjectionOperator:
     """Reusable batched projector (pkg/projection.py:182-214): the augmented KKT is
     factorized once on the host and its inverse blocks live on the device."""
@@ -129,6 +143,7 @@ class ProjectionOperator:
                  config: ProjectionConfig = ProjectionConfig(), device: int = 0, context: Context | None = None):
         if num_obstacles < 0:
             raise ValueError("num_obstacles must be nonnegative")
+        require_device_order(basis)
         self.basis = basis
         self.qp = qp
         self.num_obstacles = num_obstacles

@@ -87,3 +87,17 @@ def test_highway_scenes_match_reference(seed):
         lim = g[tag + "_lim"]
         assert (sc.spec.ellipse_a, sc.spec.ellipse_b, sc.spec.v_min, sc.spec.v_max) == tuple(lim[:4])
         assert (sc.spec.y_lb, sc.spec.y_ub) == tuple(lim[7:9])
+
+
+def test_other_basis_orders_are_refused_before_any_work():
+    """The device kernels are compiled for order-10 bases; another order raises a clear
+    NotImplementedError before the factorization counter moves (pkg/basis.py:156-179 accepts it)."""
+    import pytest
+
+    import paper_2212_02224_b200 as bd
+    from paper_2212_02224_b200 import batch_qp
+    basis = bd.build_basis(6, 100, 5.0, "bernstein")
+    n0 = batch_qp.FACTORIZATION_COUNT
+    with pytest.raises(NotImplementedError, match="order-10"):
+        bd.LowerLevelSolver(basis, bd.TrackingWeights(), bd.ParamLayout(4), bd.ProjectionConfig(), 10)
+    assert batch_qp.FACTORIZATION_COUNT == n0
