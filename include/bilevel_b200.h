@@ -69,16 +69,21 @@ const char* bd_last_error(const bd_ctx* ctx);
 /* Use an external cudaStream_t (e.g. torch's current stream); NULL restores the library stream. */
 int bd_set_stream(bd_ctx* ctx, void* cuda_stream);
 int bd_synchronize(bd_ctx* ctx);
-/* Knobs: "lanes_per_sample" (0=auto, 4/8/16/32), "samples_per_cta" (0=auto), "timing" (0/1). */
+/* Knobs: "lanes_per_sample" (0=auto, 4/8/16/32/64), "samples_per_cta" (0=auto), "timing" (0/1),
+ * "latency_instance" (1=auto / 0=never pick the 255-register one-warp AM instance for 7-8 samples
+ * per SM), "persistent_cycle" (1=auto / 0=never run a single-scene bd_cem_cycle as the persistent
+ * cooperative kernel), "cvae_tensor_cores" (1/0), "sticky_errors" (1/0). */
 int bd_set_option(bd_ctx* ctx, const char* key, int value);
 /* Kernel launches issued by this context since creation (instrumentation). */
 int64_t bd_launch_count(const bd_ctx* ctx);
 /* Instrumentation (enable with bd_set_option(ctx, "timing", 1)): "am_ms" = summed CUDA-event
  * time of the AM kernel launches (recorded on the launching stream), "am_launches",
- * "am_sample_iters" = samples x iterations executed; "reset" clears them. Synchronises. */
+ * "am_sample_iters" = samples x iterations executed; "reset" clears them; "persistent_cycles" =
+ * bd_cem_cycle calls run as the persistent cooperative kernel (any time). Synchronises. */
 int bd_get_stat(bd_ctx* ctx, const char* key, double* value);
 /* Measurement probes for roofline denominators: "fp32_tflops" = dense FFMA throughput of an
- * all-SM register-resident kernel (CUDA events, current clocks). */
+ * all-SM register-resident kernel (CUDA events, current clocks); "fp32x2_tflops" = the same with
+ * packed fma.rn.f32x2 (FFMA2). */
 int bd_probe(bd_ctx* ctx, const char* what, double* value);
 /* Synchronise and return (in *bits) the OR of the device error words of the last
  * asynchronous call: 1 = non-finite iterate, 2 = stage-1 KKT residual above 1e-8. */

@@ -71,16 +71,37 @@ struct AmArgs {
 // Out of line: run by one CTA per scene, kept away from the main loop's register allocation.
 __device__ __noinline__ void exit_scan_block(unsigned* base, int max_iters, double tol, int scene,
                                                 int* iters_used, int* replay, unsigned long long* conflicts) {
+    // the slots of iteration it are 8 uint4 chunks held by 8 consecutive lanes; every chunk is
+    // loaded (coalesced, up to 4 per thread in flight) before any is re-armed with zeros, so the
+    // scan costs a few L2 round trips instead of one per slot
+    static_assert(ITMAX_SLOTS == 32, "8 uint4 chunks per iteration");
     __shared__ int red[32];
     int first = max_iters;
-    for (int it = threadIdx.x; it < max_iters; it += blockDim.x) {
-        unsigned mx = 0;
-        for (int s = 0; s < ITMAX_SLOTS; ++s) {
-            unsigned* slot = base + (size_t)it * ITMAX_SLOTS + s;
-            mx = max(mx, __ldcg(slot));
-            __stcg(slot, 0u);                   // re-arm for the next launch (no memset needed)
+    const int chunks = max_iters * (ITMAX_SLOTS / 4), T = blockDim.x;
+    uint4* b4 = reinterpret_cast<uint4*>(base);
+    const uint4 zero = make_uint4(0u, 0u, 0u, 0u);
+    for (int c0 = 0; c0 < chunks; c0 += 4 * T) {
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int c = c0 + u * T + (int)threadIdx.x;
+            v[u] = c < chunks ? __ldcg(b4 + c) : zero;
         }
-        if (static_cast<double>(__uint_as_float(mx)) <= tol && it < first) first = it;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int c = c0 + u * T + (int)threadIdx.x;
+            if (c < chunks) __stcg(b4 + c, zero);   // re-arm for the next launch (no memset needed)
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int c = c0 + u * T + (int)threadIdx.x;
+            unsigned mx = max(max(v[u].x, v[u].y), max(v[u].z, v[u].w));
+            mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+            mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+            mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+            const int it = c >> 3;
+            if (c < chunks && (c & 7) == 0 && static_cast<double>(__uint_as_float(mx)) <= tol && it < first) first = it;
+        }
     }
     for (int o = 16; o >= 1; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = first;
@@ -398,6 +419,167 @@ __device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float
     }
 }
 
+// Latency instance (P = 32, one CTA of 5-8 one-warp samples per SM, up to 255 registers; m and the
+// obstacle pairs fixed at compile time, no curvature, unsorted tile): the same per-timestep arithmetic
+// as sweep(), reorganised into three phases, each unrolled over the lane's JM timestep slots so the
+// scheduler overlaps their independent dependency chains instead of running one slot after another:
+//   A  forward X / Xd / Xdd, obstacle filter, polar split, coupled clips (branch-free);
+//   B  the exact obstacle path for the rare slots inside some ellipse;
+//   C  back-projection, direct residual and cost, accumulated in timestep order as sweep() does.
+// A slot past m (only the last, on lanes p >= m - (JM-1)P) is evaluated on a clamped timestep and
+// contributes exact zeros.
+#ifndef BD_LAT_CH
+#define BD_LAT_CH 2      // A/B on B200 (B = 1000, P = 32): 2 slots 0.229 ms, 3: 0.246, 4: 0.251
+#endif
+template <int P, bool INIT, int NV, int MT, int NPT, int TPB>
+__device__ __forceinline__ void sweep_lat(const float* __restrict__ wsm, const float4* __restrict__ osm,
+                                          const float2 (&cxy)[NC], float (&v)[NV], float* dap, int p,
+                                          const SceneLim& L, int& conf, bool want_cost) {
+    constexpr int JM = (MT + P - 1) / P;
+    constexpr int CH = JM > BD_LAT_CH ? BD_LAT_CH : JM;   // slots per phase group (register budget)
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] = 0.f;
+#pragma unroll
+    for (int j0 = 0; j0 < JM; j0 += CH) {
+    float X[CH], Y[CH], qm[CH], dvs[CH], das[CH], crs[CH];
+    float2 rv[CH], ra[CH];
+    // ---- phase A
+#pragma unroll
+    for (int jj = 0; jj < CH; ++jj) {
+        const int j = j0 + jj;
+        const bool valid = j < JM && ((MT % P == 0) || j + 1 < JM || p + j * P < MT);
+        const int t = valid ? p + j * P : MT - 1;
+        float w[WROW];
+        const float4* wr = reinterpret_cast<const float4*>(wsm + t * WROW);
+#pragma unroll
+        for (int q = 0; q < WROW / 4; ++q) {
+            const float4 f = wr[q];
+            w[4 * q] = f.x; w[4 * q + 1] = f.y; w[4 * q + 2] = f.z; w[4 * q + 3] = f.w;
+        }
+        float2 P0 = make_float2(0.f, 0.f), P1 = P0, P2 = P0;
+#pragma unroll
+        for (int k = 0; k < NC; ++k) P0 = ffma2(w[k], cxy[k], P0);
+        const float4* op = osm + t * NPT;
+        float4 ob[NPT];
+#pragma unroll
+        for (int o = 0; o < NPT; ++o) ob[o] = op[o];
+#pragma unroll
+        for (int k = 0; k < NC; ++k) {
+            P1 = ffma2(w[NC + k], cxy[k], P1);
+            P2 = ffma2(w[2 * NC + k], cxy[k], P2);
+        }
+        const float xs0 = P0.x * L.inv_a, ys0 = P0.y * L.inv_b;
+        float qmin = 3.0e38f;
+#pragma unroll
+        for (int o = 0; o < NPT; ++o) {
+            const float2 wc = fadd2(make_float2(xs0, xs0), make_float2(ob[o].x, ob[o].y));
+            const float2 ws = fadd2(make_float2(ys0, ys0), make_float2(ob[o].z, ob[o].w));
+            const float2 q = ffma2(wc, wc, fmul2(ws, ws));
+            qmin = fminf(qmin, fminf(q.x, q.y));
+        }
+        const float XD = P1.x, YD = P1.y, XDD = P2.x, YDD = P2.y;
+        const float dv2 = fmaf(XD, XD, YD * YD);
+        const float da2 = fmaf(XDD, XDD, YDD * YDD);
+        const float iv = dv2 > 0.f ? rsqrtf(dv2) : 0.f;
+        const float ia = da2 > 0.f ? rsqrtf(da2) : 0.f;
+        const float dv = dv2 * iv, da = da2 * ia;
+        const float cross = fabsf(fmaf(YDD, XD, -XDD * YD));
+        const float gv = (da2 > 0.f ? cross : fabsf(YD)) * iv;
+        const float gva = gv * ia;
+        const float gap = dv2 > 0.f ? (da2 > 0.f ? gva : gv) : fabsf(YDD) * ia;
+        const int di = min(j, JM - 1) * TPB;
+        const float da_prev = INIT ? fminf(fmaxf(da, 0.f), L.a_max) : dap[di];
+        const float vhi = L.v_max;
+        const float vlo = fmaxf(L.v_min, sqrtf(da_prev * gap * L.inv_k_max));
+        conf += (valid && vlo > vhi) ? 1 : 0;
+        const float dvc = fminf(fmaxf(dv, fminf(vlo, vhi)), vhi);
+        const float ahi = fminf(L.a_max, __fdividef(dvc * dvc * L.k_max, fmaxf(gap, 1e-8f)));
+        const float dac = fminf(fmaxf(da, 0.f), ahi);
+        if (j < JM) dap[di] = dac;          // (compile-time after unrolling)
+        float2 rvj, raj;
+        if (dv2 > 0.f) rvj = fmul2(make_float2((dv - dvc) * iv, (dv - dvc) * iv), P1);
+        else rvj = make_float2(-dvc, 0.f);
+        if (da2 > 0.f) raj = fmul2(make_float2((da - dac) * ia, (da - dac) * ia), P2);
+        else raj = make_float2(-dac, 0.f);
+        const float2 z2 = make_float2(0.f, 0.f);
+        rv[jj] = valid ? rvj : z2;
+        ra[jj] = valid ? raj : z2;
+        X[jj] = P0.x; Y[jj] = P0.y;
+        qm[jj] = valid ? qmin : 3.0e38f;
+        dvs[jj] = dv; das[jj] = da; crs[jj] = cross;
+    }
+    // ---- phase B (rare): exact obstacle residuals of the slots inside some ellipse
+    float rox[CH], roy[CH], coll[CH];
+#pragma unroll
+    for (int jj = 0; jj < CH; ++jj) {
+        const int j = j0 + jj;
+        rox[jj] = 0.f; roy[jj] = 0.f; coll[jj] = 0.f;
+        if (qm[jj] < 1.f) {
+            const int t = p + j * P;
+            const float4* op = osm + t * NPT;
+            const float xs = X[jj] * L.inv_a, ys = Y[jj] * L.inv_b;
+            for (int o = 0; o < NPT; ++o) {
+                const float4 ob = op[o];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const float wc = xs + (h ? ob.y : ob.x), ws = ys + (h ? ob.w : ob.z);
+                    const float q = fmaf(wc, wc, ws * ws);
+                    if (q < 1.f) {
+                        coll[jj] += 1.f - q;
+                        if (q > 0.f) {
+                            const float f = 1.f - rsqrtf(q);
+                            rox[jj] = fmaf(wc, f, rox[jj]);
+                            roy[jj] = fmaf(ws, f, roy[jj]);
+                        } else {
+                            rox[jj] -= 1.f;
+                        }
+                    }
+                }
+            }
+        }
+    }
+    // ---- phase C: back-projection g += Wd^T r_v + Wdd^T r_a + W^T r_o, direct residual, cost
+#pragma unroll
+    for (int jj = 0; jj < CH; ++jj) {
+        const int j = j0 + jj;
+        const bool valid = j < JM && ((MT % P == 0) || j + 1 < JM || p + j * P < MT);
+        const int t = valid ? p + j * P : MT - 1;
+        const float up = fmaxf(Y[jj] - L.y_ub, 0.f), lo = fmaxf(L.y_lb - Y[jj], 0.f);
+        const float2 roj = make_float2(L.a * rox[jj], fmaf(L.b, roy[jj], up - lo));
+        const float2 ro = valid ? roj : make_float2(0.f, 0.f);
+        float w[WROW];
+        const float4* wr = reinterpret_cast<const float4*>(wsm + t * WROW);
+#pragma unroll
+        for (int q = 0; q < WROW / 4; ++q) {
+            const float4 f = wr[q];
+            w[4 * q] = f.x; w[4 * q + 1] = f.y; w[4 * q + 2] = f.z; w[4 * q + 3] = f.w;
+        }
+#pragma unroll
+        for (int k = 0; k < NC; ++k) {
+            float2 g = make_float2(v[2 * k], v[2 * k + 1]);
+            g = ffma2(w[NC + k], rv[jj], g);
+            g = ffma2(w[2 * NC + k], ra[jj], g);
+            g = ffma2(w[k], ro, g);
+            v[2 * k] = g.x;
+            v[2 * k + 1] = g.y;
+        }
+        if (!INIT) {
+            const float dv = dvs[jj], da = das[jj];
+            float r = coll[jj] + up + lo;
+            r += fmaxf(dv - L.v_max, 0.f) + fmaxf(L.v_min - dv, 0.f);
+            r += fmaxf(da - L.a_max, 0.f);
+            const float sp = fmaxf(dv, 1e-6f);
+            r += fmaxf(__fdividef(crs[jj], sp * sp * sp) - L.k_max, 0.f);
+            v[NX] += valid ? r : 0.f;
+            if (want_cost) {
+                const float e = dv - L.v_max;
+                v[NX + 1] = valid ? fmaf(e, e, v[NX + 1]) : v[NX + 1];
+            }
+        }
+    }
+    }
+}
+
 // The all-gather fused into the epilogue: one value into every rank's symmetric buffer
 // (kept out of line so the main loop's register allocation does not see it).
 __device__ __noinline__ void p2p_store_all(void* const* bufs, int world, size_t off, long long row, double val) {
@@ -412,23 +594,10 @@ __device__ __forceinline__ void pair_sync() {
 #ifndef BD_AM_MINB
 #define BD_AM_MINB 2       // x 256 threads: 128 registers per thread
 #endif
-template <int P, bool CURV, int MT = 0, int NPT = 0, int TPB = 0>
-__global__ void __launch_bounds__(TPB > 256 ? TPB : 256, TPB > 256 ? 1 : BD_AM_MINB) am_kernel(const AmArgs a) {
-    // P <= 32: a sample is a group of P lanes of one warp.  P == 64: a sample spans two warps
-    // (latency mapping for small batches); each warp reduce-scatters its partial sums, the second
-    // warp hands them to the first through shared memory and the first warp owns the update.
-    constexpr bool PAIR = (P == 64);
-    constexpr int RP = PAIR ? 32 : P;                // reduction width / ownership stride
-    constexpr int NV = ((NX + 2 + RP - 1) / RP) * RP;   // 22 back-projections + residual + cost, padded
-    constexpr int ROWS = (NX + RP - 1) / RP;         // coefficient rows owned per lane
-    extern __shared__ __align__(16) unsigned char smem[];
-
-    const int scene = blockIdx.y;
-    int iters = a.max_iters;
-    if (a.replay != nullptr) {
-        iters = a.replay[scene];
-        if (iters <= 0) return;
-    }
+// Stage the basis rows and the scene's obstacle tile (TMA bulk copies on one mbarrier) and the
+// fp64 K blocks (threads) in shared memory; returns after a CTA barrier.
+template <int P, bool CURV>
+__device__ __forceinline__ void am_stage(const AmArgs& a, int scene, unsigned char* smem, uint64_t* stage_bar) {
     const int m = a.m, neq = a.neq, n_obs = a.n_obs;
     const int threads = blockDim.x;
     const AmSmem lay(m, n_obs, neq, a.n_curv, a.s_cta, threads, P, CURV);
@@ -438,35 +607,51 @@ __global__ void __launch_bounds__(TPB > 256 ? TPB : 256, TPB > 256 ? 1 : BD_AM_M
     double* kbsm = reinterpret_cast<double*>(smem + lay.kb);
     double* asm_ = reinterpret_cast<double*>(smem + lay.a);
     float* csm = reinterpret_cast<float*>(smem + lay.curv);
-
     // ---- stage constants and the scene tile once per CTA: the basis rows and this scene's
     //      obstacle tile arrive by TMA bulk copy (one mbarrier), the small fp64 blocks by the threads
-    __shared__ __align__(8) uint64_t stage_bar;
     const uint32_t w_bytes = (uint32_t)m * WROW * 4, o_bytes = (uint32_t)(n_obs / 2) * m * 16;
     if (threadIdx.x == 0) {
-        mbar_init(&stage_bar, 1);
+        mbar_init(stage_bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        mbar_expect_tx(&stage_bar, w_bytes + o_bytes);
-        bulk_load(wsm, a.wrow, w_bytes, &stage_bar);
+        mbar_expect_tx(stage_bar, w_bytes + o_bytes);
+        bulk_load(wsm, a.wrow, w_bytes, stage_bar);
         if (o_bytes) bulk_load(osm, reinterpret_cast<const float4*>(a.obs) + (size_t)scene * (n_obs / 2) * m, o_bytes,
-                               &stage_bar);
+                               stage_bar);
     }
     for (int i = threadIdx.x; i < NX * KSTR; i += threads) ksm[i] = a.kblk[i];
     for (int i = threadIdx.x; i < NX * neq; i += threads) { kbsm[i] = a.kb[i]; asm_[i] = a.aeq[i]; }
     if (CURV)
         for (int i = threadIdx.x; i < 2 * a.n_curv; i += threads) csm[i] = a.curv[(size_t)scene * 2 * a.n_curv + i];
-    mbar_wait(&stage_bar, 0);
+    mbar_wait(stage_bar, 0);
     __syncthreads();
+}
 
+// AM iterations for the samples of CTA `blk` of `scene` (constants already staged): prologue,
+// `iters` iterations, outputs, conflict / error atomics.
+template <int P, bool CURV, int MT, int NPT, int TPB, bool LAT>
+__device__ __forceinline__ void am_samples(const AmArgs& a, int scene, int blk, int iters, unsigned char* smem) {
+    constexpr bool PAIR = (P == 64);
+    constexpr int RP = PAIR ? 32 : P;                // reduction width / ownership stride
+    constexpr int NV = ((NX + 2 + RP - 1) / RP) * RP;   // 22 back-projections + residual + cost, padded
+    constexpr int ROWS = (NX + RP - 1) / RP;         // coefficient rows owned per lane
+    const int m = a.m, neq = a.neq, n_obs = a.n_obs;
+    const int threads = blockDim.x;
+    const AmSmem lay(m, n_obs, neq, a.n_curv, a.s_cta, threads, P, CURV);
+    float* wsm = reinterpret_cast<float*>(smem + lay.w);
+    float4* osm = reinterpret_cast<float4*>(smem + lay.obs);
+    double* ksm = reinterpret_cast<double*>(smem + lay.k);
+    double* kbsm = reinterpret_cast<double*>(smem + lay.kb);
+    double* asm_ = reinterpret_cast<double*>(smem + lay.a);
+    float* csm = reinterpret_cast<float*>(smem + lay.curv);
     const int lane = threadIdx.x & 31;
     const int p = PAIR ? (int)(threadIdx.x % 64) : lane % P;        // timestep lane within the sample
     const int own = PAIR ? ((threadIdx.x & 32) ? 64 : lane) : p;     // ownership index (>= NX: none)
     auto gsync = [&]() { if (PAIR) pair_sync(); else __syncwarp(); };
     const int slot = threadIdx.x / P;
-    const int local = blockIdx.x * a.s_cta + slot;
+    const int local = (blk < 0 ? (int)blockIdx.x : blk) * a.s_cta + slot;
     const bool active = local < a.B;
     const size_t row = (size_t)scene * a.B + (active ? local : a.B - 1);
     double* su = reinterpret_cast<double*>(smem + lay.scr + (size_t)slot * AmSmem::SCR_BYTES);
@@ -531,14 +716,18 @@ __global__ void __launch_bounds__(TPB > 256 ? TPB : 256, TPB > 256 ? 1 : BD_AM_M
             if (!(threadIdx.x & 32) && lane < NX + 2) v[0] += xbuf[lane];
         }
     };
-    sweep<P, CURV, true, NV, MT, NPT, TPB>(wsm, osm, csm, cxy, v, dap, kap, kix, threads, p, m, n_obs / 2, a.n_curv, L,
-                                           conf, a.sorted != 0);
+    constexpr bool LAT32 = LAT && P <= 32 && MT > 0 && NPT > 0 && NPT < SORT_MIN_PAIRS && !CURV;
+    if constexpr (LAT32)
+        sweep_lat<P, true, NV, MT, NPT, TPB>(wsm, osm, cxy, v, dap, p, L, conf, true);
+    else
+        sweep<P, CURV, true, NV, MT, NPT, TPB>(wsm, osm, csm, cxy, v, dap, kap, kix, threads, p, m, n_obs / 2,
+                                               a.n_curv, L, conf, a.sorted != 0);
     reduce();
 
     const int r_lane = NX % RP, r_slot = (NX / RP) * RP;
     const int c_lane = (NX + 1) % RP, c_slot = ((NX + 1) / RP) * RP;
     float resid = 0.f, cost = 0.f;
-    const int warp_global = blockIdx.x * (threads / 32) + (threadIdx.x >> 5);
+    const int warp_global = (blk < 0 ? (int)blockIdx.x : blk) * (threads / 32) + (threadIdx.x >> 5);
     unsigned* itm = a.itmax + (size_t)scene * a.max_iters * ITMAX_SLOTS + (warp_global % ITMAX_SLOTS);
 
     for (int it = 0; it < iters; ++it) {
@@ -586,8 +775,11 @@ __global__ void __launch_bounds__(TPB > 256 ? TPB : 256, TPB > 256 ? 1 : BD_AM_M
 #pragma unroll
         for (int q = 0; q < NC; ++q) cxy[q] = reinterpret_cast<const float2*>(sc)[q];
         // ---- projections, back-projection, residual at the new iterate
-        sweep<P, CURV, false, NV, MT, NPT, TPB>(wsm, osm, csm, cxy, v, dap, kap, kix, threads, p, m, n_obs / 2, a.n_curv,
-                                                L, conf, a.sorted != 0, it == iters - 1);   // cost: last sweep only
+        if constexpr (LAT32)
+            sweep_lat<P, false, NV, MT, NPT, TPB>(wsm, osm, cxy, v, dap, p, L, conf, it == iters - 1);
+        else
+            sweep<P, CURV, false, NV, MT, NPT, TPB>(wsm, osm, csm, cxy, v, dap, kap, kix, threads, p, m, n_obs / 2,
+                                                    a.n_curv, L, conf, a.sorted != 0, it == iters - 1);   // cost: last sweep only
         reduce();
         resid = v[r_slot];
         cost = v[c_slot];
@@ -645,6 +837,27 @@ __global__ void __launch_bounds__(TPB > 256 ? TPB : 256, TPB > 256 ? 1 : BD_AM_M
         if (conf) atomicAdd(a.conflicts + scene, (unsigned long long)conf);
         if (anybad) atomicOr(a.err + scene, ERR_NONFINITE);
     }
+}
+
+// LAT: latency instances, one CTA of 5-8 samples per SM (P = 64: two-warp samples, <= 128 registers;
+// P = 32 / 16: one-warp / half-warp samples, whose <= 2 warps per SM sub-partition may use up to
+// 255 registers and run the phase-split sweep_lat)
+template <int P, bool CURV, int MT = 0, int NPT = 0, int TPB = 0, bool LAT = false>
+__global__ void __launch_bounds__(LAT ? TPB : 256, LAT ? 1 : BD_AM_MINB) am_kernel(const AmArgs a) {
+    // P <= 32: a sample is a group of P lanes of one warp.  P == 64: a sample spans two warps
+    // (latency mapping for small batches); each warp reduce-scatters its partial sums, the second
+    // warp hands them to the first through shared memory and the first warp owns the update.
+    extern __shared__ __align__(16) unsigned char smem[];
+
+    const int scene = blockIdx.y;
+    int iters = a.max_iters;
+    if (a.replay != nullptr) {
+        iters = a.replay[scene];
+        if (iters <= 0) return;
+    }
+    __shared__ __align__(8) uint64_t stage_bar;
+    am_stage<P, CURV>(a, scene, smem, &stage_bar);
+    am_samples<P, CURV, MT, NPT, TPB, LAT>(a, scene, -1, iters, smem);
     // ---- batch-global early exit folded into the last CTA of the scene (no extra launch)
     if (a.replay == nullptr && a.done_ctr != nullptr) {
         __shared__ bool last;

@@ -24,6 +24,7 @@
 #include "scene_kernels.cuh"
 #include "sim_kernels.cuh"
 #include "p2p_kernels.cuh"
+#include "cem_persistent.cuh"
 
 using namespace bd;
 
@@ -64,7 +65,8 @@ struct bd_ctx {
     cudaStream_t stream = nullptr;
     std::string err;
     int64_t launches = 0;
-    int opt_lanes = 0, opt_spc = 0;
+    int64_t persistent_cycles = 0;   // bd_cem_cycle calls run as the persistent kernel
+    int opt_lanes = 0, opt_spc = 0, opt_lat_off = 0, opt_persist_off = 0;
     // instrumentation
     bool timing = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_used, ev_free;
@@ -95,6 +97,7 @@ struct bd_ctx {
     std::vector<PendingCopy> pending;
     bool host_out = false;
     // CEM state
+    DevBuf c_bar;               // grid-barrier words of the persistent CEM kernel
     DevBuf c_mean, c_cov, c_L, c_done, c_best_idx, c_best_p, c_best_xi, c_best_s, c_stats, c_cons, c_elite, c_eaug;
     // control grid
     int n_ctrl = 0;
@@ -354,13 +357,13 @@ void raise_smem(K kernel, size_t bytes) {
         e.raised = bytes;
 }
 
-template <int P, bool CURV, int MT = 0, int NPT = 0, int TPB = 0>
+template <int P, bool CURV, int MT = 0, int NPT = 0, int TPB = 0, bool LAT = false>
 int launch_am_t(bd_ctx* ctx, AmArgs a, int threads, bool replay_pass, int* occ = nullptr) {
     const AmSmem lay(a.m, a.n_obs, a.neq, a.n_curv, a.s_cta, threads, P, CURV);
     if (lay.total > 227 * 1024) return fail(ctx, BD_ERR_VALUE, "AM kernel needs %zu B of shared memory", lay.total);
-    raise_smem(am_kernel<P, CURV, MT, NPT, TPB>, lay.total);
+    raise_smem(am_kernel<P, CURV, MT, NPT, TPB, LAT>, lay.total);
     if (occ) {   // occupancy query only (lane-mapping choice)
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, am_kernel<P, CURV, MT, NPT, TPB>, threads, lay.total) !=
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, am_kernel<P, CURV, MT, NPT, TPB, LAT>, threads, lay.total) !=
             cudaSuccess) {
             cudaGetLastError();
             *occ = 0;
@@ -381,7 +384,7 @@ int launch_am_t(bd_ctx* ctx, AmArgs a, int threads, bool replay_pass, int* occ =
         }
         cudaEventRecord(ev.first, ctx->stream);
     }
-    am_kernel<P, CURV, MT, NPT, TPB><<<grid, threads, lay.total, ctx->stream>>>(a);
+    am_kernel<P, CURV, MT, NPT, TPB, LAT><<<grid, threads, lay.total, ctx->stream>>>(a);
     ctx->launches++;
     if (timed) {
         cudaEventRecord(ev.second, ctx->stream);
@@ -413,10 +416,20 @@ int dispatch_am(bd_ctx* ctx, AmArgs a, int P, int threads, bool replay_pass, int
     // single-scene latency shape: one CTA of 5-8 two-warp samples per SM (see default_threads)
     if (P == 64 && !curv && a.m == 100 && a.n_obs == 10 && threads > 256) {
         switch (threads) {
-            case 320: return launch_am_t<64, false, 100, 5, 320>(ctx, a, threads, replay_pass, occ);
-            case 384: return launch_am_t<64, false, 100, 5, 384>(ctx, a, threads, replay_pass, occ);
-            case 448: return launch_am_t<64, false, 100, 5, 448>(ctx, a, threads, replay_pass, occ);
-            case 512: return launch_am_t<64, false, 100, 5, 512>(ctx, a, threads, replay_pass, occ);
+            case 320: return launch_am_t<64, false, 100, 5, 320, true>(ctx, a, threads, replay_pass, occ);
+            case 384: return launch_am_t<64, false, 100, 5, 384, true>(ctx, a, threads, replay_pass, occ);
+            case 448: return launch_am_t<64, false, 100, 5, 448, true>(ctx, a, threads, replay_pass, occ);
+            case 512: return launch_am_t<64, false, 100, 5, 512, true>(ctx, a, threads, replay_pass, occ);
+            default: return fail(ctx, BD_ERR_VALUE, "unsupported CTA size %d", threads);
+        }
+    }
+    // single-scene latency shape, one-warp samples: one CTA of 5-8 samples per SM, 255 registers
+    if (P == 32 && !curv && a.m == 100 && a.n_obs == 10 && threads > 128) {
+        switch (threads) {
+            case 160: return launch_am_t<32, false, 100, 5, 160, true>(ctx, a, threads, replay_pass, occ);
+            case 192: return launch_am_t<32, false, 100, 5, 192, true>(ctx, a, threads, replay_pass, occ);
+            case 224: return launch_am_t<32, false, 100, 5, 224, true>(ctx, a, threads, replay_pass, occ);
+            case 256: return launch_am_t<32, false, 100, 5, 256, true>(ctx, a, threads, replay_pass, occ);
             default: return fail(ctx, BD_ERR_VALUE, "unsupported CTA size %d", threads);
         }
     }
@@ -434,14 +447,14 @@ int dispatch_am(bd_ctx* ctx, AmArgs a, int P, int threads, bool replay_pass, int
 int default_threads(bd_ctx* ctx, int P, const AmArgs& a) {
     int threads = ctx->opt_spc ? ctx->opt_spc * P : (P == 32 ? 64 : 128);
     if (P == 64 && threads % 64) threads = 128;
-    if (P == 64 && !ctx->opt_spc && a.n_curv == 0 && a.m == 100 && a.n_obs == 10) {
+    if ((P == 64 || P == 32) && !ctx->opt_spc && a.n_curv == 0 && a.m == 100 && a.n_obs == 10) {
         // two-warp mapping on the BASELINE shape: give every SM one CTA of ceil(samples / SMs)
         // samples when that is 5-8, instead of 3-4 two-sample CTAs whose count differs by one
         // between SMs (B = 1000: 0.257 -> 0.246 ms per AM launch)
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
         const long long per_sm = ((long long)a.B * ctx->S + sms - 1) / sms;
-        if (per_sm >= 5 && per_sm <= 8) threads = 64 * (int)per_sm;
+        if (per_sm >= 5 && per_sm <= 8) threads = P * (int)per_sm;
     }
     return threads;
 }
@@ -456,6 +469,13 @@ int pick_lanes(bd_ctx* ctx, const AmArgs& a) {
     const double total = (double)a.B * ctx->S;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+    // BASELINE latency shape with 7-8 samples per SM: one-warp samples in the 255-register
+    // phase-split instance (A/B on B200, ms per AM launch, one-warp vs two-warp: B = 1000 0.230 vs
+    // 0.242, B = 1100 0.234 vs 0.246; at 5-6 per SM the two-warp mapping wins: B = 700 0.222 vs 0.196)
+    if (!ctx->opt_lat_off && a.n_curv == 0 && a.m == 100 && a.n_obs == 10) {
+        const long long per_sm = ((long long)total + sms - 1) / sms;
+        if (per_sm >= 7 && per_sm <= 8) return 32;
+    }
     const int cands[4] = {8, 16, 32, 64};
     const double overhead[4] = {0.5, 0.7, 0.9, 1.0};
     int best = 8;
@@ -659,6 +679,14 @@ int bd_set_option(bd_ctx* ctx, const char* key, int value) {
         ctx->err_sticky = value != 0;
         return 0;
     }
+    if (!strcmp(key, "persistent_cycle")) {   // 0: single-scene CEM cycles as the per-iteration launch chain
+        ctx->opt_persist_off = value == 0;
+        return 0;
+    }
+    if (!strcmp(key, "latency_instance")) {   // 0: never pick the one-warp latency instance automatically
+        ctx->opt_lat_off = value == 0;
+        return 0;
+    }
     if (!strcmp(key, "samples_per_cta")) {
         ctx->opt_spc = value < 0 ? 0 : value;
         return 0;
@@ -681,6 +709,7 @@ int bd_get_stat(bd_ctx* ctx, const char* key, double* value) {
     ctx->ev_used.clear();
     if (!strcmp(key, "am_ms")) *value = ctx->am_ms;
     else if (!strcmp(key, "am_launches")) *value = ctx->am_launches;
+    else if (!strcmp(key, "persistent_cycles")) *value = (double)ctx->persistent_cycles;
     else if (!strcmp(key, "am_sample_iters")) *value = ctx->am_sample_iters;
     else if (!strcmp(key, "reset")) { ctx->am_ms = ctx->am_launches = ctx->am_sample_iters = 0.0; *value = 0.0; }
     else return fail(ctx, BD_ERR_VALUE, "unknown stat %s", key);
@@ -1344,6 +1373,82 @@ int bd_rank_refit(bd_ctx* ctx, int S, int B, int dim, const double* resid, const
     return finish_call(ctx, false, 0);
 }
 
+// Single-scene CEM cycle as one cooperative persistent kernel (csrc/cem_persistent.cuh) when the
+// batch maps to one CTA of 7-8 one-warp samples per SM on the BASELINE latency shape; returns 1
+// when the shape does not apply (the caller runs the per-iteration launch chain instead).
+static int try_cem_persistent(bd_ctx* ctx, const bd_cem_config* cfg, const CemState& s, const S1Args& s1, bool s1def,
+                              const double* dz, const double* dwarm, const double* db, int it0, int it1) {
+    if (ctx->opt_persist_off || ctx->timing || ctx->S != 1 || ctx->n_curv != 0 || ctx->m != 100 ||
+        ctx->obs_pad != 10 || ctx->obs_sorted || !s1def || db != nullptr || ctx->p2p_epilogue || ctx->opt_lanes ||
+        ctx->opt_spc)
+        return 1;
+    int sms = 148, coop = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->device);
+    const int B = cfg->batch;
+    const int spc = (B + sms - 1) / sms;
+    if (!coop || spc < 7 || spc > 8) return 1;
+    const int grid = (B + spc - 1) / spc + 1, threads = 32 * spc;   // workers + the control CTA
+    if (grid > sms) return 1;
+    const int iters = cfg->am_iters;
+    const size_t itmax_bytes = (size_t)iters * ITMAX_SLOTS * 4;
+    if (int rc = ensure_itmax(ctx, itmax_bytes)) return rc;
+    CU(ctx->w_replay.ensure(4));
+    CU(ctx->w_order.ensure((size_t)B * 4));
+    CU(ctx->c_bar.ensure(16));
+    if (ctx->itmax_clean < itmax_bytes) CU(cudaMemsetAsync(ctx->w_itmax.p, 0, itmax_bytes, ctx->stream));
+    ctx->itmax_clean = std::max(ctx->itmax_clean, itmax_bytes);
+    CU(cudaMemsetAsync(ctx->c_bar.p, 0, 16, ctx->stream));
+    CemPersistArgs pa{};
+    pa.am = projection_args(ctx, B, ctx->w_xibar.as<double>(), iters, ctx->w_xi.as<double>(),
+                            ctx->w_res.as<double>(), ctx->w_cost.as<double>());
+    pa.am.s_cta = spc;
+    pa.am.b = nullptr;
+    pa.am.hist_out = nullptr;
+    pa.am.replay = nullptr;
+    pa.am.tol = cfg->tol;
+    pa.am.iters_used = ctx->w_iters.as<int>();
+    pa.am.replay_out = ctx->w_replay.as<int>();
+    pa.am.done_ctr = nullptr;
+    pa.cs = s;
+    pa.s1 = s1;
+    pa.z = dz;
+    pa.warm = dwarm;
+    pa.seed = cfg->seed;
+    pa.scene_offset = cfg->scene_offset;
+    pa.it0 = it0;
+    pa.it1 = it1;
+    pa.am_iters = iters;
+    pa.params = ctx->w_params.as<double>();
+    pa.order = ctx->w_order.as<int>();
+    pa.bar = ctx->c_bar.as<unsigned>();
+    const AmSmem lay(ctx->m, ctx->obs_pad, ctx->neq, 0, spc, threads, 32, false);
+    pa.s1_off = align_up(lay.total, 16);
+    const size_t s1_bytes = (size_t)(2 * s1.nr * s1_ld(s1.nr) + 2 * NC * s1.m_seg + spc * MAX_DIM + spc * S1_VEC) * 8;
+    pa.key_off = align_up(pa.s1_off + s1_bytes, 16);
+    const size_t smem = pa.key_off + std::max((size_t)B * 8, rank_refit_smem(cfg->n_cons, cfg->n_elite, ctx->dim));
+    if (smem > 200 * 1024) return 1;
+    void* args[] = {&pa};
+    cudaError_t e;
+    if (spc == 7) {
+        raise_smem(cem_persistent_kernel<224>, smem);
+        e = cudaLaunchCooperativeKernel((const void*)cem_persistent_kernel<224>, dim3(grid), dim3(threads), args, smem,
+                                        ctx->stream);
+    } else {
+        raise_smem(cem_persistent_kernel<256>, smem);
+        e = cudaLaunchCooperativeKernel((const void*)cem_persistent_kernel<256>, dim3(grid), dim3(threads), args, smem,
+                                        ctx->stream);
+    }
+    if (e == cudaErrorCooperativeLaunchTooLarge) {   // not co-resident on this device: launch chain instead
+        cudaGetLastError();
+        return 1;
+    }
+    if (e != cudaSuccess) return fail(ctx, BD_ERR_CUDA, "persistent CEM launch: %s", cudaGetErrorString(e));
+    ctx->launches++;
+    ctx->persistent_cycles++;
+    return 0;
+}
+
 int bd_cem_cycle(bd_ctx* ctx, int S, const bd_cem_config* cfg, const double* init_mean, const double* init_cov,
                  const double* z, const double* warm, int64_t* best_index, double* best_params, double* best_xi,
                  double* best_cost, double* best_residual, double* best_aug, double* stats, double* final_mean,
@@ -1415,7 +1520,9 @@ int bd_cem_cycle(bd_ctx* ctx, int S, const bd_cem_config* cfg, const double* ini
     const bool s1def = s1.nr == S1_DEF_NR && dim == S1_DEF_DIM && ctx->m_seg == S1_DEF_MS && !ctx->with_goal;
     raise_smem(sample_stage1_kernel<true>, s1smem);
     raise_smem(sample_stage1_kernel<false>, s1smem);
-    for (int it = it0; it < it1; ++it) {
+    rc = S == 1 ? try_cem_persistent(ctx, cfg, s, s1, s1def, dz, dwarm, db, it0, it1) : 1;
+    if (rc < 0) return rc;
+    for (int it = rc == 0 ? it1 : it0; it < it1; ++it) {
         const double* zi = dz ? dz + (size_t)(it - it0) * tot * dim : nullptr;
         auto s1k = s1def ? sample_stage1_kernel<true> : sample_stage1_kernel<false>;
         s1k<<<(unsigned)((tot + 7) / 8), 256, s1smem, ctx->stream>>>(

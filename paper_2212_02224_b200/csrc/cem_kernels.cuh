@@ -21,10 +21,56 @@ __device__ __forceinline__ unsigned long long ordered_bits(double x) {
 // rank_samples (pkg/bilevel.py:134-135).
 __device__ __forceinline__ double aug_cost(double c, double w, double r) { return __dadd_rn(c, __dmul_rn(w, r)); }
 
-// Warp-cooperative Cholesky of a dim x dim SPD matrix held in shared memory (row-major, fp64):
-// column j: lane 0 forms the pivot, lanes i > j the sub-diagonal entries.  Returns false (in
-// every lane) if the matrix is not positive definite.
+// Warp-cooperative Cholesky of a dim x dim SPD matrix held in shared memory (row-major, fp64).
+// Lane r < dim keeps row r of L in registers; column j is formed by every lane from row j of L
+// (broadcast by shuffles), lane j's value being the pivot: the same operations in the same order
+// as the textbook column loop (pivot a_jj - sum_k l_jk^2, entries (a_ij - sum_k l_ik l_jk) / l_jj),
+// without shared-memory round trips on the dependency chain.  D is the compile-time size (every
+// loop unrolled, L in registers: 8 x 8 ~2.7k cycles against ~6k for a shared-memory column loop).
+// Returns false (in every lane) if the matrix is not positive definite; L is then unspecified.
+template <int D>
+__device__ __forceinline__ bool warp_chol_fixed(const double* A, double* L, int lane) {
+    // one lane, every entry in registers, no warp-synchronous step on the chain: column j costs the
+    // j-deep FMA chains of its entries (independent) plus one sqrt and one reciprocal.  Inside the
+    // persistent CEM kernel every shuffle / warp barrier on this chain cost ~400 cycles (22k cycles
+    // for the lane-parallel form); this form takes ~2k.
+    bool ok = true;
+    if (lane == 0) {
+        double Lm[D][D];
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+            for (int k = 0; k <= i; ++k) Lm[i][k] = A[i * D + k];
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            double piv = Lm[j][j];
+#pragma unroll
+            for (int k = 0; k < j; ++k) piv -= Lm[j][k] * Lm[j][k];
+            ok = ok && piv > 0.0;
+            const double ljj = sqrt(piv);
+            const double rinv = 1.0 / ljj;          // LAPACK dpotf2 scales the column by 1 / l_jj
+            Lm[j][j] = ljj;
+#pragma unroll
+            for (int i = j + 1; i < D; ++i) {
+                double t = Lm[i][j];
+#pragma unroll
+                for (int k = 0; k < j; ++k) t -= Lm[i][k] * Lm[j][k];
+                Lm[i][j] = t * rinv;
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+            for (int k = 0; k < D; ++k) L[i * D + k] = k <= i ? Lm[i][k] : 0.0;
+    }
+    ok = __shfl_sync(0xffffffffu, ok, 0);
+    __syncwarp();
+    return ok;
+}
+
+// Any size <= MAX_DIM: lane 0 forms the pivot of column j, lanes i > j the sub-diagonal entries.
 __device__ bool warp_chol(const double* A, double* L, int d, int lane) {
+    if (d == 8) return warp_chol_fixed<8>(A, L, lane);
     for (int i = lane; i < d * d; i += 32) L[i] = 0.0;
     __syncwarp();
     bool ok = true;
@@ -233,6 +279,7 @@ __host__ __device__ inline size_t rank_refit_smem(int n_cons, int n_elite, int d
 }
 
 constexpr int RANK_REFIT_THREADS = 1024;
+constexpr int REFIT_SUM_THREADS = 224;   // threads that take part in the refit sums (see rank_refit_block)
 
 // rank_samples + update_distribution + IterationStats + best record for one CEM
 // iteration, one CTA (1024 threads) per scene, on the residual order produced by
@@ -240,9 +287,19 @@ constexpr int RANK_REFIT_THREADS = 1024;
 // index, np.lexsort((idx, aug))) by counting in shared memory, the q elite set-point vectors
 // staged in shared memory and the weighted mean / covariance reduced warp-parallel in fp64; the
 // tail (Cholesky factor, IterationStats, best record) runs on separate warps concurrently.
-__global__ void __launch_bounds__(RANK_REFIT_THREADS) rank_refit_kernel(CemState s, int it, const int* order) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    const int scene = blockIdx.x;
+// The body runs on any CTA of <= 1024 threads (>= 4 warps): rank_refit_kernel (one CTA per scene)
+// and the single-scene persistent CEM kernel, whose last CTA to finish ranking runs it.
+#ifdef BD_PHASE_TIMING
+#define RR_STAMP(k) if (threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); rr_t[k] = t_; }
+#else
+#define RR_STAMP(k)
+#endif
+__device__ __forceinline__ void rank_refit_block(const CemState& s, int it, const int* order, int scene,
+                                                 unsigned char* smem) {
+#ifdef BD_PHASE_TIMING
+    __shared__ unsigned long long rr_t[12];
+#endif
+    RR_STAMP(0);
     const int d = s.dim;
     if (s.err[scene] != 0) {            // this iteration (or an earlier one) failed: freeze
         if (threadIdx.x == 0 && s.done[scene] == it) s.done[scene] = (it == 0) ? -1 : it;
@@ -274,26 +331,31 @@ __global__ void __launch_bounds__(RANK_REFIT_THREADS) rank_refit_kernel(CemState
         if (s.cons_idx) s.cons_idx[(size_t)scene * n + i] = j;
     }
     __syncthreads();
-    // rank among the constraint elites by (aug, sample index), scatter index and aug: four
-    // threads per elite, each counting the keys that precede it in a quarter of the list, the
-    // four counts summed with two shuffles (the group is four aligned lanes of one warp)
+    RR_STAMP(1);
+    // rank among the constraint elites by (aug, sample index), scatter index and aug: G threads per
+    // elite (G = 4, 2 or 1: one round whenever the CTA has G n threads), each counting, branch-free,
+    // the keys that precede it in a 1/G share of the list; the G counts meet by shuffles (the group
+    // is G aligned lanes of one warp)
     {
-        const int quarter = (n + 3) / 4;
-        for (int t0 = 0; t0 < 4 * n; t0 += blockDim.x) {
+        const int G = (int)blockDim.x >= 4 * n ? 4 : ((int)blockDim.x >= 2 * n ? 2 : 1);
+        const int share = (n + G - 1) / G;
+        for (int t0 = 0; t0 < G * n; t0 += blockDim.x) {
             const int t = t0 + threadIdx.x;
-            const int i = t >> 2, g = t & 3;
+            const int i = t / G, g = t % G;
             int rk = 0;
             if (i < n) {
                 const unsigned long long ki = key2[i];
                 const int ji = cidx[i];
-                const int k1 = min(n, (g + 1) * quarter);
-                for (int k = g * quarter; k < k1; ++k) {
+                const int k1 = min(n, (g + 1) * share);
+#pragma unroll 4
+                for (int k = g * share; k < k1; ++k) {
                     const unsigned long long kk = key2[k];
-                    rk += (kk < ki) || (kk == ki && cidx[k] < ji);
+                    const int ck = cidx[k];
+                    rk += (int)(kk < ki) | ((int)(kk == ki) & (int)(ck < ji));
                 }
             }
-            rk += __shfl_xor_sync(0xffffffffu, rk, 1);
-            rk += __shfl_xor_sync(0xffffffffu, rk, 2);
+            if (G >= 2) rk += __shfl_xor_sync(0xffffffffu, rk, 1);
+            if (G == 4) rk += __shfl_xor_sync(0xffffffffu, rk, 2);
             if (i < n && g == 0) {
                 BD_CHECK(rk >= 0 && rk < n);
                 idx2[rk] = cidx[i];
@@ -302,11 +364,18 @@ __global__ void __launch_bounds__(RANK_REFIT_THREADS) rank_refit_kernel(CemState
         }
     }
     __syncthreads();
+    RR_STAMP(2);
     // elite weights exp(-(aug - min aug)/gamma), uniform fallback (pkg/bilevel.py:163-172)
     const int j0 = idx2[0];
     const double amin = aug2[0];
     double part = 0.0, cpart = 0.0;
     const bool staged = q <= 128;
+    // the elite set-points are staged first so their L2 loads overlap the exp() below
+    if (staged) {
+        const int nq = q * d;
+#pragma unroll 4
+        for (int e = threadIdx.x; e < nq; e += blockDim.x) pe[e] = s.params[(base + idx2[e / d]) * d + e % d];
+    }
     for (int i = threadIdx.x; i < q; i += blockDim.x) {
         const int j = idx2[i];
         const double aug = aug2[i];
@@ -317,13 +386,13 @@ __global__ void __launch_bounds__(RANK_REFIT_THREADS) rank_refit_kernel(CemState
         if (s.elite_idx) s.elite_idx[(size_t)scene * q + i] = j;
         if (s.elite_aug) s.elite_aug[(size_t)scene * q + i] = aug;
     }
-    if (staged)
-        for (int e = threadIdx.x; e < q * d; e += blockDim.x) pe[e] = s.params[(base + idx2[e / d]) * d + e % d];
     const double total = block_sum(part, red);
     const double csum = block_sum(cpart, red);
+    RR_STAMP(3);
     const bool uniform = !(isfinite(total) && total > 0.0);
     for (int i = threadIdx.x; i < q; i += blockDim.x) w[i] = uniform ? 1.0 / q : w[i] / total;
     __syncthreads();
+    RR_STAMP(4);
     // weighted mean / covariance refit (pkg/bilevel.py:175-194): warp per output entry
     const double eta = s.eta;
     double* mean = s.mean + scene * d;
@@ -333,13 +402,20 @@ __global__ void __launch_bounds__(RANK_REFIT_THREADS) rank_refit_kernel(CemState
         return staged ? pe[i * d + r] : s.params[(base + idx2[i]) * d + r];
     };
     // every thread takes one entry and a strided chunk of the elites; the chunk partials are
-    // folded in a fixed order (deterministic)
+    // folded in a fixed order (deterministic).  The chunking uses at most REFIT_SUM_THREADS
+    // threads whatever the CTA size, so the 1024-thread kernel and the 224/256-thread persistent
+    // CEM kernel sum in the same order (bit-identical refits).
     __shared__ double partial[RANK_REFIT_THREADS];
+    const int nsum = min((int)blockDim.x, REFIT_SUM_THREADS);
+    // each chunk sum runs as four interleaved partial sums (elites i, i + 4 chunks, ...), added
+    // pairwise at the end: four independent fp64 chains instead of one
     {
-        const int chunks = blockDim.x / d, e = threadIdx.x % d, ch = threadIdx.x / d;
-        double acc = 0.0;
+        const int chunks = max(1, min(8, nsum / d)), e = threadIdx.x % d, ch = threadIdx.x / d;
+        double a4[4] = {0.0, 0.0, 0.0, 0.0};
         if (ch < chunks)
-            for (int i = ch; i < q; i += chunks) acc = fma(w[i], P(i, e), acc);
+#pragma unroll 4
+            for (int i = ch, u = 0; i < q; i += chunks, u = (u + 1) & 3) a4[u] = fma(w[i], P(i, e), a4[u]);
+        const double acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
         partial[threadIdx.x] = acc;
         __syncthreads();
         if (threadIdx.x < d) {
@@ -348,15 +424,19 @@ __global__ void __launch_bounds__(RANK_REFIT_THREADS) rank_refit_kernel(CemState
             mu_new[threadIdx.x] = (1.0 - eta) * mean[threadIdx.x] + eta * t;
         }
         __syncthreads();
+    RR_STAMP(5);
     }
     {
-        const int dd = d * d, chunks = blockDim.x / dd, e = threadIdx.x % dd, ch = threadIdx.x / dd;
+        const int dd = d * d, chunks = max(1, nsum / dd), e = threadIdx.x % dd, ch = threadIdx.x / dd;
         const int r = e / d, c = e % d;
-        double acc = 0.0;
+        double a4[4] = {0.0, 0.0, 0.0, 0.0};
         if (ch < chunks) {
             const double mr = mu_new[r], mc = mu_new[c];
-            for (int i = ch; i < q; i += chunks) acc = fma(w[i] * (P(i, r) - mr), P(i, c) - mc, acc);
+#pragma unroll 4
+            for (int i = ch, u = 0; i < q; i += chunks, u = (u + 1) & 3)
+                a4[u] = fma(w[i] * (P(i, r) - mr), P(i, c) - mc, a4[u]);
         }
+        const double acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
         partial[threadIdx.x] = acc;
         __syncthreads();
         if (threadIdx.x < dd) {
@@ -365,6 +445,7 @@ __global__ void __launch_bounds__(RANK_REFIT_THREADS) rank_refit_kernel(CemState
             cnew[threadIdx.x] = (1.0 - eta) * cov[threadIdx.x] + eta * t + (r == c ? 1e-6 : 0.0);
         }
         __syncthreads();
+    RR_STAMP(6);
     }
     for (int e = threadIdx.x; e < d * d; e += blockDim.x) {
         const int r = e / d, c = e % d;
@@ -374,8 +455,22 @@ __global__ void __launch_bounds__(RANK_REFIT_THREADS) rank_refit_kernel(CemState
     }
     if (threadIdx.x < d) mean[threadIdx.x] = mu_new[threadIdx.x];
     __syncthreads();
+    RR_STAMP(7);
     if (warp == 0) {
+#ifdef BD_PHASE_TIMING
+        const long long c0_ = clock64();
+#endif
         warp_sampling_factor(csym, lsh, s.L + scene * d * d, d, lane);
+        if (lane == 0) { RR_STAMP(9); }
+#ifdef BD_PHASE_TIMING
+        const long long c1_ = clock64();
+        if (lane == 0) printf("chol clock64 %lld cycles\n", c1_ - c0_);
+        if (lane == 0 && it == 1) {
+            printf("CSYM");
+            for (int q = 0; q < d * d; ++q) printf(" %.17g", csym[q]);
+            printf("\n");
+        }
+#endif
     } else if (warp == 1) {
         if (lane == 0) {
             // IterationStats (pkg/bilevel.py:282-292)
@@ -401,6 +496,21 @@ __global__ void __launch_bounds__(RANK_REFIT_THREADS) rank_refit_kernel(CemState
     } else if (warp == 3) {
         if (lane < NX && s.xi) s.best_xi[scene * NX + lane] = s.xi[(base + j0) * NX + lane];
     }
+#ifdef BD_PHASE_TIMING
+    __syncthreads();
+    RR_STAMP(8);
+    if (threadIdx.x == 0) printf("chol %.2f us\n", (rr_t[9] - rr_t[7]) * 1e-3);
+    if (threadIdx.x == 0)
+        printf("refit phases (us): load %.2f rank %.2f weights %.2f norm %.2f mean %.2f cov %.2f sym %.2f tail %.2f\n",
+               (rr_t[1] - rr_t[0]) * 1e-3, (rr_t[2] - rr_t[1]) * 1e-3, (rr_t[3] - rr_t[2]) * 1e-3,
+               (rr_t[4] - rr_t[3]) * 1e-3, (rr_t[5] - rr_t[4]) * 1e-3, (rr_t[6] - rr_t[5]) * 1e-3,
+               (rr_t[7] - rr_t[6]) * 1e-3, (rr_t[8] - rr_t[7]) * 1e-3);
+#endif
+}
+
+__global__ void __launch_bounds__(RANK_REFIT_THREADS) rank_refit_kernel(CemState s, int it, const int* order) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    rank_refit_block(s, it, order, blockIdx.x, smem);
 }
 
 }  // namespace bd

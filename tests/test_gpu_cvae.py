@@ -5,6 +5,7 @@ import numpy as np
 import pytest
 
 from oracle.cvae import decode as decode_ref
+from oracle.cvae import decode_bf16
 
 pytestmark = pytest.mark.gpu
 
@@ -25,18 +26,51 @@ def test_cvae_decoder_fp32_matches_float64_restatement():
 
 @pytest.mark.parametrize("count", [1000, 128, 77])
 def test_cvae_decoder_tcgen05_bf16(count):
-    """Hidden layers on tcgen05 (bf16 operands, fp32 TMEM accumulation): bf16 rounding bound."""
+    """Hidden layers on tcgen05 (bf16 operands, fp32 TMEM accumulation) against a float64
+    restatement that rounds weights and activations to bf16 exactly where the kernel does
+    (oracle.cvae.decode_bf16): what is left is the fp32 accumulation order inside the tensor core
+    and the bf16 rounding flips it causes (an activation one bf16 ulp away, ~2e-3 relative, for a
+    few of the 4096 activations of a sample): measured max 2.6e-3 - 4.8e-3, mean 1.3e-4 - 1.5e-4
+    of the output scale.  A wrong swizzle, descriptor or epilogue mapping gives O(1) errors.  The
+    bit-exact layer test below pins the GEMM itself; the plain float64 decoder bounds the total
+    bf16 error."""
     from paper_2212_02224_b200.cvae import CVAEDecoder
     dec = CVAEDecoder.synthetic(7)
     rng = np.random.default_rng(1)
     obs = rng.standard_normal(55).astype(np.float32)
     z = rng.standard_normal((count, 2)).astype(np.float32)
     got = dec.decode(obs, z)
+    emu = decode_bf16(dec.W, dec.b, obs, z)
+    scale = np.abs(emu).max()
+    err = np.abs(got - emu)
+    print(f"bf16-emulated: max {err.max() / scale:.2e} mean {err.mean() / scale:.2e} of the output scale")
+    assert err.max() <= 1e-2 * scale, err.max() / scale
+    assert err.mean() <= 3e-4 * scale, err.mean() / scale
     ref = decode_ref(dec.W, dec.b, obs, z)
-    scale = np.abs(ref).max()
-    err = np.abs(got - ref)
-    assert err.max() <= 5e-2 * scale, err.max() / scale
-    assert err.mean() <= 1e-2 * scale, err.mean() / scale
+    assert np.abs(got - ref).max() <= 5e-2 * np.abs(ref).max()
+
+
+def test_cvae_tcgen05_layer_bit_exact():
+    """One tcgen05 hidden layer on inputs whose every product and partial sum is exact in fp32
+    (multiples of 1/64 with few significant bits): any accumulation order gives the same fp32
+    value, so the bf16 output must equal the float64 restatement bit for bit.  The last layer
+    selects every 8th activation with weight 1.0 (exact), so the decoder output IS the tcgen05
+    layer's bf16 activations.  Pins the TMA swizzle, UMMA descriptors and the TMEM epilogue."""
+    from paper_2212_02224_b200.cvae import CVAEDecoder
+    rng = np.random.default_rng(11)
+    W0 = np.zeros((256, 57), np.float32)
+    W0[:, 55:] = rng.integers(-4, 5, (256, 2)) / 64.0           # latent part; obs = 0
+    b0 = (rng.integers(-8, 9, 256) / 64.0).astype(np.float32)
+    W1 = (rng.integers(-7, 8, (1024, 256)) / 64.0).astype(np.float32)   # bf16-exact
+    b1 = (rng.integers(-64, 65, 1024) / 4096.0).astype(np.float32)
+    W2 = np.zeros((128, 1024), np.float32)
+    W2[np.arange(128), 8 * np.arange(128)] = 1.0
+    b2 = np.zeros(128, np.float32)
+    dec = CVAEDecoder([W0, W1, W2], [b0, b1, b2])
+    z = rng.integers(-3, 4, (300, 2)).astype(np.float32)
+    got = dec.decode(np.zeros(55), z)
+    np.testing.assert_array_equal(got, decode_bf16(dec.W, dec.b, np.zeros(55), z))
+    assert np.count_nonzero(got) > 0.2 * got.size                 # ReLU leaves plenty of signal
 
 
 def test_cvae_odd_sizes_and_errors():
@@ -69,6 +103,9 @@ def test_config3_cvae_warm_start_then_cem():
     res = bd.solve_bilevel(scene, solver, cfg, np.random.default_rng(6), warm_start=ws)
     assert not res.degraded and len(res.diagnostics) == 4
     assert np.isfinite(res.best.upper_cost)
-    # iteration 1 ranked the decoder's samples: the best record's set-points are one of them
-    if res.best.index >= 0 and len(res.diagnostics) == 1:
-        assert np.any(np.all(np.isclose(ws.samples, res.best.params.to_vector()), axis=1))
+    # a one-iteration cycle ranks only the decoder's samples: its best record's set-points are
+    # exactly the decoder sample at the best index
+    one = bd.solve_bilevel(scene, solver, bd.BiLevelConfig(1000, 150, 100, 1, 0.7, 0.9, 1.0, mean, cov),
+                           np.random.default_rng(6), warm_start=ws)
+    assert len(one.diagnostics) == 1 and 0 <= one.best.index < 1000
+    np.testing.assert_array_equal(one.best.params.to_vector(), ws.samples[one.best.index])
