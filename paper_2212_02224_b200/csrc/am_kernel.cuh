@@ -123,8 +123,9 @@ constexpr int SORT_MIN_PAIRS = BD_SORT_MIN_PAIRS;   // >= 16 obstacles: sorted-w
 
 // Shared-memory carve-up, identical on host and device.
 struct AmSmem {
-    size_t w, obs, k, kb, a, curv, scr, dap, kap, kix, total;
-    __host__ __device__ AmSmem(int m, int n_obs, int neq, int n_curv, int s_cta, int threads, int P, bool curv_on) {
+    size_t w, obs, k, kb, a, curv, scr, dap, kap, kix, itm, total;
+    __host__ __device__ AmSmem(int m, int n_obs, int neq, int n_curv, int s_cta, int threads, int P, bool curv_on,
+                               int max_iters) {
         const int J = (m + P - 1) / P;
         size_t o = 0;
         w = o;    o = align_up(o + (size_t)m * WROW * 4, 16);
@@ -138,6 +139,8 @@ struct AmSmem {
         kap = o;  o = align_up(o + (curv_on ? (size_t)J * threads * 4 : 0), 16);
         // dense scenes: each (timestep slot, thread)'s window start of the previous iteration
         kix = o;  o = align_up(o + (n_obs >= 2 * SORT_MIN_PAIRS ? (size_t)J * threads * 2 : 0), 16);
+        // the CTA's per-iteration residual maxima (float bits), flushed to the global table once
+        itm = o;  o = align_up(o + (size_t)max_iters * 4, 16);
         total = o;
     }
     // per-sample scratch: u (24 doubles) | c32 (24 floats) | lambda-state l (24 doubles) | first-step
@@ -591,6 +594,9 @@ __device__ __forceinline__ void pair_sync() {
     asm volatile("bar.sync %0, 64;" ::"r"(1 + (int)(threadIdx.x >> 6)) : "memory");
 }
 
+#ifndef BD_NO_ITMAX
+#define BD_NO_ITMAX 0      // diagnostic builds only: drop the per-iteration batch-max atomics
+#endif
 #ifndef BD_AM_MINB
 #define BD_AM_MINB 2       // x 256 threads: 128 registers per thread
 #endif
@@ -600,7 +606,7 @@ template <int P, bool CURV>
 __device__ __forceinline__ void am_stage(const AmArgs& a, int scene, unsigned char* smem, uint64_t* stage_bar) {
     const int m = a.m, neq = a.neq, n_obs = a.n_obs;
     const int threads = blockDim.x;
-    const AmSmem lay(m, n_obs, neq, a.n_curv, a.s_cta, threads, P, CURV);
+    const AmSmem lay(m, n_obs, neq, a.n_curv, a.s_cta, threads, P, CURV, a.max_iters);
     float* wsm = reinterpret_cast<float*>(smem + lay.w);
     float4* osm = reinterpret_cast<float4*>(smem + lay.obs);
     double* ksm = reinterpret_cast<double*>(smem + lay.k);
@@ -639,7 +645,7 @@ __device__ __forceinline__ void am_samples(const AmArgs& a, int scene, int blk, 
     constexpr int ROWS = (NX + RP - 1) / RP;         // coefficient rows owned per lane
     const int m = a.m, neq = a.neq, n_obs = a.n_obs;
     const int threads = blockDim.x;
-    const AmSmem lay(m, n_obs, neq, a.n_curv, a.s_cta, threads, P, CURV);
+    const AmSmem lay(m, n_obs, neq, a.n_curv, a.s_cta, threads, P, CURV, a.max_iters);
     float* wsm = reinterpret_cast<float*>(smem + lay.w);
     float4* osm = reinterpret_cast<float4*>(smem + lay.obs);
     double* ksm = reinterpret_cast<double*>(smem + lay.k);
@@ -727,8 +733,15 @@ __device__ __forceinline__ void am_samples(const AmArgs& a, int scene, int blk, 
     const int r_lane = NX % RP, r_slot = (NX / RP) * RP;
     const int c_lane = (NX + 1) % RP, c_slot = ((NX + 1) / RP) * RP;
     float resid = 0.f, cost = 0.f;
-    const int warp_global = (blk < 0 ? (int)blockIdx.x : blk) * (threads / 32) + (threadIdx.x >> 5);
-    unsigned* itm = a.itmax + (size_t)scene * a.max_iters * ITMAX_SLOTS + (warp_global % ITMAX_SLOTS);
+    const int cta = blk < 0 ? (int)blockIdx.x : blk;
+    // per-iteration batch maxima: shared-memory atomics during the loop, one global atomic per
+    // (CTA, iteration) afterwards (per-iteration global atomics cost 8 % of the latency launch)
+    unsigned* itm_s = reinterpret_cast<unsigned*>(smem + lay.itm);
+    const bool record = a.replay == nullptr && !BD_NO_ITMAX;
+    if (record) {
+        for (int t = threadIdx.x; t < iters; t += threads) itm_s[t] = 0u;
+        __syncthreads();
+    }
 
     for (int it = 0; it < iters; ++it) {
         // ---- coefficient update: lambda step, then c <- c + K (l - c - rho g) (+ delta on the first step)
@@ -787,19 +800,25 @@ __device__ __forceinline__ void am_samples(const AmArgs& a, int scene, int blk, 
         const bool owner = (own == r_lane);
         if (a.hist_out && owner && active)
             a.hist_out[((size_t)scene * a.max_iters + it) * a.B + local] = resid;
-        if (a.replay == nullptr) {
+        if (record) {
             const float rk = resid != resid ? INFINITY : resid;   // a NaN never passes the exit test
             float mx = owner ? rk : 0.f;
             if (P < 32) {
 #pragma unroll
                 for (int o = 16; o >= 1; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-                if (lane == 0) atomicMax(itm + (size_t)it * ITMAX_SLOTS, float_key(mx));
+                if (lane == 0) atomicMax(itm_s + it, float_key(mx));
             } else if (owner) {
-                atomicMax(itm + (size_t)it * ITMAX_SLOTS, float_key(rk));
+                atomicMax(itm_s + it, float_key(rk));
             }
         }
     }
 
+    if (record) {
+        __syncthreads();
+        unsigned* itm = a.itmax + (size_t)scene * a.max_iters * ITMAX_SLOTS + (cta % ITMAX_SLOTS);
+        for (int t = threadIdx.x; t < iters; t += threads)
+            if (const unsigned v = itm_s[t]) atomicMax(itm + (size_t)t * ITMAX_SLOTS, v);
+    }
     // ---- outputs (out-of-range samples: stage-1 coefficients, +inf residual and cost)
     {
         constexpr unsigned gmask = RP >= 32 ? 0xffffffffu : ((1u << (RP & 31)) - 1u);

@@ -359,7 +359,7 @@ void raise_smem(K kernel, size_t bytes) {
 
 template <int P, bool CURV, int MT = 0, int NPT = 0, int TPB = 0, bool LAT = false>
 int launch_am_t(bd_ctx* ctx, AmArgs a, int threads, bool replay_pass, int* occ = nullptr) {
-    const AmSmem lay(a.m, a.n_obs, a.neq, a.n_curv, a.s_cta, threads, P, CURV);
+    const AmSmem lay(a.m, a.n_obs, a.neq, a.n_curv, a.s_cta, threads, P, CURV, a.max_iters);
     if (lay.total > 227 * 1024) return fail(ctx, BD_ERR_VALUE, "AM kernel needs %zu B of shared memory", lay.total);
     raise_smem(am_kernel<P, CURV, MT, NPT, TPB, LAT>, lay.total);
     if (occ) {   // occupancy query only (lane-mapping choice)
@@ -1422,7 +1422,7 @@ static int try_cem_persistent(bd_ctx* ctx, const bd_cem_config* cfg, const CemSt
     pa.params = ctx->w_params.as<double>();
     pa.order = ctx->w_order.as<int>();
     pa.bar = ctx->c_bar.as<unsigned>();
-    const AmSmem lay(ctx->m, ctx->obs_pad, ctx->neq, 0, spc, threads, 32, false);
+    const AmSmem lay(ctx->m, ctx->obs_pad, ctx->neq, 0, spc, threads, 32, false, iters);
     pa.s1_off = align_up(lay.total, 16);
     const size_t s1_bytes = (size_t)(2 * s1.nr * s1_ld(s1.nr) + 2 * NC * s1.m_seg + spc * MAX_DIM + spc * S1_VEC) * 8;
     pa.key_off = align_up(pa.s1_off + s1_bytes, 16);

@@ -29,7 +29,12 @@
 
 namespace bd {
 
-#ifdef BD_PHASE_TIMING   // diagnostic build: per-phase %globaltimer stamps printed by CTA 0 / the last CTA
+#ifdef BD_PHASE_TIMING   // diagnostic build: per-phase %globaltimer stamps printed by every worker CTA
+__device__ __forceinline__ unsigned __smid() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+    return r;
+}
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -232,10 +237,10 @@ __global__ void __launch_bounds__(TPB, 1) cem_persistent_kernel(const CemPersist
         BD_STAMP(7);
         if (ld_acquire_gpu(p.bar + 2) != 0u) break;      // the control CTA froze the scene
 #ifdef BD_PHASE_TIMING
-        if (threadIdx.x == 0 && blockIdx.x == 0)
-            printf("it %d cta0: S %.2f A %.2f bar1 %.2f R %.2f bar2 %.2f us\n", it, (stamp[1] - stamp[0]) * 1e-3,
-                   (stamp[2] - stamp[1]) * 1e-3, (stamp[3] - stamp[2]) * 1e-3, (stamp[4] - stamp[3]) * 1e-3,
-                   (stamp[7] - stamp[4]) * 1e-3);
+        if (threadIdx.x == 0)
+            printf("PH it %d cta %d smid %d: S %.2f A %.2f bar1 %.2f R %.2f bar2 %.2f Aend %.2f\n", it, blockIdx.x,
+                   __smid(), (stamp[1] - stamp[0]) * 1e-3, (stamp[2] - stamp[1]) * 1e-3, (stamp[3] - stamp[2]) * 1e-3,
+                   (stamp[4] - stamp[3]) * 1e-3, (stamp[7] - stamp[4]) * 1e-3, (stamp[2] % 1000000000ull) * 1e-3);
 #endif
     }
 }
