@@ -20,6 +20,7 @@
 #include "aux_kernels.cuh"
 #include "cvae_kernel.cuh"
 #include "cvae_tc.cuh"
+#include "cvae_fused.cuh"
 #include <cudaTypedefs.h>
 #include "scene_kernels.cuh"
 #include "sim_kernels.cuh"
@@ -94,6 +95,19 @@ struct bd_ctx {
     DevBuf out_pack;              // coalesced device->host outputs: gathered here, one D2H copy
     void* out_pin = nullptr;      // pinned host staging for out_pack
     size_t out_pin_bytes = 0;
+    // pinned host staging of a call's host inputs: one CPU memcpy + an asynchronous DMA each
+    // (a pageable cudaMemcpyAsync is a synchronous driver copy); reused once the event has passed
+    void* in_pin = nullptr;
+    size_t in_pin_bytes = 0, in_pin_off = 0;
+    cudaEvent_t in_pin_ev = nullptr;
+    bool in_pin_pending = false;
+    // fused CVAE: tensor maps of the last (count, activation buffer, weights) configuration
+    int fz_count = -1;
+    const void* fz_key_a = nullptr;
+    const void* fz_key_w = nullptr;
+    FusedMaps fz_maps;
+    unsigned fz_epoch = 0;
+    int fz_ctr_mblocks = -1;
     std::vector<PendingCopy> pending;
     bool host_out = false;
     // CEM state
@@ -113,7 +127,9 @@ struct bd_ctx {
     std::vector<int> cvae_dims;
     std::vector<DevBuf*> cvae_w, cvae_b, cvae_w16;
     DevBuf cvae_h0, cvae_h1, cvae_obs, cvae_z, cvae_a0, cvae_a1;
+    DevBuf cvae_ready;          // fused decoder's arrival counters (persist across launches)
     int cvae_tc = 1;            // option "cvae_tensor_cores": bf16 tcgen05 hidden layers (1) or fp32 SIMT (0)
+    int cvae_fused = 1;         // option "cvae_fused": the whole decoder in one persistent launch (1) or per layer (0)
     bool err_sticky = false;    // option "sticky_errors": entry points accumulate into the error word
                                 // instead of clearing it (multi-call loops read it once at the end)
     ~bd_ctx() {
@@ -123,6 +139,9 @@ struct bd_ctx {
         for (auto* b : cvae_b) delete b;
         for (auto* b : cvae_w16) delete b;
         if (out_pin) cudaFreeHost(out_pin);
+        if (in_pin_ev) cudaEventSynchronize(in_pin_ev);
+        if (in_pin) cudaFreeHost(in_pin);
+        if (in_pin_ev) cudaEventDestroy(in_pin_ev);
     }
 };
 
@@ -200,8 +219,35 @@ int stage_in(bd_ctx* ctx, const T* p, size_t count, const T** out) {
     if (!p || count == 0 || is_device_ptr(p)) { *out = p; return 0; }
     if (ctx->n_stage >= 8) return fail(ctx, BD_ERR_STATE, "too many staged inputs");
     DevBuf& b = ctx->stage[ctx->n_stage++];
-    CU(b.ensure(count * sizeof(T)));
-    CU(cudaMemcpyAsync(b.p, p, count * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+    const size_t bytes = count * sizeof(T);
+    CU(b.ensure(bytes));
+    // the previous call's DMAs must have left the pinned buffer before it is overwritten
+    if (ctx->in_pin_pending && ctx->in_pin_off == 0) {
+        CU(cudaEventSynchronize(ctx->in_pin_ev));
+        ctx->in_pin_pending = false;
+    }
+    const size_t need = ctx->in_pin_off + (bytes + 255) / 256 * 256;
+    if (need > ctx->in_pin_bytes) {
+        if (ctx->in_pin_off == 0) {        // grow between calls only (no DMA of this call in flight)
+            if (ctx->in_pin) cudaFreeHost(ctx->in_pin);
+            ctx->in_pin = nullptr;
+            ctx->in_pin_bytes = 0;
+            const size_t want = std::max(need, (size_t)1 << 20) * 2;
+            CU(cudaHostAlloc(&ctx->in_pin, want, cudaHostAllocDefault));
+            ctx->in_pin_bytes = want;
+            if (!ctx->in_pin_ev) CU(cudaEventCreateWithFlags(&ctx->in_pin_ev, cudaEventDisableTiming));
+        } else {                           // does not fit behind this call's other inputs: pageable copy
+            CU(cudaMemcpyAsync(b.p, p, bytes, cudaMemcpyHostToDevice, ctx->stream));
+            *out = b.as<T>();
+            return 0;
+        }
+    }
+    unsigned char* pin = static_cast<unsigned char*>(ctx->in_pin) + ctx->in_pin_off;
+    std::memcpy(pin, p, bytes);
+    CU(cudaMemcpyAsync(b.p, pin, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaEventRecord(ctx->in_pin_ev, ctx->stream));
+    ctx->in_pin_off = need;
+    ctx->in_pin_pending = true;
     *out = b.as<T>();
     return 0;
 }
@@ -251,6 +297,7 @@ cudaError_t clear_err(bd_ctx* ctx, size_t bytes) {
 
 void begin_call(bd_ctx* ctx) {
     ctx->n_stage = 0;
+    ctx->in_pin_off = 0;
     ctx->pending.clear();
     ctx->host_out = false;
     cudaSetDevice(ctx->device);
@@ -278,10 +325,6 @@ int flush_outputs(bd_ctx* ctx) {
     auto& pend = ctx->pending;
     if (pend.empty()) return 0;
     const bool single = pend.size() == 1 && pend[0].src_stride == 0;
-    if (single) {
-        CU(cudaMemcpyAsync(pend[0].dst, pend[0].src, pend[0].bytes, cudaMemcpyDeviceToHost, ctx->stream));
-        return 0;
-    }
     std::vector<size_t> off(pend.size());
     size_t total = 0;
     for (size_t i = 0; i < pend.size(); ++i) { off[i] = total; total += (pend[i].bytes + 15) / 16 * 16; }
@@ -294,7 +337,9 @@ int flush_outputs(bd_ctx* ctx) {
         CU(cudaHostAlloc(&ctx->out_pin, want, cudaHostAllocDefault));
         ctx->out_pin_bytes = want;
     }
-    for (size_t b = 0; b < pend.size(); b += GATHER_MAX) {
+    // one contiguous output goes straight to the pinned buffer (no gather)
+    const void* pack_src = single ? pend[0].src : ctx->out_pack.p;
+    for (size_t b = 0; !single && b < pend.size(); b += GATHER_MAX) {
         GatherArgs g{};
         g.n = (int)std::min(pend.size() - b, (size_t)GATHER_MAX);
         g.pack = ctx->out_pack.as<unsigned char>();
@@ -308,7 +353,7 @@ int flush_outputs(bd_ctx* ctx) {
         gather_kernel<<<dim3(gx, g.n), 256, 0, ctx->stream>>>(g);
         ctx->launches++;
     }
-    CU(cudaMemcpyAsync(ctx->out_pin, ctx->out_pack.p, total, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(ctx->out_pin, pack_src, single ? pend[0].bytes : total, cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
     for (size_t i = 0; i < pend.size(); ++i)
         std::memcpy(pend[i].dst, static_cast<unsigned char*>(ctx->out_pin) + off[i], pend[i].bytes);
@@ -667,6 +712,10 @@ int bd_set_option(bd_ctx* ctx, const char* key, int value) {
     }
     if (!strcmp(key, "cvae_tensor_cores")) {
         ctx->cvae_tc = value != 0;
+        return 0;
+    }
+    if (!strcmp(key, "cvae_fused")) {
+        ctx->cvae_fused = value != 0;
         return 0;
     }
     if (!strcmp(key, "timing")) {
@@ -1719,6 +1768,7 @@ int bd_cvae_set_weights(bd_ctx* ctx, int n_layers, const int* dims, const float*
     ctx->cvae_b.clear();
     ctx->cvae_w16.clear();
     ctx->cvae_dims.assign(dims, dims + n_layers + 1);
+    ctx->fz_count = -1;                  // cached fused-decoder tensor maps refer to the old weights
     for (int l = 0; l < n_layers; ++l) {
         const size_t nw = (size_t)dims[l] * dims[l + 1], nb = dims[l + 1];
         if (dims[l] < 1 || dims[l + 1] < 1) return fail(ctx, BD_ERR_VALUE, "bad layer dims");
@@ -1756,13 +1806,13 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     return fn;
 }
 
-// 2-D bf16 row-major [rows x cols] tensor map with a 128-row x 64-col box and 128-byte swizzle.
-bool make_map_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols) {
+// 2-D bf16 row-major [rows x cols] tensor map with a box_rows x 64-col box and 128-byte swizzle.
+bool make_map_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows = TC_BM) {
     auto enc = tensor_map_encoder();
     if (!enc) return false;
     const cuuint64_t dims[2] = {cols, rows};
     const cuuint64_t strides[1] = {cols * 2};
-    const cuuint32_t box[2] = {(cuuint32_t)TC_BK, (cuuint32_t)TC_BM};
+    const cuuint32_t box[2] = {(cuuint32_t)TC_BK, (cuuint32_t)box_rows};
     const cuuint32_t estr[2] = {1, 1};
     return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -1787,6 +1837,77 @@ int bd_cvae_decode(bd_ctx* ctx, int count, const float* obs, const float* z, dou
     for (int l = 1; l <= L; ++l) widest = widest > d[l] ? widest : d[l];
     bool tc_ok = ctx->cvae_tc && L >= 3 && tensor_map_encoder() != nullptr;
     for (int l = 1; l < L - 1 && tc_ok; ++l) tc_ok = d[l] % TC_BK == 0 && d[l + 1] % TC_BN == 0;
+    // the whole decoder as one persistent cooperative kernel (csrc/cvae_fused.cuh)
+    bool fused_ok = tc_ok && ctx->cvae_fused && L - 2 <= FZ_MAXH && d[L] <= FZ_MAXOUT && zdim <= FZ_MAXZ / 2;
+    for (int l = 1; l < L && fused_ok; ++l) fused_ok = d[l] % FZ_BN == 0 && d[l] % FZ_BK == 0;
+    if (fused_ok) {
+        int sms = 148, coop = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->device);
+        const int nh = L - 2, mblocks = (count + FZ_BM - 1) / FZ_BM;
+        int tiles = 0;
+        for (int l = 0; l <= nh; ++l) tiles = std::max(tiles, mblocks * (d[l + 1] / FZ_BN));
+        const int grid = std::min(tiles, sms);
+        if (coop) {
+            const size_t mpad = (size_t)mblocks * FZ_BM;
+            size_t act_elems = 0;                 // one buffer per layer (rows of a block flow through layers)
+            for (int l = 0; l < nh; ++l) act_elems += mpad * d[l + 1];
+            CU(ctx->cvae_a0.ensure(act_elems * 2));
+            CU(ctx->cvae_h0.ensure((size_t)(d[L - 1] / FZ_BN) * count * d[L] * 4));
+            // arrival counters grow by (tiles per row block) each launch; reset when (re)allocated,
+            // when the layout changes or long before they could wrap
+            const size_t ctr_bytes = (size_t)(nh + 1) * mblocks * 4;
+            if (ctx->cvae_ready.bytes < ctr_bytes || ctx->fz_ctr_mblocks != mblocks || ctx->fz_epoch >= (1u << 20)) {
+                CU(ctx->cvae_ready.ensure(ctr_bytes));
+                CU(cudaMemsetAsync(ctx->cvae_ready.p, 0, ctx->cvae_ready.bytes, ctx->stream));
+                ctx->fz_epoch = 0;
+                ctx->fz_ctr_mblocks = mblocks;
+            }
+            ++ctx->fz_epoch;
+            double* dout;
+            DevBuf& ws = ctx->stage[7];
+            if ((rc = stage_out(ctx, params, (size_t)count * d[L], ws, &dout))) return rc;
+            FusedArgs fa{};
+            FusedMaps fm{};
+            fa.count = count; fa.nh = nh; fa.zdim = zdim;
+            for (int l = 0; l <= L; ++l) fa.dims[l] = d[l];
+            fa.W0 = ctx->cvae_w[0]->as<float>();
+            for (int l = 0; l < L; ++l) fa.bias[l] = ctx->cvae_b[l]->as<float>();
+            fa.Wlast = ctx->cvae_w[L - 1]->as<float>();
+            fa.obs = dobs; fa.z = dz;
+            size_t off = 0;
+            for (int l = 0; l < nh; ++l) {
+                fa.act[l] = ctx->cvae_a0.as<__nv_bfloat16>() + off;
+                off += mpad * d[l + 1];
+            }
+            fa.act[nh] = nullptr;                 // the last hidden layer feeds the fused output layer
+            fa.partial = ctx->cvae_h0.as<float>();
+            fa.out = dout;
+            fa.ready = ctx->cvae_ready.as<unsigned>();
+            fa.epoch = ctx->fz_epoch;
+            if (ctx->fz_count != count || ctx->fz_key_a != ctx->cvae_a0.p || ctx->fz_key_w != ctx->cvae_w16[1]->p) {
+                ctx->fz_count = -1;
+                for (int h = 0; h < nh; ++h) {
+                    const int l = h + 1;
+                    if (!make_map_bf16(&ctx->fz_maps.a[h], fa.act[l - 1], (uint64_t)count, (uint64_t)d[l], FZ_BM) ||
+                        !make_map_bf16(&ctx->fz_maps.b[h], ctx->cvae_w16[l]->p, (uint64_t)d[l + 1], (uint64_t)d[l],
+                                       FZ_BN))
+                        return fail(ctx, BD_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+                }
+                ctx->fz_count = count;
+                ctx->fz_key_a = ctx->cvae_a0.p;
+                ctx->fz_key_w = ctx->cvae_w16[1]->p;
+            }
+            fm = ctx->fz_maps;
+            raise_smem(cvae_fused_kernel, FZ_SMEM);
+            void* args[] = {&fm, &fa};
+            cudaError_t e = cudaLaunchCooperativeKernel((const void*)cvae_fused_kernel, dim3(grid), dim3(128), args,
+                                                        FZ_SMEM, ctx->stream);
+            if (e != cudaSuccess) return fail(ctx, BD_ERR_CUDA, "fused CVAE launch: %s", cudaGetErrorString(e));
+            ctx->launches++;
+            return finish_call(ctx, false, 0);
+        }
+    }
     if (tc_ok) {
         const int mpad = (count + TC_BM - 1) / TC_BM * TC_BM;
         CU(ctx->cvae_a0.ensure((size_t)mpad * widest * 2));

@@ -346,13 +346,23 @@ __device__ __forceinline__ void rank_refit_block(const CemState& s, int it, cons
             if (i < n) {
                 const unsigned long long ki = key2[i];
                 const int ji = cidx[i];
-                const int k1 = min(n, (g + 1) * share);
-#pragma unroll 4
-                for (int k = g * share; k < k1; ++k) {
-                    const unsigned long long kk = key2[k];
-                    const int ck = cidx[k];
-                    rk += (int)(kk < ki) | ((int)(kk == ki) & (int)(ck < ji));
+                const int k0 = g * share, k1 = min(n, (g + 1) * share);
+                // eight keys per step, four independent counts (the loads of a step overlap)
+                int c4[4] = {0, 0, 0, 0};
+                int k = k0;
+                for (; k + 8 <= k1; k += 8) {
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const unsigned long long kk = key2[k + u];
+                        const int ck = cidx[k + u];
+                        c4[u & 3] += (int)(kk < ki) | ((int)(kk == ki) & (int)(ck < ji));
+                    }
                 }
+                for (; k < k1; ++k) {
+                    const unsigned long long kk = key2[k];
+                    c4[0] += (int)(kk < ki) | ((int)(kk == ki) & (int)(cidx[k] < ji));
+                }
+                rk = (c4[0] + c4[1]) + (c4[2] + c4[3]);
             }
             if (G >= 2) rk += __shfl_xor_sync(0xffffffffu, rk, 1);
             if (G == 4) rk += __shfl_xor_sync(0xffffffffu, rk, 2);
@@ -399,7 +409,7 @@ __device__ __forceinline__ void rank_refit_block(const CemState& s, int it, cons
     double* cov = s.cov + scene * d * d;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     auto P = [&](int i, int r) -> double {
-        return staged ? pe[i * d + r] : s.params[(base + idx2[i]) * d + r];
+        return staged ? pe[i * d + r] : __ldg(s.params + (base + idx2[i]) * d + r);
     };
     // every thread takes one entry and a strided chunk of the elites; the chunk partials are
     // folded in a fixed order (deterministic).  The chunking uses at most REFIT_SUM_THREADS
@@ -457,20 +467,8 @@ __device__ __forceinline__ void rank_refit_block(const CemState& s, int it, cons
     __syncthreads();
     RR_STAMP(7);
     if (warp == 0) {
-#ifdef BD_PHASE_TIMING
-        const long long c0_ = clock64();
-#endif
         warp_sampling_factor(csym, lsh, s.L + scene * d * d, d, lane);
         if (lane == 0) { RR_STAMP(9); }
-#ifdef BD_PHASE_TIMING
-        const long long c1_ = clock64();
-        if (lane == 0) printf("chol clock64 %lld cycles\n", c1_ - c0_);
-        if (lane == 0 && it == 1) {
-            printf("CSYM");
-            for (int q = 0; q < d * d; ++q) printf(" %.17g", csym[q]);
-            printf("\n");
-        }
-#endif
     } else if (warp == 1) {
         if (lane == 0) {
             // IterationStats (pkg/bilevel.py:282-292)
@@ -499,7 +497,8 @@ __device__ __forceinline__ void rank_refit_block(const CemState& s, int it, cons
 #ifdef BD_PHASE_TIMING
     __syncthreads();
     RR_STAMP(8);
-    if (threadIdx.x == 0) printf("chol %.2f us\n", (rr_t[9] - rr_t[7]) * 1e-3);
+    if (threadIdx.x == 0)
+        printf("refit phases (us): chol %.2f; ", (rr_t[9] - rr_t[7]) * 1e-3);
     if (threadIdx.x == 0)
         printf("refit phases (us): load %.2f rank %.2f weights %.2f norm %.2f mean %.2f cov %.2f sym %.2f tail %.2f\n",
                (rr_t[1] - rr_t[0]) * 1e-3, (rr_t[2] - rr_t[1]) * 1e-3, (rr_t[3] - rr_t[2]) * 1e-3,

@@ -71,6 +71,9 @@ __device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
 // Barrier words (p.bar): [0] arrivals of the worker CTAs, [1] generation released by the control
 // CTA, [2] the control CTA's stop verdict (scene frozen after a failed iteration).  A worker reads the generation before arriving, so a release is never missed; every wait
 // gives up after ~10 s (a CTA that never arrives) and flags ERR_P2P_TIMEOUT instead of hanging.
+#ifndef BD_POLL_NS
+#define BD_POLL_NS 32
+#endif
 __device__ __forceinline__ void worker_arrive_wait(unsigned* bar, int* err) {
     __shared__ unsigned s_gen;
     __syncthreads();
@@ -80,7 +83,7 @@ __device__ __forceinline__ void worker_arrive_wait(unsigned* bar, int* err) {
         atomicAdd(bar, 1u);
         long long spins = 0;
         while (ld_acquire_gpu(bar + 1) == s_gen) {
-            __nanosleep(32);
+            __nanosleep(BD_POLL_NS);
             if (++spins > (1ll << 28)) { atomicOr(err, ERR_P2P_TIMEOUT); break; }
         }
     }
