@@ -70,6 +70,20 @@ __device__ __forceinline__ void tma_load_2d_fz(void* dst, const CUtensorMap* map
         : "memory");
 }
 
+// mbarrier wait that traps after ~2 s instead of spinning forever (a lost arrival must fail the
+// launch, not hang the GPU)
+__device__ __forceinline__ void mbar_wait_fz(uint64_t* bar, uint32_t parity) {
+    const long long t0 = clock64();
+    uint32_t ok = 0;
+    while (true) {
+        asm volatile(
+            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+        if (ok) return;
+        if (clock64() - t0 > (4ll << 30)) __trap();
+    }
+}
+
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
     unsigned v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -227,7 +241,7 @@ __global__ void __launch_bounds__(128, 1) cvae_fused_kernel(const __grid_constan
                 // ---- TMA producer
                 for (int kb = 0; kb < kblocks; ++kb) {
                     const uint32_t g = gk + kb, s = g % FZ_STAGES;
-                    if (g >= FZ_STAGES) mbar_wait(empty + s, ((g / FZ_STAGES) + 1) & 1);
+                    if (g >= FZ_STAGES) mbar_wait_fz(empty + s, ((g / FZ_STAGES) + 1) & 1);
                     mbar_expect_tx(full + s, FZ_A_BYTES + FZ_B_BYTES);
                     tma_load_2d_fz(tiles_a + s * FZ_A_BYTES, &maps.a[h], kb * FZ_BK, m * FZ_BM, full + s);
                     tma_load_2d_fz(tiles_b + s * FZ_B_BYTES, &maps.b[h], kb * FZ_BK, n * FZ_BN, full + s);
@@ -236,7 +250,7 @@ __global__ void __launch_bounds__(128, 1) cvae_fused_kernel(const __grid_constan
                 // ---- MMA issuer: 4 x (128 x 64 x 16) per 64-wide K block
                 for (int kb = 0; kb < kblocks; ++kb) {
                     const uint32_t g = gk + kb, s = g % FZ_STAGES;
-                    mbar_wait(full + s, (g / FZ_STAGES) & 1);
+                    mbar_wait_fz(full + s, (g / FZ_STAGES) & 1);
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                     const uint64_t da = umma_desc_sw128(smem_u32(tiles_a + s * FZ_A_BYTES));
                     const uint64_t db = umma_desc_sw128(smem_u32(tiles_b + s * FZ_B_BYTES));
@@ -258,7 +272,7 @@ __global__ void __launch_bounds__(128, 1) cvae_fused_kernel(const __grid_constan
             }
             gk += kblocks;
             __syncwarp();
-            mbar_wait(done, tiles & 1);
+            mbar_wait_fz(done, tiles & 1);
             FZ_STAMP();
             ++tiles;
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
