@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define BD_ABI_VERSION 2
+#define BD_ABI_VERSION 3
 
 #define BD_OK 0
 #define BD_ERR_VALUE (-1)      /* ValueError        pkg/batch_qp.py:99-106,223-227,265-269; pkg/projection.py:225-233 */
@@ -59,6 +59,14 @@ typedef struct bd_cem_config {
     int iter_begin;     /* run CEM iterations [iter_begin, iter_end) of the cycle (0, 0 = all);  */
     int iter_end;       /* a cycle may be split over calls on one context (state stays on the   */
                         /* device; no other solve in between), z then covering only this range */
+    /* numpy stream mode (z == NULL and pcg64_state != NULL): the normals are numpy's
+     * Generator(PCG64).standard_normal stream, drawn on the device from pcg64_state = {state lo,
+     * state hi, increment lo, increment hi} (bit generator state before the first draw of this
+     * call); needs bd_set_normal_tables.  pcg64_positions (host or device, draw-iterations + 1
+     * entries) receives the raw 64-bit outputs consumed after each drawing CEM iteration, so the
+     * caller can advance its Generator exactly (pkg/bilevel.py:51-57 consumption). */
+    const uint64_t* pcg64_state;
+    int64_t* pcg64_positions;
 } bd_cem_config;
 
 /* ------------------------------------------------------------------ lifecycle */
@@ -216,6 +224,18 @@ int bd_cem_cycle(bd_ctx* ctx, int n_scenes, const bd_cem_config* cfg, const doub
                  const double* init_cov, const double* z, const double* warm, int64_t* best_index,
                  double* best_params, double* best_xi, double* best_cost, double* best_residual,
                  double* best_aug, double* stats, double* final_mean, double* final_cov, int* iterations_done);
+
+/* numpy's 256-layer ziggurat tables (ki: uint64, wi / fi: double, 256 each) for the numpy stream
+ * mode of bd_cem_cycle and bd_numpy_normals.  Host pointers. */
+int bd_set_normal_tables(bd_ctx* ctx, const uint64_t* ki, const double* wi, const double* fi);
+
+/* numpy's Generator(PCG64).standard_normal stream on the device: `count` normals from the PCG64
+ * state {state lo, state hi, increment lo, increment hi} into z (host or device), and the raw
+ * outputs consumed after every block of block_len draws into positions (count / block_len + 1
+ * entries, host or device).  Replaces rng.standard_normal in SamplingDistribution.sample
+ * (pkg/bilevel.py:56). */
+int bd_numpy_normals(bd_ctx* ctx, const uint64_t* pcg64_state, long long count, long long block_len, double* z,
+                     int64_t* positions);
 
 /* The last CEM iteration's batch of the preceding bd_cem_cycle on this context (the arguments of the
  * reference's trace_hook, pkg/bilevel.py:269-270): set-points S x B x dim, projected coefficients

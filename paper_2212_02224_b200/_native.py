@@ -54,6 +54,8 @@ SIGNATURES = {
                               _P, _P, _P, _P]),
     "bd_cem_cycle": (c_int, [_P, c_int, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "bd_cem_last_batch": (c_int, [_P, c_int, c_int, _P, _P, _P, _P]),
+    "bd_set_normal_tables": (c_int, [_P, _P, _P, _P]),
+    "bd_numpy_normals": (c_int, [_P, _P, c_longlong, c_longlong, _P, _P]),
     "bd_build_scenes": (c_int, [_P, c_int, c_int, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "bd_set_curvature": (c_int, [_P, c_int, c_int, _P, _P]),
     "bd_set_control_grid": (c_int, [_P, c_int, _P, _P, c_double, c_double, c_double, c_double]),
@@ -76,7 +78,7 @@ class CemConfig(ctypes.Structure):
     _fields_ = [("batch", c_int), ("n_cons", c_int), ("n_elite", c_int), ("iterations", c_int),
                 ("am_iters", c_int), ("eta", c_double), ("gamma", c_double), ("residual_weight", c_double),
                 ("tol", c_double), ("seed", c_uint64), ("scene_offset", c_int), ("iter_begin", c_int),
-                ("iter_end", c_int)]
+                ("iter_end", c_int), ("pcg64_state", c_void_p), ("pcg64_positions", c_void_p)]
 
 
 class Traffic(ctypes.Structure):

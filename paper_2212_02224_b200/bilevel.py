@@ -17,10 +17,12 @@ from __future__ import annotations
 
 import ctypes
 import logging
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
 
+from . import numpy_stream
 from ._native import CemConfig, f64, ptr, upload_scenes
 from .basis import PolynomialBasis, TrajectoryCoeffs, eval_trajectory
 from .batch_qp import NumericalFailure, QPSolutionBatch, TrackingWeights, build_qp_structure
@@ -35,6 +37,9 @@ __all__ = [
 ]
 
 log = logging.getLogger(__name__)
+
+# BD_HOST_DRAWS=1: draw the caller's normals on the host (numpy) instead of the device stream
+_DEVICE_STREAM = os.environ.get("BD_HOST_DRAWS", "0") != "1"
 
 _COV_REG = 1e-6
 
@@ -307,6 +312,30 @@ def solve_bilevel(scene: PlanningScene, solver: LowerLevelSolver, config: BiLeve
         return CemConfig(B, config.constraint_elites, config.elites, N, pcfg.max_iters, config.eta, config.gamma,
                          config.residual_weight, pcfg.tol, 0, 0, a, b)
 
+    # numpy stream mode: the caller's PCG64 normals are generated on the device (identical values,
+    # csrc/numpy_normals.cuh) and the generator is advanced by the raw outputs they consumed; one
+    # call runs the whole cycle.  Other bit generators draw on the host below.
+    st_words = numpy_stream.pcg64_state_words(rng.bit_generator) if _DEVICE_STREAM else None
+    if st_words is not None and numpy_stream.ensure_device_tables(solver.context):
+        pos = np.zeros(n_draw + 1, dtype=np.int64)
+        cfg = cfg_range(0, N)
+        cfg.pcg64_state = st_words.ctypes.data
+        cfg.pcg64_positions = pos.ctypes.data
+        try:
+            solver.context.call("bd_cem_cycle", 1, ctypes.byref(cfg), mean0, cov0, None, ptr(warm), ptr(bi), ptr(bp),
+                                ptr(bx), ptr(bc), ptr(br), ptr(ba), ptr(st), ptr(fm), ptr(fc), ptr(done))
+        except RuntimeError as e:
+            if "numpy normal stream" not in str(e):
+                raise
+            st_words = None          # a draw needed more raw values than evaluated: draw on the host
+        else:
+            k = int(done[0])
+            attempted = N if k >= N else (1 if k <= 0 else k + 1)
+            consumed = attempted - (1 if warm is not None else 0)
+            if consumed > 0:
+                rng.bit_generator.advance(int(pos[consumed]))
+            return _finish(k, N, layout, bi, bp, bx, bc, br, ba, st, fm, fc)
+
     # Iteration 1 is launched as soon as its draws exist; the remaining N-1 batches of the caller's
     # Generator are drawn while the GPU runs it (the stream is the same sequence as one
     # standard_normal((N, B, dim)) call), then iterations 2..N follow in a second call.
@@ -329,6 +358,10 @@ def solve_bilevel(scene: PlanningScene, solver: LowerLevelSolver, config: BiLeve
         rng.bit_generator.state = state0
         if consumed > 0:
             rng.standard_normal((consumed, B, dim))
+    return _finish(k, N, layout, bi, bp, bx, bc, br, ba, st, fm, fc)
+
+
+def _finish(k, N, layout, bi, bp, bx, bc, br, ba, st, fm, fc) -> BiLevelResult:
     if k <= 0:
         raise NumericalFailure("bilevel iteration 1 failed: non-finite projection iterate or KKT residual")
     if k < N:

@@ -26,6 +26,7 @@
 #include "sim_kernels.cuh"
 #include "p2p_kernels.cuh"
 #include "cem_persistent.cuh"
+#include "numpy_normals.cuh"
 
 using namespace bd;
 
@@ -112,6 +113,11 @@ struct bd_ctx {
     bool host_out = false;
     // CEM state
     DevBuf c_bar;               // grid-barrier words of the persistent CEM kernel
+    DevBuf nn_tab, nn_z, nn_pos, nn_err;   // numpy normal stream (tables, draws, block positions, error)
+    DevBuf nn_raw, nn_x, nn_cs, nn_cnt, nn_bar;   // its grid-wide working buffers
+    bool nn_tables = false;
+    bool nn_check = false;      // the call drew numpy normals: check nn_err when it completes
+    int nn_err_host = 0;
     DevBuf c_mean, c_cov, c_L, c_done, c_best_idx, c_best_p, c_best_xi, c_best_s, c_stats, c_cons, c_elite, c_eaug;
     // control grid
     int n_ctrl = 0;
@@ -297,6 +303,7 @@ cudaError_t clear_err(bd_ctx* ctx, size_t bytes) {
 
 void begin_call(bd_ctx* ctx) {
     ctx->n_stage = 0;
+    ctx->nn_check = false;
     ctx->in_pin_off = 0;
     ctx->pending.clear();
     ctx->host_out = false;
@@ -369,6 +376,11 @@ int finish_call(bd_ctx* ctx, bool check_err, int n_err) {
     const bool sync = ctx->host_out || check_err;
     if (!sync) return 0;
     CU(cudaStreamSynchronize(ctx->stream));
+    if (ctx->nn_check) {
+        ctx->nn_check = false;
+        if (ctx->nn_err_host)
+            return fail(ctx, BD_ERR_STATE, "numpy normal stream: a draw needed more raw values than evaluated");
+    }
     if (check_err && n_err > 0) {
         std::vector<int> errs(n_err);
         CU(cudaMemcpy(errs.data(), ctx->w_err.p, n_err * sizeof(int), cudaMemcpyDeviceToHost));
@@ -1422,6 +1434,66 @@ int bd_rank_refit(bd_ctx* ctx, int S, int B, int dim, const double* resid, const
     return finish_call(ctx, false, 0);
 }
 
+// numpy's standard_normal stream (csrc/numpy_normals.cuh) into device z; positions (nblocks + 1
+// raw counts) into a device buffer the caller copies out.  Error bits come back through the
+// context error word (ERR_BAD_RHS-style host check is not possible asynchronously): the caller
+// reads nn_err with the outputs.
+static int launch_numpy_normals(bd_ctx* ctx, const uint64_t* st4, long long count, long long block_len, double* z,
+                                long long* positions) {
+    if (!ctx->nn_tables) return fail(ctx, BD_ERR_STATE, "numpy ziggurat tables not set (bd_set_normal_tables)");
+    if (count < 1 || block_len < 1 || count % block_len) return fail(ctx, BD_ERR_VALUE, "bad normal count / block");
+    CU(ctx->nn_err.ensure(4));
+    CU(cudaMemsetAsync(ctx->nn_err.p, 0, 4, ctx->stream));
+    NumpyNormalArgs a{};
+    a.state = U128{st4[0], st4[1]};
+    a.inc = U128{st4[2], st4[3]};
+    a.count = count;
+    a.block_len = block_len;
+    a.ki = ctx->nn_tab.as<uint64_t>();
+    a.wi = reinterpret_cast<const double*>(a.ki + 256);
+    a.fi = a.wi + 256;
+    a.z = z;
+    a.positions = positions;
+    a.err = ctx->nn_err.as<int>();
+    // grid-wide cooperative form: one position per thread over the whole GPU (5 grid barriers)
+    int sms = 148, coop = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->device);
+    const long long R = count + count / 32 + 4096;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, numpy_normals_grid_kernel, NN_GT, 0);
+    const long long want = (R + NN_GT - 1) / NN_GT;
+    const int grid = (int)std::max(1ll, std::min(want, (long long)sms * std::max(per_sm, 1)));
+    if (coop && per_sm > 0) {
+        CU(ctx->nn_raw.ensure((size_t)(R + NN_CMAX) * 8));
+        CU(ctx->nn_x.ensure((size_t)R * 8));
+        CU(ctx->nn_cs.ensure((size_t)R * 2 + 64));
+        CU(ctx->nn_cnt.ensure((size_t)grid * 8));
+        CU(ctx->nn_bar.ensure(8));
+        CU(cudaMemsetAsync(ctx->nn_bar.p, 0, 8, ctx->stream));
+        NumpyNormalGrid gg{};
+        gg.a = a;
+        gg.R = R;
+        gg.raw = ctx->nn_raw.as<uint64_t>();
+        gg.xv = ctx->nn_x.as<double>();
+        gg.cv = ctx->nn_cs.as<unsigned char>();
+        gg.st = gg.cv + ((R + 63) / 64) * 64;
+        gg.cta_count = ctx->nn_cnt.as<long long>();
+        gg.bar = ctx->nn_bar.as<unsigned>();
+        void* args[] = {&gg};
+        CU(cudaLaunchCooperativeKernel((const void*)numpy_normals_grid_kernel, dim3(grid), dim3(NN_GT), args, 0,
+                                       ctx->stream));
+    } else {
+        raise_smem(numpy_normals_kernel, NN_SMEM);
+        numpy_normals_kernel<<<1, NN_THREADS, NN_SMEM, ctx->stream>>>(a);
+    }
+    ctx->launches++;
+    ctx->pending.push_back({&ctx->nn_err_host, ctx->nn_err.p, 4});
+    ctx->host_out = true;
+    ctx->nn_check = true;
+    return 0;
+}
+
 // Single-scene CEM cycle as one cooperative persistent kernel (csrc/cem_persistent.cuh) when the
 // batch maps to one CTA of 7-8 one-warp samples per SM on the BASELINE latency shape; returns 1
 // when the shape does not apply (the caller runs the per-iteration launch chain instead).
@@ -1498,6 +1570,33 @@ static int try_cem_persistent(bd_ctx* ctx, const bd_cem_config* cfg, const CemSt
     return 0;
 }
 
+int bd_set_normal_tables(bd_ctx* ctx, const uint64_t* ki, const double* wi, const double* fi) {
+    if (!ctx || !ki || !wi || !fi) return BD_ERR_VALUE;
+    begin_call(ctx);
+    CU(ctx->nn_tab.ensure(768 * 8));
+    CU(cudaMemcpy(ctx->nn_tab.p, ki, 256 * 8, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(ctx->nn_tab.as<uint64_t>() + 256, wi, 256 * 8, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(ctx->nn_tab.as<uint64_t>() + 512, fi, 256 * 8, cudaMemcpyHostToDevice));
+    ctx->nn_tables = true;
+    return 0;
+}
+
+int bd_numpy_normals(bd_ctx* ctx, const uint64_t* pcg64_state, long long count, long long block_len, double* z,
+                     int64_t* positions) {
+    NvtxRange nvtx_("bd_numpy_normals");
+    if (!ctx || !pcg64_state || !z || !positions || count < 1 || block_len < 1) return BD_ERR_VALUE;
+    begin_call(ctx);
+    int rc;
+    double* dz;
+    long long* dp;
+    if ((rc = stage_out(ctx, z, (size_t)count, ctx->nn_z, &dz))) return rc;
+    if ((rc = stage_out(ctx, reinterpret_cast<long long*>(positions), (size_t)(count / block_len + 1), ctx->nn_pos,
+                        &dp)))
+        return rc;
+    if ((rc = launch_numpy_normals(ctx, pcg64_state, count, block_len, dz, dp))) return rc;
+    return finish_call(ctx, false, 0);
+}
+
 int bd_cem_cycle(bd_ctx* ctx, int S, const bd_cem_config* cfg, const double* init_mean, const double* init_cov,
                  const double* z, const double* warm, int64_t* best_index, double* best_params, double* best_xi,
                  double* best_cost, double* best_residual, double* best_aug, double* stats, double* final_mean,
@@ -1522,6 +1621,31 @@ int bd_cem_cycle(bd_ctx* ctx, int S, const bd_cem_config* cfg, const double* ini
     if ((rc = stage_in(ctx, init_cov, (size_t)S * dim * dim, &dc0))) return rc;
     if ((rc = stage_in(ctx, z, z ? (size_t)(it1 - it0) * tot * dim : 0, &dz))) return rc;
     if ((rc = stage_in(ctx, warm, warm ? tot * dim : 0, &dwarm))) return rc;
+    if (!z && cfg->pcg64_state) {
+        // numpy stream mode: the caller's Generator(PCG64) normals of every drawing iteration of the
+        // range, generated on the device (the first iteration of a warm-started cycle draws none)
+        const int first = (warm && it0 == 0) ? 1 : 0, nblk = (it1 - it0) - first;
+        CU(ctx->nn_z.ensure((size_t)(it1 - it0) * tot * dim * 8));
+        CU(ctx->nn_pos.ensure((size_t)(nblk + 1) * 8));
+        if (nblk > 0) {
+            if ((rc = launch_numpy_normals(ctx, cfg->pcg64_state, (long long)nblk * tot * dim, (long long)tot * dim,
+                                           ctx->nn_z.as<double>() + (size_t)first * tot * dim,
+                                           ctx->nn_pos.as<long long>())))
+                return rc;
+        } else {
+            CU(cudaMemsetAsync(ctx->nn_pos.p, 0, 8, ctx->stream));
+        }
+        dz = ctx->nn_z.as<double>();
+        if (cfg->pcg64_positions) {
+            if (is_device_ptr(cfg->pcg64_positions)) {
+                CU(cudaMemcpyAsync(cfg->pcg64_positions, ctx->nn_pos.p, (size_t)(nblk + 1) * 8, cudaMemcpyDeviceToDevice,
+                                   ctx->stream));
+            } else {
+                ctx->pending.push_back({cfg->pcg64_positions, ctx->nn_pos.p, (size_t)(nblk + 1) * 8});
+                ctx->host_out = true;
+            }
+        }
+    }
     CU(ctx->c_mean.ensure((size_t)S * dim * 8));
     CU(ctx->c_cov.ensure((size_t)S * dim * dim * 8));
     CU(ctx->c_L.ensure((size_t)S * dim * dim * 8));

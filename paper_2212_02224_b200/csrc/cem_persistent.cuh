@@ -86,9 +86,9 @@ __device__ __forceinline__ void worker_arrive_wait(unsigned* bar, int* err) {
             __nanosleep(BD_POLL_NS);
             if (++spins > (1ll << 28)) { atomicOr(err, ERR_P2P_TIMEOUT); break; }
         }
+        __threadfence();
     }
-    __syncthreads();
-    __threadfence();
+    __syncthreads();       // thread 0's acquire + the CTA barrier publish the other CTAs' writes
 }
 
 // Control CTA: wait until every worker arrived, reset the count (the caller then does the serial
@@ -102,9 +102,9 @@ __device__ __forceinline__ void control_gather(unsigned* bar, int* err, unsigned
             if (++spins > (1ll << 28)) { atomicOr(err, ERR_P2P_TIMEOUT); break; }
         }
         bar[0] = 0u;
+        __threadfence();
     }
     __syncthreads();
-    __threadfence();
 }
 
 __device__ __forceinline__ void control_release(unsigned* bar) {

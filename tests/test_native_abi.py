@@ -36,12 +36,13 @@ def test_library_exports_every_declared_symbol(lib):
 
 
 def test_abi_version(lib):
-    assert lib.bd_abi_version() == 2
+    assert lib.bd_abi_version() == 3
 
 
 def test_struct_layouts():
     assert ctypes.sizeof(_native.Limits) == 9 * 8
-    assert ctypes.sizeof(_native.CemConfig) == 5 * 4 + 4 + 4 * 8 + 8 + 16  # 5 ints, pad, 4 doubles, u64, 3 ints+pad
+    # 5 ints, pad, 4 doubles, u64, 3 ints + pad, 2 pointers (numpy stream state / positions)
+    assert ctypes.sizeof(_native.CemConfig) == 5 * 4 + 4 + 4 * 8 + 8 + 16 + 16
 
 
 def test_no_cpu_fallback_without_gpu(lib):
