@@ -55,7 +55,7 @@ struct CemPersistArgs {
     int scene_offset, it0, it1, am_iters;
     double* params;         // B x dim set-points of the current iteration
     int* order;             // B   stable residual order
-    unsigned* bar;          // 3 words: arrival count, generation, stop flag (zeroed before every launch)
+    unsigned* bar;          // 4 words: arrival count, generation, stop flag, replay flag (zero at launch)
     size_t s1_off, key_off; // dynamic shared-memory offsets of the stage-1 constants / rank keys
 };
 
@@ -69,7 +69,8 @@ __device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
 }
 
 // Barrier words (p.bar): [0] arrivals of the worker CTAs, [1] generation released by the control
-// CTA, [2] the control CTA's stop verdict (scene frozen after a failed iteration).  A worker reads the generation before arriving, so a release is never missed; every wait
+// CTA, [2] the control CTA's stop verdict (scene frozen after a failed iteration), [3] its
+// early-exit verdict (replay, then rank again).  A worker reads the generation before arriving, so a release is never missed; every wait
 // gives up after ~10 s (a CTA that never arrives) and flags ERR_P2P_TIMEOUT instead of hanging.
 #ifndef BD_POLL_NS
 #define BD_POLL_NS 32
@@ -139,17 +140,22 @@ __global__ void __launch_bounds__(TPB, 1) cem_persistent_kernel(const CemPersist
         __shared__ int s_rep, s_stop;
         for (int it = p.it0; it < p.it1; ++it) {
             control_gather(p.bar, cs.err, workers);            // every worker finished its AM pass
+            control_release(p.bar);                            // workers rank while the exit scan runs
             exit_scan_block(p.am.itmax, p.am.max_iters, p.am.tol, 0, p.am.iters_used, p.am.replay_out, nullptr);
             __syncthreads();
             if (threadIdx.x == 0) s_rep = p.am.replay_out[0];
             __syncthreads();
-            const bool rep = s_rep > 0;
-            control_release(p.bar);
-            if (rep) {                                          // workers replay, then arrive again
-                control_gather(p.bar, cs.err, workers);
-                control_release(p.bar);
-            }
             control_gather(p.bar, cs.err, workers);            // every worker ranked its sample
+            if (s_rep > 0) {
+                // early exit: the ranking used the full pass; workers replay for the exit
+                // iteration count and rank again (bar[3] carries the verdict with the release)
+                if (threadIdx.x == 0) p.bar[3] = 1u;
+                control_release(p.bar);
+                control_gather(p.bar, cs.err, workers);        // replayed
+                control_release(p.bar);
+                control_gather(p.bar, cs.err, workers);        // ranked again
+                if (threadIdx.x == 0) p.bar[3] = 0u;
+            }
             rank_refit_block(cs, it, p.order, 0, reinterpret_cast<unsigned char*>(keys));
             __syncthreads();
             if (threadIdx.x == 0) {
@@ -211,32 +217,38 @@ __global__ void __launch_bounds__(TPB, 1) cem_persistent_kernel(const CemPersist
         // ---- A: the AM projection of this CTA's samples
         am_samples<P, false, 100, 5, TPB, true>(p.am, 0, blockIdx.x, p.am_iters, smem);
         BD_STAMP(2);
-        worker_arrive_wait(p.bar, cs.err);               // control: batch-global early exit
+        worker_arrive_wait(p.bar, cs.err);               // every worker's residuals are final
         BD_STAMP(3);
-        const int rep = p.am.replay_out[0];
-        if (rep > 0) {                                   // exact replay for the exit iteration count
+        // ---- R: stable residual rank of this warp's sample, scattered into the order (the control
+        //      CTA scans for a batch-global early exit meanwhile)
+        auto rank_phase = [&]() {
+            for (int j = threadIdx.x; j < B; j += TPB) keys[j] = ordered_bits(cs.resid[j]);
+            __syncthreads();
+            if (active) {
+                const unsigned long long ki = keys[i];
+                int cnt = 0;
+#pragma unroll 4
+                for (int j = lane; j < B; j += 32) {
+                    const unsigned long long kj = keys[j];
+                    cnt += (int)(kj < ki) | ((int)(kj == ki) & (int)(j < i));
+                }
+                for (int o = 16; o >= 1; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+                BD_CHECK(cnt >= 0 && cnt < B);
+                if (lane == 0) p.order[cnt] = i;
+            }
+        };
+        rank_phase();
+        worker_arrive_wait(p.bar, cs.err);               // control: exit verdict (or refit)
+        if (ld_acquire_gpu(p.bar + 3) != 0u) {           // early exit: replay for exactly that many
+            const int rep = p.am.replay_out[0];          // iterations, then rank the final batch
             AmArgs ar = p.am;
             ar.replay = p.am.replay_out;
             am_samples<P, false, 100, 5, TPB, true>(ar, 0, blockIdx.x, rep, smem);
             worker_arrive_wait(p.bar, cs.err);
-        }
-        // ---- R: stable residual rank of this warp's sample, scattered into the order
-        for (int j = threadIdx.x; j < B; j += TPB) keys[j] = ordered_bits(cs.resid[j]);
-        __syncthreads();
-        if (active) {
-            const unsigned long long ki = keys[i];
-            int cnt = 0;
-#pragma unroll 4
-            for (int j = lane; j < B; j += 32) {
-                const unsigned long long kj = keys[j];
-                cnt += (int)(kj < ki) | ((int)(kj == ki) & (int)(j < i));
-            }
-            for (int o = 16; o >= 1; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-            BD_CHECK(cnt >= 0 && cnt < B);
-            if (lane == 0) p.order[cnt] = i;
+            rank_phase();
+            worker_arrive_wait(p.bar, cs.err);
         }
         BD_STAMP(4);
-        worker_arrive_wait(p.bar, cs.err);               // control: elites, refit, Cholesky
         BD_STAMP(7);
         if (ld_acquire_gpu(p.bar + 2) != 0u) break;      // the control CTA froze the scene
 #ifdef BD_PHASE_TIMING
