@@ -333,7 +333,13 @@ def solve_bilevel(scene: PlanningScene, solver: LowerLevelSolver, config: BiLeve
             attempted = N if k >= N else (1 if k <= 0 else k + 1)
             consumed = attempted - (1 if warm is not None else 0)
             if consumed > 0:
+                # PCG64.advance drops a buffered 32-bit half; standard_normal never touches it
+                buf = rng.bit_generator.state
                 rng.bit_generator.advance(int(pos[consumed]))
+                if buf.get("has_uint32"):
+                    st_now = rng.bit_generator.state
+                    st_now["has_uint32"], st_now["uinteger"] = buf["has_uint32"], buf["uinteger"]
+                    rng.bit_generator.state = st_now
             return _finish(k, N, layout, bi, bp, bx, bc, br, ba, st, fm, fc)
 
     # Iteration 1 is launched as soon as its draws exist; the remaining N-1 batches of the caller's

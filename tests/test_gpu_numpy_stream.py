@@ -75,3 +75,40 @@ def test_solve_bilevel_device_stream_equals_host_draws(monkeypatch, warm, N):
     np.testing.assert_allclose(a.distribution.mean, b.distribution.mean, rtol=1e-12)
     np.testing.assert_allclose([d.residual_median for d in a.diagnostics], [d.residual_median for d in b.diagnostics],
                                rtol=1e-9, atol=1e-12)
+
+
+@pytest.mark.parametrize("prep", ["uint32_buffered", "mt19937"])
+def test_solve_bilevel_generator_edge_cases(monkeypatch, prep):
+    """A PCG64 generator holding a buffered 32-bit half (standard_normal never touches it) and a
+    non-PCG64 bit generator (host draws) both end where the host-draw path leaves them."""
+    import paper_2212_02224_b200 as bd
+    from paper_2212_02224_b200 import bilevel as bl
+    from paper_2212_02224_b200.fleet import initial_distribution
+    from paper_2212_02224_b200.scenes import highway_scene
+    basis = bd.build_basis(10, 100, 5.0, "bernstein")
+    solver = bd.LowerLevelSolver(basis, bd.TrackingWeights(), bd.ParamLayout(4), bd.ProjectionConfig(1.0, 100, 1e-3),
+                                 10)
+    scene = highway_scene(4)
+    mean, cov = initial_distribution(scene)
+    cfg = bd.BiLevelConfig(1000, 150, 100, 2, 0.7, 0.9, 1.0, mean, cov)
+
+    def make():
+        if prep == "mt19937":
+            return np.random.Generator(np.random.MT19937(5))
+        g = np.random.default_rng(5)
+        g.integers(0, 1000, size=3, dtype=np.uint32)          # leaves has_uint32 = 1
+        return g
+    out = []
+    for device_stream in (True, False):
+        monkeypatch.setattr(bl, "_DEVICE_STREAM", device_stream)
+        rng = make()
+        r = bd.solve_bilevel(scene, solver, cfg, rng)
+        out.append((r.best.index, rng.bit_generator.state, rng.integers(0, 2**31), rng.standard_normal()))
+    def same(a, b):
+        if isinstance(a, dict):
+            return a.keys() == b.keys() and all(same(a[k], b[k]) for k in a)
+        if isinstance(a, np.ndarray):
+            return np.array_equal(a, b)
+        return a == b
+    assert same(out[0][1], out[1][1])
+    assert out[0][0] == out[1][0] and out[0][2] == out[1][2] and out[0][3] == out[1][3]
