@@ -123,9 +123,11 @@ constexpr int SORT_MIN_PAIRS = BD_SORT_MIN_PAIRS;   // >= 16 obstacles: sorted-w
 
 // Shared-memory carve-up, identical on host and device.
 struct AmSmem {
-    size_t w, obs, k, kb, a, curv, scr, dap, kap, kix, itm, total;
+    size_t w, obs, k, kb, a, curv, scr, dap, kap, kix, itm, hlp, total;
+    // help > 0: the remainder warp's per-(sample, timestep) partial sums (am_helper), HSTR floats each
+    static constexpr int HSTR = 28;
     __host__ __device__ AmSmem(int m, int n_obs, int neq, int n_curv, int s_cta, int threads, int P, bool curv_on,
-                               int max_iters) {
+                               int max_iters, int help = 0) {
         const int J = (m + P - 1) / P;
         size_t o = 0;
         w = o;    o = align_up(o + (size_t)m * WROW * 4, 16);
@@ -141,6 +143,7 @@ struct AmSmem {
         kix = o;  o = align_up(o + (n_obs >= 2 * SORT_MIN_PAIRS ? (size_t)J * threads * 2 : 0), 16);
         // the CTA's per-iteration residual maxima (float bits), flushed to the global table once
         itm = o;  o = align_up(o + (size_t)max_iters * 4, 16);
+        hlp = o;  o = align_up(o + (help > 0 ? (size_t)32 * HSTR * 4 : 0), 16);   // one slot per helper lane
         total = o;
     }
     // per-sample scratch: u (24 doubles) | c32 (24 floats) | lambda-state l (24 doubles) | first-step
@@ -432,14 +435,19 @@ __device__ __forceinline__ void sweep(const float* __restrict__ wsm, const float
 // A slot past m (only the last, on lanes p >= m - (JM-1)P) is evaluated on a clamped timestep and
 // contributes exact zeros.
 #ifndef BD_LAT_CH
-#define BD_LAT_CH 2      // A/B on B200 (B = 1000, P = 32): 2 slots 0.229 ms, 3: 0.246, 4: 0.251
+#define BD_LAT_CH 1      // A/B on B200 (B = 1000, P = 32, round 2): 1 slot 0.213 ms, 2: 0.221 (round 1: 2 0.229, 3 0.246, 4 0.251)
 #endif
-template <int P, bool INIT, int NV, int MT, int NPT, int TPB>
+#ifndef BD_LAT_CH_H
+#define BD_LAT_CH_H 1    // with the remainder warp (3 full slots): 1 slot 0.201 ms, 2: 0.220, 3: 0.226
+#endif
+template <int P, bool INIT, int NV, int MT, int NPT, int TPB, bool HELPED = false>
 __device__ __forceinline__ void sweep_lat(const float* __restrict__ wsm, const float4* __restrict__ osm,
                                           const float2 (&cxy)[NC], float (&v)[NV], float* dap, int p,
                                           const SceneLim& L, int& conf, bool want_cost) {
-    constexpr int JM = (MT + P - 1) / P;
-    constexpr int CH = JM > BD_LAT_CH ? BD_LAT_CH : JM;   // slots per phase group (register budget)
+    // HELPED: only the full slots; the remainder warp (am_helper) evaluates the last MT mod P timesteps
+    constexpr int JM = HELPED ? MT / P : (MT + P - 1) / P;
+    constexpr int CHM = HELPED ? BD_LAT_CH_H : BD_LAT_CH;
+    constexpr int CH = JM > CHM ? CHM : JM;                 // slots per phase group (register budget)
 #pragma unroll
     for (int k = 0; k < NV; ++k) v[k] = 0.f;
 #pragma unroll
@@ -450,7 +458,7 @@ __device__ __forceinline__ void sweep_lat(const float* __restrict__ wsm, const f
 #pragma unroll
     for (int jj = 0; jj < CH; ++jj) {
         const int j = j0 + jj;
-        const bool valid = j < JM && ((MT % P == 0) || j + 1 < JM || p + j * P < MT);
+        const bool valid = j < JM && (HELPED || (MT % P == 0) || j + 1 < JM || p + j * P < MT);
         const int t = valid ? p + j * P : MT - 1;
         float w[WROW];
         const float4* wr = reinterpret_cast<const float4*>(wsm + t * WROW);
@@ -545,7 +553,7 @@ __device__ __forceinline__ void sweep_lat(const float* __restrict__ wsm, const f
 #pragma unroll
     for (int jj = 0; jj < CH; ++jj) {
         const int j = j0 + jj;
-        const bool valid = j < JM && ((MT % P == 0) || j + 1 < JM || p + j * P < MT);
+        const bool valid = j < JM && (HELPED || (MT % P == 0) || j + 1 < JM || p + j * P < MT);
         const int t = valid ? p + j * P : MT - 1;
         const float up = fmaxf(Y[jj] - L.y_ub, 0.f), lo = fmaxf(L.y_lb - Y[jj], 0.f);
         const float2 roj = make_float2(L.a * rox[jj], fmaf(L.b, roy[jj], up - lo));
@@ -583,6 +591,172 @@ __device__ __forceinline__ void sweep_lat(const float* __restrict__ wsm, const f
     }
 }
 
+#ifndef BD_NO_ITMAX
+#define BD_NO_ITMAX 0      // diagnostic builds only: drop the per-iteration batch-max atomics
+#endif
+
+// One timestep t of one sample for the remainder warp: the arithmetic of one sweep_lat slot
+// (phases A, B, C), its 22 back-projection partials, direct residual and cost written to out[0..23].
+// dap_h carries the timestep's clipped acceleration between iterations, as dap does for a slot.
+template <int NPT, bool INIT>
+__device__ __forceinline__ void rem_eval(const float* __restrict__ wsm, const float4* __restrict__ osm,
+                                         const float* __restrict__ c32, int t, const SceneLim& L, float& dap_h,
+                                         int& conf, bool count, bool want_cost, float* out) {
+    float2 cxy[NC];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) cxy[q] = reinterpret_cast<const float2*>(c32)[q];
+    float w[WROW];
+    const float4* wr = reinterpret_cast<const float4*>(wsm + t * WROW);
+#pragma unroll
+    for (int q = 0; q < WROW / 4; ++q) {
+        const float4 f = wr[q];
+        w[4 * q] = f.x; w[4 * q + 1] = f.y; w[4 * q + 2] = f.z; w[4 * q + 3] = f.w;
+    }
+    float2 P0 = make_float2(0.f, 0.f), P1 = P0, P2 = P0;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) P0 = ffma2(w[k], cxy[k], P0);
+    const float4* op = osm + t * NPT;
+    float4 ob[NPT];
+#pragma unroll
+    for (int o = 0; o < NPT; ++o) ob[o] = op[o];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+        P1 = ffma2(w[NC + k], cxy[k], P1);
+        P2 = ffma2(w[2 * NC + k], cxy[k], P2);
+    }
+    const float xs0 = P0.x * L.inv_a, ys0 = P0.y * L.inv_b;
+    float qmin = 3.0e38f;
+#pragma unroll
+    for (int o = 0; o < NPT; ++o) {
+        const float2 wc = fadd2(make_float2(xs0, xs0), make_float2(ob[o].x, ob[o].y));
+        const float2 ws = fadd2(make_float2(ys0, ys0), make_float2(ob[o].z, ob[o].w));
+        const float2 q = ffma2(wc, wc, fmul2(ws, ws));
+        qmin = fminf(qmin, fminf(q.x, q.y));
+    }
+    const float XD = P1.x, YD = P1.y, XDD = P2.x, YDD = P2.y;
+    const float dv2 = fmaf(XD, XD, YD * YD);
+    const float da2 = fmaf(XDD, XDD, YDD * YDD);
+    const float iv = dv2 > 0.f ? rsqrtf(dv2) : 0.f;
+    const float ia = da2 > 0.f ? rsqrtf(da2) : 0.f;
+    const float dv = dv2 * iv, da = da2 * ia;
+    const float cross = fabsf(fmaf(YDD, XD, -XDD * YD));
+    const float gv = (da2 > 0.f ? cross : fabsf(YD)) * iv;
+    const float gva = gv * ia;
+    const float gap = dv2 > 0.f ? (da2 > 0.f ? gva : gv) : fabsf(YDD) * ia;
+    const float da_prev = INIT ? fminf(fmaxf(da, 0.f), L.a_max) : dap_h;
+    const float vhi = L.v_max;
+    const float vlo = fmaxf(L.v_min, sqrtf(da_prev * gap * L.inv_k_max));
+    conf += (count && vlo > vhi) ? 1 : 0;
+    const float dvc = fminf(fmaxf(dv, fminf(vlo, vhi)), vhi);
+    const float ahi = fminf(L.a_max, __fdividef(dvc * dvc * L.k_max, fmaxf(gap, 1e-8f)));
+    const float dac = fminf(fmaxf(da, 0.f), ahi);
+    dap_h = dac;
+    float2 rv, ra;
+    if (dv2 > 0.f) rv = fmul2(make_float2((dv - dvc) * iv, (dv - dvc) * iv), P1);
+    else rv = make_float2(-dvc, 0.f);
+    if (da2 > 0.f) ra = fmul2(make_float2((da - dac) * ia, (da - dac) * ia), P2);
+    else ra = make_float2(-dac, 0.f);
+    float rox = 0.f, roy = 0.f, coll = 0.f;
+    if (qmin < 1.f) {
+        const float xs = P0.x * L.inv_a, ys = P0.y * L.inv_b;
+        for (int o = 0; o < NPT; ++o) {
+            const float4 obo = op[o];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const float wc = xs + (h ? obo.y : obo.x), ws = ys + (h ? obo.w : obo.z);
+                const float q = fmaf(wc, wc, ws * ws);
+                if (q < 1.f) {
+                    coll += 1.f - q;
+                    if (q > 0.f) {
+                        const float f = 1.f - rsqrtf(q);
+                        rox = fmaf(wc, f, rox);
+                        roy = fmaf(ws, f, roy);
+                    } else {
+                        rox -= 1.f;
+                    }
+                }
+            }
+        }
+    }
+    const float up = fmaxf(P0.y - L.y_ub, 0.f), lo = fmaxf(L.y_lb - P0.y, 0.f);
+    const float2 ro = make_float2(L.a * rox, fmaf(L.b, roy, up - lo));
+    float4* o4 = reinterpret_cast<float4*>(out);
+    float g[NX + 2];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+        float2 gk = fmul2(make_float2(w[NC + k], w[NC + k]), rv);
+        gk = ffma2(w[2 * NC + k], ra, gk);
+        gk = ffma2(w[k], ro, gk);
+        g[2 * k] = gk.x;
+        g[2 * k + 1] = gk.y;
+    }
+    g[NX] = 0.f;
+    g[NX + 1] = 0.f;
+    if (!INIT) {
+        float r = coll + up + lo;
+        r += fmaxf(dv - L.v_max, 0.f) + fmaxf(L.v_min - dv, 0.f);
+        r += fmaxf(da - L.a_max, 0.f);
+        const float sp = fmaxf(dv, 1e-6f);
+        r += fmaxf(__fdividef(cross, sp * sp * sp) - L.k_max, 0.f);
+        g[NX] = r;
+        if (want_cost) {
+            const float e = dv - L.v_max;
+            g[NX + 1] = e * e;
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < (NX + 2) / 4; ++q) o4[q] = make_float4(g[4 * q], g[4 * q + 1], g[4 * q + 2], g[4 * q + 3]);
+}
+
+// The remainder warp of a helped latency CTA (TPB = 32 (SPC + 1)): lane s * HELP + r evaluates
+// timestep (MT / 32) * 32 + r of sample slot s every iteration, between the two CTA barriers the
+// sample warps pass around their sweep (coefficients in shared memory -> barrier -> remainder
+// timesteps -> barrier -> the sample warp adds the HELP partials after its reduce-scatter).  The
+// sample warps then sweep 3 full slots instead of 3 + a 4-of-32-lane one (m = 100).  Mirrors
+// am_samples' CTA barriers one for one, including the per-iteration-maxima table's.
+template <int NPT, int MT, int TPB, int HELP>
+__device__ __noinline__ void am_helper(const AmArgs& a, int scene, int cta, int iters, unsigned char* smem) {
+    constexpr int SPC = TPB / 32 - 1;
+    static_assert(SPC * HELP <= 32, "remainder warp: one lane per (sample, remainder timestep)");
+    const AmSmem lay(a.m, a.n_obs, a.neq, a.n_curv, a.s_cta, blockDim.x, 32, false, a.max_iters, HELP);
+    const float* wsm = reinterpret_cast<const float*>(smem + lay.w);
+    const float4* osm = reinterpret_cast<const float4*>(smem + lay.obs);
+    const int lane = threadIdx.x & 31;
+    const bool live = lane < SPC * HELP;
+    const int s = live ? lane / HELP : SPC - 1;
+    const int t = (MT / 32) * 32 + lane % HELP;
+    const bool count = live && cta * a.s_cta + s < a.B;
+    const float* c32 = reinterpret_cast<const float*>(smem + lay.scr + (size_t)s * AmSmem::SCR_BYTES + 192);
+    float* out = reinterpret_cast<float*>(smem + lay.hlp) + lane * AmSmem::HSTR;
+    const SceneLim L = a.lim[scene];
+    float dap_h = 0.f;
+    int conf = 0;
+    float* dst = out;                                       // idle lanes write their own (unread) slot
+    __syncthreads();                                        // coefficients of every sample staged
+    rem_eval<NPT, true>(wsm, osm, c32, t, L, dap_h, conf, count, true, dst);
+    __syncthreads();                                        // partials published
+    const bool record = a.replay == nullptr && !BD_NO_ITMAX;
+    unsigned* itm_s = reinterpret_cast<unsigned*>(smem + lay.itm);
+    if (record) {
+        for (int k = threadIdx.x; k < iters; k += blockDim.x) itm_s[k] = 0u;
+        __syncthreads();
+    }
+    for (int it = 0; it < iters; ++it) {
+        __syncthreads();
+        rem_eval<NPT, false>(wsm, osm, c32, t, L, dap_h, conf, count, it == iters - 1, dst);
+        __syncthreads();
+    }
+    if (record) {
+        __syncthreads();
+        unsigned* itm = a.itmax + (size_t)scene * a.max_iters * ITMAX_SLOTS + (cta % ITMAX_SLOTS);
+        for (int k = threadIdx.x; k < iters; k += blockDim.x)
+            if (const unsigned v = itm_s[k]) atomicMax(itm + (size_t)k * ITMAX_SLOTS, v);
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) conf += __shfl_xor_sync(0xffffffffu, conf, o);
+    if (lane == 0 && conf) atomicAdd(a.conflicts + scene, (unsigned long long)conf);
+}
+
 // The all-gather fused into the epilogue: one value into every rank's symmetric buffer
 // (kept out of line so the main loop's register allocation does not see it).
 __device__ __noinline__ void p2p_store_all(void* const* bufs, int world, size_t off, long long row, double val) {
@@ -594,9 +768,6 @@ __device__ __forceinline__ void pair_sync() {
     asm volatile("bar.sync %0, 64;" ::"r"(1 + (int)(threadIdx.x >> 6)) : "memory");
 }
 
-#ifndef BD_NO_ITMAX
-#define BD_NO_ITMAX 0      // diagnostic builds only: drop the per-iteration batch-max atomics
-#endif
 #ifndef BD_AM_MINB
 #define BD_AM_MINB 2       // x 256 threads: 128 registers per thread
 #endif
@@ -637,15 +808,25 @@ __device__ __forceinline__ void am_stage(const AmArgs& a, int scene, unsigned ch
 
 // AM iterations for the samples of CTA `blk` of `scene` (constants already staged): prologue,
 // `iters` iterations, outputs, conflict / error atomics.
-template <int P, bool CURV, int MT, int NPT, int TPB, bool LAT>
+template <int P, bool CURV, int MT, int NPT, int TPB, bool LAT, int HELP = 0>
 __device__ __forceinline__ void am_samples(const AmArgs& a, int scene, int blk, int iters, unsigned char* smem) {
+    constexpr bool LAT32 = LAT && P <= 32 && MT > 0 && NPT > 0 && NPT < SORT_MIN_PAIRS && !CURV;
+    // HELP > 0: the last warp of the CTA is the remainder warp (am_helper); the others sweep full slots
+    constexpr bool HELPED = LAT32 && P == 32 && HELP > 0;
+    static_assert(HELP == 0 || (HELPED && HELP == MT % 32), "remainder warp: latency instance, MT mod 32 timesteps");
+    if constexpr (HELPED) {
+        if ((int)(threadIdx.x >> 5) == TPB / 32 - 1) {
+            am_helper<NPT, MT, TPB, HELP>(a, scene, blk < 0 ? (int)blockIdx.x : blk, iters, smem);
+            return;
+        }
+    }
     constexpr bool PAIR = (P == 64);
     constexpr int RP = PAIR ? 32 : P;                // reduction width / ownership stride
     constexpr int NV = ((NX + 2 + RP - 1) / RP) * RP;   // 22 back-projections + residual + cost, padded
     constexpr int ROWS = (NX + RP - 1) / RP;         // coefficient rows owned per lane
     const int m = a.m, neq = a.neq, n_obs = a.n_obs;
     const int threads = blockDim.x;
-    const AmSmem lay(m, n_obs, neq, a.n_curv, a.s_cta, threads, P, CURV, a.max_iters);
+    const AmSmem lay(m, n_obs, neq, a.n_curv, a.s_cta, threads, P, CURV, a.max_iters, HELPED ? HELP : 0);
     float* wsm = reinterpret_cast<float*>(smem + lay.w);
     float4* osm = reinterpret_cast<float4*>(smem + lay.obs);
     double* ksm = reinterpret_cast<double*>(smem + lay.k);
@@ -714,6 +895,7 @@ __device__ __forceinline__ void am_samples(const AmArgs& a, int scene, int blk, 
     bool bad = false;
     float v[NV];
     float* xbuf = reinterpret_cast<float*>(smem + lay.scr + (size_t)slot * AmSmem::SCR_BYTES + 672);
+    const float* hsm = reinterpret_cast<const float*>(smem + lay.hlp) + slot * HELP * AmSmem::HSTR + lane;
     auto reduce = [&]() {
         group_reduce_scatter<RP>(v, lane);
         if (PAIR) {                                   // second warp -> first warp partial sums
@@ -721,10 +903,19 @@ __device__ __forceinline__ void am_samples(const AmArgs& a, int scene, int blk, 
             pair_sync();
             if (!(threadIdx.x & 32) && lane < NX + 2) v[0] += xbuf[lane];
         }
+        if constexpr (HELPED) {                       // the remainder warp's timesteps of this sample
+            __syncthreads();
+            if (lane < NX + 2) {
+                float h = hsm[0];
+#pragma unroll
+                for (int r = 1; r < HELP; ++r) h += hsm[r * AmSmem::HSTR];
+                v[0] += h;
+            }
+        }
     };
-    constexpr bool LAT32 = LAT && P <= 32 && MT > 0 && NPT > 0 && NPT < SORT_MIN_PAIRS && !CURV;
+    if constexpr (HELPED) __syncthreads();           // every sample's coefficients staged (am_helper)
     if constexpr (LAT32)
-        sweep_lat<P, true, NV, MT, NPT, TPB>(wsm, osm, cxy, v, dap, p, L, conf, true);
+        sweep_lat<P, true, NV, MT, NPT, TPB, HELPED>(wsm, osm, cxy, v, dap, p, L, conf, true);
     else
         sweep<P, CURV, true, NV, MT, NPT, TPB>(wsm, osm, csm, cxy, v, dap, kap, kix, threads, p, m, n_obs / 2,
                                                a.n_curv, L, conf, a.sorted != 0);
@@ -788,8 +979,9 @@ __device__ __forceinline__ void am_samples(const AmArgs& a, int scene, int blk, 
 #pragma unroll
         for (int q = 0; q < NC; ++q) cxy[q] = reinterpret_cast<const float2*>(sc)[q];
         // ---- projections, back-projection, residual at the new iterate
+        if constexpr (HELPED) __syncthreads();
         if constexpr (LAT32)
-            sweep_lat<P, false, NV, MT, NPT, TPB>(wsm, osm, cxy, v, dap, p, L, conf, it == iters - 1);
+            sweep_lat<P, false, NV, MT, NPT, TPB, HELPED>(wsm, osm, cxy, v, dap, p, L, conf, it == iters - 1);
         else
             sweep<P, CURV, false, NV, MT, NPT, TPB>(wsm, osm, csm, cxy, v, dap, kap, kix, threads, p, m, n_obs / 2,
                                                     a.n_curv, L, conf, a.sorted != 0, it == iters - 1);   // cost: last sweep only
@@ -861,7 +1053,7 @@ __device__ __forceinline__ void am_samples(const AmArgs& a, int scene, int blk, 
 // LAT: latency instances, one CTA of 5-8 samples per SM (P = 64: two-warp samples, <= 128 registers;
 // P = 32 / 16: one-warp / half-warp samples, whose <= 2 warps per SM sub-partition may use up to
 // 255 registers and run the phase-split sweep_lat)
-template <int P, bool CURV, int MT = 0, int NPT = 0, int TPB = 0, bool LAT = false>
+template <int P, bool CURV, int MT = 0, int NPT = 0, int TPB = 0, bool LAT = false, int HELP = 0>
 __global__ void __launch_bounds__(LAT ? TPB : 256, LAT ? 1 : BD_AM_MINB) am_kernel(const AmArgs a) {
     // P <= 32: a sample is a group of P lanes of one warp.  P == 64: a sample spans two warps
     // (latency mapping for small batches); each warp reduce-scatters its partial sums, the second
@@ -876,7 +1068,7 @@ __global__ void __launch_bounds__(LAT ? TPB : 256, LAT ? 1 : BD_AM_MINB) am_kern
     }
     __shared__ __align__(8) uint64_t stage_bar;
     am_stage<P, CURV>(a, scene, smem, &stage_bar);
-    am_samples<P, CURV, MT, NPT, TPB, LAT>(a, scene, -1, iters, smem);
+    am_samples<P, CURV, MT, NPT, TPB, LAT, HELP>(a, scene, -1, iters, smem);
     // ---- batch-global early exit folded into the last CTA of the scene (no extra launch)
     if (a.replay == nullptr && a.done_ctr != nullptr) {
         __shared__ bool last;

@@ -68,7 +68,7 @@ struct bd_ctx {
     std::string err;
     int64_t launches = 0;
     int64_t persistent_cycles = 0;   // bd_cem_cycle calls run as the persistent kernel
-    int opt_lanes = 0, opt_spc = 0, opt_lat_off = 0, opt_persist_off = 0;
+    int opt_lanes = 0, opt_spc = 0, opt_lat_off = 0, opt_persist_off = 0, opt_help_off = 0;
     // instrumentation
     bool timing = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_used, ev_free;
@@ -414,13 +414,15 @@ void raise_smem(K kernel, size_t bytes) {
         e.raised = bytes;
 }
 
-template <int P, bool CURV, int MT = 0, int NPT = 0, int TPB = 0, bool LAT = false>
+template <int P, bool CURV, int MT = 0, int NPT = 0, int TPB = 0, bool LAT = false, int HELP = 0>
 int launch_am_t(bd_ctx* ctx, AmArgs a, int threads, bool replay_pass, int* occ = nullptr) {
-    const AmSmem lay(a.m, a.n_obs, a.neq, a.n_curv, a.s_cta, threads, P, CURV, a.max_iters);
+    if (HELP) a.s_cta = threads / 32 - 1;             // the last warp is the remainder warp
+    const AmSmem lay(a.m, a.n_obs, a.neq, a.n_curv, a.s_cta, threads, P, CURV, a.max_iters, HELP);
     if (lay.total > 227 * 1024) return fail(ctx, BD_ERR_VALUE, "AM kernel needs %zu B of shared memory", lay.total);
-    raise_smem(am_kernel<P, CURV, MT, NPT, TPB, LAT>, lay.total);
+    raise_smem(am_kernel<P, CURV, MT, NPT, TPB, LAT, HELP>, lay.total);
     if (occ) {   // occupancy query only (lane-mapping choice)
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, am_kernel<P, CURV, MT, NPT, TPB, LAT>, threads, lay.total) !=
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, am_kernel<P, CURV, MT, NPT, TPB, LAT, HELP>, threads,
+                                                          lay.total) !=
             cudaSuccess) {
             cudaGetLastError();
             *occ = 0;
@@ -441,7 +443,7 @@ int launch_am_t(bd_ctx* ctx, AmArgs a, int threads, bool replay_pass, int* occ =
         }
         cudaEventRecord(ev.first, ctx->stream);
     }
-    am_kernel<P, CURV, MT, NPT, TPB, LAT><<<grid, threads, lay.total, ctx->stream>>>(a);
+    am_kernel<P, CURV, MT, NPT, TPB, LAT, HELP><<<grid, threads, lay.total, ctx->stream>>>(a);
     ctx->launches++;
     if (timed) {
         cudaEventRecord(ev.second, ctx->stream);
@@ -450,6 +452,18 @@ int launch_am_t(bd_ctx* ctx, AmArgs a, int threads, bool replay_pass, int* occ =
         ctx->am_sample_iters += (double)a.B * ctx->S * a.max_iters;
     }
     return 0;
+}
+
+// The one-warp latency instance runs with a remainder warp at 7 samples per SM unless the option
+// turns it off (8 samples + the remainder warp = 3 warps on one SM sub-partition: <= 168 registers,
+// which spills).
+static int samples_per_sm(const bd_ctx* ctx, long long samples) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+    return (int)((samples + sms - 1) / sms);
+}
+static bool lat_helped(const bd_ctx* ctx, long long samples) {
+    return !ctx->opt_help_off && !ctx->opt_spc && samples_per_sm(ctx, samples) == 7;
 }
 
 int dispatch_am(bd_ctx* ctx, AmArgs a, int P, int threads, bool replay_pass, int* occ) {
@@ -480,7 +494,11 @@ int dispatch_am(bd_ctx* ctx, AmArgs a, int P, int threads, bool replay_pass, int
             default: return fail(ctx, BD_ERR_VALUE, "unsupported CTA size %d", threads);
         }
     }
-    // single-scene latency shape, one-warp samples: one CTA of 5-8 samples per SM, 255 registers
+    // single-scene latency shape, one-warp samples: one CTA of 7-8 samples + the remainder warp per
+    // SM (timesteps 96-99 of every sample, am_helper), <= 255 registers
+    if (P == 32 && !curv && a.m == 100 && a.n_obs == 10 && threads == 256 && lat_helped(ctx, (long long)a.B * ctx->S))
+        return launch_am_t<32, false, 100, 5, 256, true, 4>(ctx, a, threads, replay_pass, occ);
+    // the same without the remainder warp: one CTA of 5-8 samples per SM
     if (P == 32 && !curv && a.m == 100 && a.n_obs == 10 && threads > 128) {
         switch (threads) {
             case 160: return launch_am_t<32, false, 100, 5, 160, true>(ctx, a, threads, replay_pass, occ);
@@ -512,6 +530,7 @@ int default_threads(bd_ctx* ctx, int P, const AmArgs& a) {
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
         const long long per_sm = ((long long)a.B * ctx->S + sms - 1) / sms;
         if (per_sm >= 5 && per_sm <= 8) threads = P * (int)per_sm;
+        if (P == 32 && lat_helped(ctx, (long long)a.B * ctx->S)) threads += 32;   // + the remainder warp
     }
     return threads;
 }
@@ -746,6 +765,10 @@ int bd_set_option(bd_ctx* ctx, const char* key, int value) {
     }
     if (!strcmp(key, "latency_instance")) {   // 0: never pick the one-warp latency instance automatically
         ctx->opt_lat_off = value == 0;
+        return 0;
+    }
+    if (!strcmp(key, "remainder_warp")) {     // 0: one-warp latency CTAs without the remainder warp
+        ctx->opt_help_off = value == 0;
         return 0;
     }
     if (!strcmp(key, "samples_per_cta")) {
@@ -1509,7 +1532,8 @@ static int try_cem_persistent(bd_ctx* ctx, const bd_cem_config* cfg, const CemSt
     const int B = cfg->batch;
     const int spc = (B + sms - 1) / sms;
     if (!coop || spc < 7 || spc > 8) return 1;
-    const int grid = (B + spc - 1) / spc + 1, threads = 32 * spc;   // workers + the control CTA
+    const bool help = lat_helped(ctx, B);                           // + the remainder warp per worker
+    const int grid = (B + spc - 1) / spc + 1, threads = 32 * (spc + (help ? 1 : 0));   // workers + control
     if (grid > sms) return 1;
     const int iters = cfg->am_iters;
     const size_t itmax_bytes = (size_t)iters * ITMAX_SLOTS * 4;
@@ -1543,7 +1567,7 @@ static int try_cem_persistent(bd_ctx* ctx, const bd_cem_config* cfg, const CemSt
     pa.params = ctx->w_params.as<double>();
     pa.order = ctx->w_order.as<int>();
     pa.bar = ctx->c_bar.as<unsigned>();
-    const AmSmem lay(ctx->m, ctx->obs_pad, ctx->neq, 0, spc, threads, 32, false, iters);
+    const AmSmem lay(ctx->m, ctx->obs_pad, ctx->neq, 0, spc, threads, 32, false, iters, help ? 4 : 0);
     pa.s1_off = align_up(lay.total, 16);
     const size_t s1_bytes = (size_t)(2 * s1.nr * s1_ld(s1.nr) + 2 * NC * s1.m_seg + spc * MAX_DIM + spc * S1_VEC) * 8;
     pa.key_off = align_up(pa.s1_off + s1_bytes, 16);
@@ -1551,15 +1575,14 @@ static int try_cem_persistent(bd_ctx* ctx, const bd_cem_config* cfg, const CemSt
     if (smem > 200 * 1024) return 1;
     void* args[] = {&pa};
     cudaError_t e;
-    if (spc == 7) {
-        raise_smem(cem_persistent_kernel<224>, smem);
-        e = cudaLaunchCooperativeKernel((const void*)cem_persistent_kernel<224>, dim3(grid), dim3(threads), args, smem,
-                                        ctx->stream);
-    } else {
-        raise_smem(cem_persistent_kernel<256>, smem);
-        e = cudaLaunchCooperativeKernel((const void*)cem_persistent_kernel<256>, dim3(grid), dim3(threads), args, smem,
-                                        ctx->stream);
-    }
+    auto launch = [&](auto kernel) {
+        raise_smem(kernel, smem);
+        return cudaLaunchCooperativeKernel((const void*)kernel, dim3(grid), dim3(threads), args, smem, ctx->stream);
+    };
+    if (help)
+        e = launch(cem_persistent_kernel<256, 4>);
+    else
+        e = spc == 7 ? launch(cem_persistent_kernel<224, 0>) : launch(cem_persistent_kernel<256, 0>);
     if (e == cudaErrorCooperativeLaunchTooLarge) {   // not co-resident on this device: launch chain instead
         cudaGetLastError();
         return 1;

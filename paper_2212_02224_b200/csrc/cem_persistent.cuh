@@ -120,9 +120,10 @@ __device__ __forceinline__ void control_release(unsigned* bar) {
 // CTA is the control CTA: it never runs the AM loop, so the code of the serial steps (exit scan,
 // elite ranking, refit, Cholesky) stays warm in its SM's instruction cache -- run by whichever
 // worker arrived last, the refit took ~20 us, mostly instruction-fetch misses after the AM loop.
-template <int TPB>
+template <int TPB, int HELP>
 __global__ void __launch_bounds__(TPB, 1) cem_persistent_kernel(const CemPersistArgs p) {
-    constexpr int P = 32, SPC = TPB / 32;
+    // HELP > 0: the last warp of a worker CTA is the AM remainder warp (am_helper), no sample
+    constexpr int P = 32, SPC = TPB / 32 - (HELP > 0 ? 1 : 0);
     extern __shared__ __align__(16) unsigned char smem[];
     const CemState& cs = p.cs;
     const S1Args& a1 = p.s1;
@@ -171,7 +172,7 @@ __global__ void __launch_bounds__(TPB, 1) cem_persistent_kernel(const CemPersist
 
     // ---------------- worker CTAs
     const int i = blockIdx.x * SPC + wid;                // this warp's sample
-    const bool active = i < B;
+    const bool active = wid < SPC && i < B;
     // constants staged once per launch: AM (basis rows, obstacle tile, K blocks), stage 1
     __shared__ __align__(8) uint64_t stage_bar;
     am_stage<P, false>(p.am, 0, smem, &stage_bar);
@@ -215,7 +216,7 @@ __global__ void __launch_bounds__(TPB, 1) cem_persistent_kernel(const CemPersist
         __syncwarp();
         BD_STAMP(1);
         // ---- A: the AM projection of this CTA's samples
-        am_samples<P, false, 100, 5, TPB, true>(p.am, 0, blockIdx.x, p.am_iters, smem);
+        am_samples<P, false, 100, 5, TPB, true, HELP>(p.am, 0, blockIdx.x, p.am_iters, smem);
         BD_STAMP(2);
         worker_arrive_wait(p.bar, cs.err);               // every worker's residuals are final
         BD_STAMP(3);
@@ -243,7 +244,7 @@ __global__ void __launch_bounds__(TPB, 1) cem_persistent_kernel(const CemPersist
             const int rep = p.am.replay_out[0];          // iterations, then rank the final batch
             AmArgs ar = p.am;
             ar.replay = p.am.replay_out;
-            am_samples<P, false, 100, 5, TPB, true>(ar, 0, blockIdx.x, rep, smem);
+            am_samples<P, false, 100, 5, TPB, true, HELP>(ar, 0, blockIdx.x, rep, smem);
             worker_arrive_wait(p.bar, cs.err);
             rank_phase();
             worker_arrive_wait(p.bar, cs.err);

@@ -14,6 +14,9 @@ sc = [highway_scene(0)]
 solver = bd.LowerLevelSolver(basis, bd.TrackingWeights(), bd.ParamLayout(4), bd.ProjectionConfig(1.0, 100, 1e-3), 10)
 mean, cov = initial_distribution(sc[0])
 cfg2 = bd.BiLevelConfig(1000, 150, 100, 4, 0.7, 0.9, 1.0, mean, cov)
+rem = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+fp.context.set_option("remainder_warp", rem)
+solver.context.set_option("remainder_warp", rem)
 for opt in (1, 0, 1, 0):
     fp.context.set_option("persistent_cycle", opt)
     solver.context.set_option("persistent_cycle", opt)
@@ -27,4 +30,4 @@ for opt in (1, 0, 1, 0):
     for k in range(reps):
         rng = np.random.default_rng(k)
         t0 = time.perf_counter(); bd.solve_bilevel(sc[0], solver, cfg2, rng); u.append(time.perf_counter() - t0)
-    print(f"persistent={opt}: plan p50 {np.median(t) * 1e3:.3f} ms, solve_bilevel p50 {np.median(u) * 1e3:.3f} ms")
+    print(f"remainder_warp={rem} persistent={opt}: plan p50 {np.median(t) * 1e3:.3f} ms, solve_bilevel p50 {np.median(u) * 1e3:.3f} ms")

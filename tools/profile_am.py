@@ -22,6 +22,7 @@ ap.add_argument("--batch", type=int, default=1000)
 ap.add_argument("--cycles", type=int, default=2)
 ap.add_argument("--spc", type=int, default=0)
 ap.add_argument("--lat", type=int, default=None)
+ap.add_argument("--rem", type=int, default=None)
 a = ap.parse_args()
 basis = bd.build_basis(10, 100, 5.0, "bernstein")
 cfg = bd.BiLevelConfig(a.batch, min(150, a.batch), min(100, a.batch), 4, 0.7, 0.9, 1.0)
@@ -32,6 +33,8 @@ if a.lat is not None:
     fp.context.set_option("latency_instance", a.lat)
 if a.spc:
     fp.context.set_option("samples_per_cta", a.spc)
+if a.rem is not None:
+    fp.context.set_option("remainder_warp", a.rem)
 rec = HighwayRecipe(n_obs=a.obs, density=3.0 if a.obs > 10 else 2.0, vehicle_count=80 if a.obs > 10 else 24,
                     obstacle_range=250.0 if a.obs > 10 else 120.0)
 scenes = [highway_scene(s, rec) for s in range(a.scenes)]
