@@ -1478,7 +1478,7 @@ static int launch_numpy_normals(bd_ctx* ctx, const uint64_t* st4, long long coun
     a.z = z;
     a.positions = positions;
     a.err = ctx->nn_err.as<int>();
-    // grid-wide cooperative form: one position per thread over the whole GPU (5 grid barriers)
+    // grid-wide cooperative form: one position per thread over the whole GPU (2 grid barriers)
     int sms = 148, coop = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
     cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->device);

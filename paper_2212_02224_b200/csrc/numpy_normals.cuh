@@ -27,6 +27,10 @@
 //      forward; slow starts then mark the positions they consumed
 //   4. start flags -> block-wide exclusive scan -> draw index; starts below the requested count
 //      write z, and the raw positions at block boundaries go out to the host
+// Grid form (cooperative, one position per thread over the GPU): step 2 for every position, then
+// each CTA finds the starts of its own range with one warp walking the consumptions in shared
+// memory from the nearest sync point before the range (32 positions a step), then a grid-wide
+// scan of the per-CTA start counts places the draws: two grid barriers in all.
 #pragma once
 
 #include <cstdint>
@@ -254,8 +258,8 @@ __global__ void __launch_bounds__(NN_THREADS, 1) numpy_normals_kernel(const Nump
 
 // ---------------------------------------------------------------------------- grid-wide form
 // One position per thread (loop for larger counts), all CTAs co-resident (cooperative launch),
-// phases separated by grid barriers: raws -> draw at every position -> slow starts -> cover
-// painting -> per-CTA counts -> offsets, z and block positions.
+// two grid barriers: a draw at every position -> | starts of each CTA's range (one warp walks the
+// consumptions), per-CTA counts -> | offsets, z and block positions.
 struct NumpyNormalGrid {
     NumpyNormalArgs a;
     long long R;              // raw positions evaluated
@@ -268,6 +272,8 @@ struct NumpyNormalGrid {
 };
 
 constexpr int NN_GT = 256;                       // threads per CTA of the grid form
+constexpr int NN_HALO = 4096;                    // positions before a CTA's range searched for a sync point
+constexpr int NN_WB = 8192;                      // shared-memory window of consumptions (bytes)
 
 __device__ __forceinline__ void nn_grid_sync(unsigned* bar, int* err) {
     __shared__ unsigned s_gen;
@@ -293,45 +299,6 @@ __device__ __forceinline__ void nn_grid_sync(unsigned* bar, int* err) {
         }
     }
     __syncthreads();       // thread 0's acquire + the CTA barrier publish the other CTAs' writes
-}
-
-// Start status of position x: x starts a draw iff no earlier START reaches past it; only slow
-// positions reach, and only from within NN_CMAX before x.  Each level fetches the 80 consumptions
-// before x as five 16-byte loads held in registers and recurses into the (usually single) slow
-// position that reaches x.  -1 when the chain nests too deep or meets an unresolved draw (the
-// caller falls back to the sync-point walk).
-__device__ int nn_status(const unsigned char* gcv, long long x, int depth) {
-    if (depth > 8) return -1;
-    const long long base16 = x < NN_CMAX + 16 ? 0 : (x - NN_CMAX) & ~15ll;
-    uint4 w4[5];
-#pragma unroll
-    for (int u = 0; u < 5; ++u) w4[u] = __ldcg(reinterpret_cast<const uint4*>(gcv + base16) + u);
-    if (x < NN_CMAX + 16) {                         // stream start: replay the chain from position 0
-        long long cur = 0;
-#pragma unroll
-        for (int i = 0; i < 80; ++i) {
-            const uint32_t word = (&w4[i >> 4].x)[(i >> 2) & 3];
-            const int c = (int)((word >> (8 * (i & 3))) & 0xffu);
-            if (i < x && i == cur) {
-                if (c == 0) return -1;
-                cur += c;
-            }
-        }
-        return cur == x ? 1 : 0;
-    }
-#pragma unroll
-    for (int i = 0; i < 80; ++i) {
-        const uint32_t word = (&w4[i >> 4].x)[(i >> 2) & 3];
-        const int c = (int)((word >> (8 * (i & 3))) & 0xffu);
-        const long long p = base16 + i;
-        if (p >= x || p <= x - NN_CMAX || c == 1) continue;
-        if (c == 0) return -1;
-        if (p + c <= x) continue;
-        const int sp = nn_status(gcv, p, depth + 1);
-        if (sp < 0) return -1;
-        if (sp == 1) return 0;                     // a start reaches past x
-    }
-    return 1;
 }
 
 // draw_at with the raw values generated on the fly from the LCG state before position j (the
@@ -391,56 +358,118 @@ __global__ void __launch_bounds__(NN_GT) numpy_normals_grid_kernel(const NumpyNo
     }
     nn_grid_sync(g.bar, a.err);
     NG_T();
-    // ---- slow positions: start iff no start reaches past them (nn_status); the rare unresolved
-    //      case walks back to a sync point (CMAX fast positions in a row) and replays
-    for (long long j = tid; j < R; j += T) {
-        unsigned char v = 0;
-        if (g.cv[j] != 1) {
-            const int sj = nn_status(g.cv, j, 0);
-            if (sj >= 0) {
-                v = (unsigned char)sj;
-            } else {
-                long long q = j, run = 0;
-                while (q > 0 && run < NN_CMAX) {
-                    run = __ldcg(g.cv + q - 1) == 1 ? run + 1 : 0;
-                    --q;
+    // ---- starts of this CTA's positions [b0, b1), found by one warp walking the stream in shared
+    //      memory: back from b0 to a position that must start a draw (the stream start, or one
+    //      preceded by NN_CMAX - 1 fast positions: no earlier draw can reach past it), then forward,
+    //      32 positions a step -- a run of fast positions are all starts; a slow start skips what it
+    //      consumed.  Replaces a per-slow-position recursive status and two grid barriers.
+    const long long PB = (R + gridDim.x - 1) / gridDim.x;
+    const long long b0 = min(R, (long long)blockIdx.x * PB), b1 = min(R, b0 + PB);
+    __shared__ __align__(16) unsigned char s_cv[NN_WB];
+    __shared__ long long s_cnt;
+    for (long long j = b0 + threadIdx.x; j < b1; j += NN_GT) g.st[j] = 0;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    long long lo = max(0ll, b0 - NN_HALO) & ~15ll;
+    // s_cv[i] = cv[lo + i], 16-byte loads (positions past R read as fast: never slow)
+    for (int i = threadIdx.x; i < NN_WB / 16; i += NN_GT) {
+        const long long j = lo + 16ll * i;
+        uint4 v = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
+        if (j + 16 <= R) {
+            v = __ldcg(reinterpret_cast<const uint4*>(g.cv + j));
+        } else if (j < R) {
+            unsigned char* b = reinterpret_cast<unsigned char*>(&v);
+            for (int k = 0; k < 16 && j + k < R; ++k) b[k] = __ldcg(g.cv + j + k);
+        }
+        reinterpret_cast<uint4*>(s_cv)[i] = v;
+    }
+    __syncthreads();
+#ifdef BD_PHASE_TIMING
+    unsigned long long dbg_t[3];
+    long long dbg_q = 0;
+    int dbg_steps = 0;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(dbg_t[0]));
+#endif
+    if (w == 0 && b0 < b1) {
+#ifdef BD_PHASE_TIMING
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(dbg_t[1]));
+#endif
+        // (1) the sync point q <= b0
+        long long q = b0;
+        while (q > 0) {
+            // highest slow position in [q - NN_CMAX + 1, q - 1]
+            long long hi_slow = -1;
+            for (int h = 0; h < 2 && hi_slow < 0; ++h) {
+                const long long pos = q - 1 - (h * 32 + lane);
+                const bool in = pos >= 0 && pos > q - NN_CMAX;
+                const bool slow = in && pos >= lo && s_cv[pos - lo] != 1;
+                const bool lost = in && pos < lo;      // the halo ran out (practically never)
+                if (__any_sync(0xffffffffu, lost)) { q = -1; break; }
+                const unsigned m = __ballot_sync(0xffffffffu, slow);
+                if (m) hi_slow = q - 1 - (h * 32 + (__ffs(m) - 1));
+            }
+            if (q < 0 || hi_slow < 0) break;
+            q = hi_slow;
+        }
+        long long cnt = 0;
+        if (q < 0) {
+            if (lane == 0) atomicOr(a.err, 4);
+        } else {
+            // (2) forward from q: mark the starts in [b0, b1)
+            long long cur = q;
+            while (cur < b1) {
+                if (cur + 32 + NN_CMAX > lo + NN_WB) {   // slide the window (long CTA ranges)
+                    __syncwarp();
+                    lo = cur;
+                    for (int i = lane; i < NN_WB; i += 32) {
+                        const long long j = lo + i;
+                        s_cv[i] = j < R ? __ldcg(g.cv + j) : (unsigned char)1;
+                    }
+                    __syncwarp();
                 }
-                if (run >= NN_CMAX) q += NN_CMAX;
-                long long cur = q;
-                while (cur < j) {
-                    const int c = __ldcg(g.cv + cur);
-                    if (c == 0) break;
-                    cur += c;
+                const long long pos = cur + lane;
+#ifdef BD_PHASE_TIMING
+                ++dbg_steps;
+#endif
+                const int c = s_cv[pos - lo];
+                const unsigned m = __ballot_sync(0xffffffffu, c != 1);
+                const int f = m ? __ffs(m) - 1 : 32;
+                const bool mine = lane < f && pos >= b0 && pos < b1;
+                if (mine) g.st[pos] = 1;
+                cnt += __popc(__ballot_sync(0xffffffffu, mine));
+                if (f == 32) { cur += 32; continue; }
+                const long long p = cur + f;
+                const int cp = __shfl_sync(0xffffffffu, c, f);
+                if (cp == 0) {                      // a draw longer than NN_CMAX raw values
+                    if (lane == 0) atomicOr(a.err, 4);
+                    break;
                 }
-                v = cur == j ? 1 : 0;
+                if (p >= b0 && p < b1) {
+                    if (lane == 0) g.st[p] = 1;
+                    ++cnt;
+                }
+                cur = p + cp;
             }
         }
-        g.st[j] = v;
+        if (lane == 0) s_cnt = cnt;
+#ifdef BD_PHASE_TIMING
+        if (lane == 0) {
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(dbg_t[2]));
+            dbg_q = q;
+        }
+#endif
     }
-    nn_grid_sync(g.bar, a.err);
-    NG_T();
-    for (long long j = tid; j < R; j += T)              // slow starts mark the positions they consumed
-        if (g.st[j] == 1 && g.cv[j] > 1)
-            for (long long k = j + 1; k < j + g.cv[j] && k < R; ++k) g.st[k] = 2;
-    nn_grid_sync(g.bar, a.err);
+    __syncthreads();                                   // the st bytes of this range are final
     NG_T();
     // ---- starts, counted per CTA in position order: CTA b owns positions [b PB, (b+1) PB)
-    const long long PB = (R + gridDim.x - 1) / gridDim.x;
-    const long long b0 = (long long)blockIdx.x * PB, b1 = min(R, b0 + PB);
     __shared__ long long wsum[NN_GT / 32];
     __shared__ long long s_off;
     // each thread a contiguous sub-range of the CTA's positions
     const long long PT = (PB + NN_GT - 1) / NN_GT;
-    const long long t0 = b0 + threadIdx.x * PT, t1 = min(b1, t0 + PT);
+    const long long t0 = min(b1, b0 + threadIdx.x * PT), t1 = min(b1, t0 + PT);
     long long mine = 0;
-    for (long long j = t0; j < t1; ++j) {
-        const unsigned char v = (g.cv[j] == 1) ? (g.st[j] == 2 ? 0 : 1) : (g.st[j] == 1 ? 1 : 0);
-        g.st[j] = v;
-        mine += v;
-    }
+    for (long long j = t0; j < t1; ++j) mine += g.st[j];
     // CTA-wide inclusive scan of `mine` (warp shuffles, then the warp sums)
     long long incl = mine;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const long long v = __shfl_up_sync(0xffffffffu, incl, o);
@@ -450,7 +479,10 @@ __global__ void __launch_bounds__(NN_GT) numpy_normals_grid_kernel(const NumpyNo
     __syncthreads();
     long long wpre = 0;
     for (int k = 0; k < w; ++k) wpre += wsum[k];
-    if (threadIdx.x == NN_GT - 1) g.cta_count[blockIdx.x] = wpre + incl;
+    if (threadIdx.x == NN_GT - 1) {
+        g.cta_count[blockIdx.x] = wpre + incl;
+        if (b0 < b1 && wpre + incl != s_cnt) atomicOr(a.err, 4);   // walk and count disagree
+    }
     nn_grid_sync(g.bar, a.err);
     NG_T();
     if (threadIdx.x < 32) {                              // this CTA's offset: the counts before it
@@ -476,6 +508,9 @@ __global__ void __launch_bounds__(NN_GT) numpy_normals_grid_kernel(const NumpyNo
     }
 #ifdef BD_PHASE_TIMING
     NG_T();
+    if (threadIdx.x == 0 && b0 < b1)
+        printf("NNW cta %d q-b0 %lld steps %d load %.2f walk %.2f\n", blockIdx.x, dbg_q - b0, dbg_steps,
+               (dbg_t[0] - gt[1]) * 1e-3, (dbg_t[2] - dbg_t[1]) * 1e-3);
     if (tid == 0) {
         printf("NNG us:");
         for (int i = 1; i < ng; ++i) printf(" %.2f", (gt[i] - gt[i - 1]) * 1e-3);
