@@ -715,7 +715,7 @@ __device__ __forceinline__ void rem_eval(const float* __restrict__ wsm, const fl
 // sample warps then sweep 3 full slots instead of 3 + a 4-of-32-lane one (m = 100).  Mirrors
 // am_samples' CTA barriers one for one, including the per-iteration-maxima table's.
 template <int NPT, int MT, int TPB, int HELP>
-__device__ __noinline__ void am_helper(const AmArgs& a, int scene, int cta, int iters, unsigned char* smem) {
+__device__ __forceinline__ void am_helper(const AmArgs& a, int scene, int cta, int iters, unsigned char* smem) {
     constexpr int SPC = TPB / 32 - 1;
     static_assert(SPC * HELP <= 32, "remainder warp: one lane per (sample, remainder timestep)");
     const AmSmem lay(a.m, a.n_obs, a.neq, a.n_curv, a.s_cta, blockDim.x, 32, false, a.max_iters, HELP);

@@ -209,16 +209,26 @@ __global__ void cem_init_kernel(CemState s, const double* mean0, const double* c
     }
 }
 
-// Block-wide sum of one double per thread (result valid in every thread).
-__device__ __forceinline__ double block_sum(double v, double* red) {
-    for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+// Two block-wide sums in one pass (each in block_sum's order; results valid in every thread).
+// red holds 64 doubles.
+__device__ __forceinline__ double block_sum2(double v, double u, double* red, double& usum) {
+    for (int o = 16; o >= 1; o >>= 1) {
+        v += __shfl_xor_sync(0xffffffffu, v, o);
+        u += __shfl_xor_sync(0xffffffffu, u, o);
+    }
     __syncthreads();
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    if ((threadIdx.x & 31) == 0) {
+        red[threadIdx.x >> 5] = v;
+        red[32 + (threadIdx.x >> 5)] = u;
+    }
     __syncthreads();
-    // every warp folds the per-warp partials with shuffles (fixed order: deterministic)
     const int nw = blockDim.x >> 5, ln = threadIdx.x & 31;
-    double t = ln < nw ? red[ln] : 0.0;
-    for (int o = 16; o >= 1; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    double t = ln < nw ? red[ln] : 0.0, r = ln < nw ? red[32 + ln] : 0.0;
+    for (int o = 16; o >= 1; o >>= 1) {
+        t += __shfl_xor_sync(0xffffffffu, t, o);
+        r += __shfl_xor_sync(0xffffffffu, r, o);
+    }
+    usum = r;
     return t;
 }
 
@@ -314,7 +324,7 @@ __device__ __forceinline__ void rank_refit_block(const CemState& s, int it, cons
     int* idx2 = cidx + n;
     double* w = reinterpret_cast<double*>(idx2 + n);          // n ints + n ints: 8-byte aligned
     double* pe = w + n;                                       // q <= 128 staged; larger q read from global
-    __shared__ double red[32];
+    __shared__ double red[64];
     __shared__ double mu_new[MAX_DIM];
     __shared__ double cnew[MAX_DIM * MAX_DIM];
     __shared__ double csym[MAX_DIM * MAX_DIM], lsh[MAX_DIM * MAX_DIM];
@@ -396,8 +406,8 @@ __device__ __forceinline__ void rank_refit_block(const CemState& s, int it, cons
         if (s.elite_idx) s.elite_idx[(size_t)scene * q + i] = j;
         if (s.elite_aug) s.elite_aug[(size_t)scene * q + i] = aug;
     }
-    const double total = block_sum(part, red);
-    const double csum = block_sum(cpart, red);
+    double csum;
+    const double total = block_sum2(part, cpart, red, csum);
     RR_STAMP(3);
     const bool uniform = !(isfinite(total) && total > 0.0);
     for (int i = threadIdx.x; i < q; i += blockDim.x) w[i] = uniform ? 1.0 / q : w[i] / total;
@@ -422,9 +432,16 @@ __device__ __forceinline__ void rank_refit_block(const CemState& s, int it, cons
     {
         const int chunks = max(1, min(8, nsum / d)), e = threadIdx.x % d, ch = threadIdx.x / d;
         double a4[4] = {0.0, 0.0, 0.0, 0.0};
-        if (ch < chunks)
-#pragma unroll 4
-            for (int i = ch, u = 0; i < q; i += chunks, u = (u + 1) & 3) a4[u] = fma(w[i], P(i, e), a4[u]);
+        if (ch < chunks) {                  // element k of the chunk's sequence -> a4[k & 3]
+            int i = ch;
+            for (; i + 3 * chunks < q; i += 4 * chunks) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) a4[u] = fma(w[i + u * chunks], P(i + u * chunks, e), a4[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < 3; ++u)
+                if (i + u * chunks < q) a4[u] = fma(w[i + u * chunks], P(i + u * chunks, e), a4[u]);
+        }
         const double acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
         partial[threadIdx.x] = acc;
         __syncthreads();
@@ -442,9 +459,19 @@ __device__ __forceinline__ void rank_refit_block(const CemState& s, int it, cons
         double a4[4] = {0.0, 0.0, 0.0, 0.0};
         if (ch < chunks) {
             const double mr = mu_new[r], mc = mu_new[c];
-#pragma unroll 4
-            for (int i = ch, u = 0; i < q; i += chunks, u = (u + 1) & 3)
-                a4[u] = fma(w[i] * (P(i, r) - mr), P(i, c) - mc, a4[u]);
+            int i = ch;
+            for (; i + 3 * chunks < q; i += 4 * chunks) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int iu = i + u * chunks;
+                    a4[u] = fma(w[iu] * (P(iu, r) - mr), P(iu, c) - mc, a4[u]);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 3; ++u) {
+                const int iu = i + u * chunks;
+                if (iu < q) a4[u] = fma(w[iu] * (P(iu, r) - mr), P(iu, c) - mc, a4[u]);
+            }
         }
         const double acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
         partial[threadIdx.x] = acc;

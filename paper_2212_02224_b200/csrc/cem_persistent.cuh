@@ -75,6 +75,9 @@ __device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
 #ifndef BD_POLL_NS
 #define BD_POLL_NS 32
 #endif
+#ifndef BD_CTL_POLL_NS
+#define BD_CTL_POLL_NS 32
+#endif
 __device__ __forceinline__ void worker_arrive_wait(unsigned* bar, int* err) {
     __shared__ unsigned s_gen;
     __syncthreads();
@@ -84,7 +87,7 @@ __device__ __forceinline__ void worker_arrive_wait(unsigned* bar, int* err) {
         atomicAdd(bar, 1u);
         long long spins = 0;
         while (ld_acquire_gpu(bar + 1) == s_gen) {
-            __nanosleep(BD_POLL_NS);
+            if (BD_POLL_NS) __nanosleep(BD_POLL_NS);
             if (++spins > (1ll << 28)) { atomicOr(err, ERR_P2P_TIMEOUT); break; }
         }
         __threadfence();
@@ -99,7 +102,7 @@ __device__ __forceinline__ void control_gather(unsigned* bar, int* err, unsigned
     if (threadIdx.x == 0) {
         long long spins = 0;
         while (ld_acquire_gpu(bar) < workers) {
-            __nanosleep(32);
+            if (BD_CTL_POLL_NS) __nanosleep(BD_CTL_POLL_NS);
             if (++spins > (1ll << 28)) { atomicOr(err, ERR_P2P_TIMEOUT); break; }
         }
         bar[0] = 0u;
