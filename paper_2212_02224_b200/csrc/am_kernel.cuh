@@ -595,6 +595,13 @@ __device__ __forceinline__ void sweep_lat(const float* __restrict__ wsm, const f
 #define BD_NO_ITMAX 0      // diagnostic builds only: drop the per-iteration batch-max atomics
 #endif
 
+__device__ __forceinline__ void named_arrive(int id, int n) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
 // One timestep t of one sample for the remainder warp: the arithmetic of one sweep_lat slot
 // (phases A, B, C), its 22 back-projection partials, direct residual and cost written to out[0..23].
 // dap_h carries the timestep's clipped acceleration between iterations, as dap does for a slot.
@@ -732,9 +739,16 @@ __device__ __forceinline__ void am_helper(const AmArgs& a, int scene, int cta, i
     float dap_h = 0.f;
     int conf = 0;
     float* dst = out;                                       // idle lanes write their own (unread) slot
-    __syncthreads();                                        // coefficients of every sample staged
+    // named barriers: 1 = every sample's coefficients staged (samples arrive, this warp waits);
+    // 2 + s = the partials of sample s published (this warp arrives, sample s waits) -- a sample
+    // never waits for the other samples, only for the partials it needs
+    auto publish = [&]() {
+#pragma unroll
+        for (int k = 0; k < SPC; ++k) named_arrive(2 + k, 64);
+    };
+    named_sync(1, TPB);
     rem_eval<NPT, true>(wsm, osm, c32, t, L, dap_h, conf, count, true, dst);
-    __syncthreads();                                        // partials published
+    publish();
     const bool record = a.replay == nullptr && !BD_NO_ITMAX;
     unsigned* itm_s = reinterpret_cast<unsigned*>(smem + lay.itm);
     if (record) {
@@ -742,9 +756,9 @@ __device__ __forceinline__ void am_helper(const AmArgs& a, int scene, int cta, i
         __syncthreads();
     }
     for (int it = 0; it < iters; ++it) {
-        __syncthreads();
+        named_sync(1, TPB);
         rem_eval<NPT, false>(wsm, osm, c32, t, L, dap_h, conf, count, it == iters - 1, dst);
-        __syncthreads();
+        publish();
     }
     if (record) {
         __syncthreads();
@@ -904,7 +918,7 @@ __device__ __forceinline__ void am_samples(const AmArgs& a, int scene, int blk, 
             if (!(threadIdx.x & 32) && lane < NX + 2) v[0] += xbuf[lane];
         }
         if constexpr (HELPED) {                       // the remainder warp's timesteps of this sample
-            __syncthreads();
+            named_sync(2 + slot, 64);
             if (lane < NX + 2) {
                 float h = hsm[0];
 #pragma unroll
@@ -913,7 +927,7 @@ __device__ __forceinline__ void am_samples(const AmArgs& a, int scene, int blk, 
             }
         }
     };
-    if constexpr (HELPED) __syncthreads();           // every sample's coefficients staged (am_helper)
+    if constexpr (HELPED) named_arrive(1, TPB);      // this sample's coefficients staged (am_helper)
     if constexpr (LAT32)
         sweep_lat<P, true, NV, MT, NPT, TPB, HELPED>(wsm, osm, cxy, v, dap, p, L, conf, true);
     else
@@ -979,7 +993,7 @@ __device__ __forceinline__ void am_samples(const AmArgs& a, int scene, int blk, 
 #pragma unroll
         for (int q = 0; q < NC; ++q) cxy[q] = reinterpret_cast<const float2*>(sc)[q];
         // ---- projections, back-projection, residual at the new iterate
-        if constexpr (HELPED) __syncthreads();
+        if constexpr (HELPED) named_arrive(1, TPB);
         if constexpr (LAT32)
             sweep_lat<P, false, NV, MT, NPT, TPB, HELPED>(wsm, osm, cxy, v, dap, p, L, conf, it == iters - 1);
         else
