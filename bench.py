@@ -238,7 +238,7 @@ def cvae_config3(device: int, cycles: int = 120):
         assert not res.degraded
     return {"p50_ms": float(np.percentile(ts, 50)), "p99_ms": float(np.percentile(ts, 99)), "cycles": cycles,
             "config": "CVAE decode of 1000 set-points (tcgen05 bf16 hidden layers) + config-2 CEM cycle warm-started "
-                      "from them; host call to host-visible best xi"}
+                      "from them (rows stay on the device: bd_cvae_warm_start); host call to host-visible best xi"}
 
 
 def dense_config4(device: int, steps: int = 3):

@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define BD_ABI_VERSION 3
+#define BD_ABI_VERSION 4
 
 #define BD_OK 0
 #define BD_ERR_VALUE (-1)      /* ValueError        pkg/batch_qp.py:99-106,223-227,265-269; pkg/projection.py:225-233 */
@@ -313,6 +313,14 @@ int bd_cvae_set_weights(bd_ctx* ctx, int n_layers, const int* dims, const float*
                         const float* const* biases);
 int bd_cvae_decode(bd_ctx* ctx, int count, const float* obs /* 55 */, const float* z /* count x 2 */,
                    double* params /* count x dim */);
+/* The decoder's samples as warm-start rows, kept on the device: rows = decode * scale + shift
+ * (per column; either may be NULL; two float64 roundings, as numpy's p * scale + shift).
+ * *rows_dev receives the device address of the count x dim rows, valid until the next call of
+ * this function on the context; pass it as bd_cem_cycle's `warm` (device pointers are used in
+ * place).  params (host or device, count x dim) may be NULL: then nothing is copied back and
+ * the call does not synchronise. */
+int bd_cvae_warm_start(bd_ctx* ctx, int count, const float* obs, const float* z, const double* scale,
+                       const double* shift, double* params, const double** rows_dev);
 
 #ifdef __cplusplus
 }

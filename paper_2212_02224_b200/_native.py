@@ -64,6 +64,7 @@ SIGNATURES = {
                            _P]),
     "bd_cvae_set_weights": (c_int, [_P, c_int, _P, _P, _P]),
     "bd_cvae_decode": (c_int, [_P, c_int, _P, _P, _P]),
+    "bd_cvae_warm_start": (c_int, [_P, c_int, _P, _P, _P, _P, _P, _P]),
 }
 
 

@@ -26,7 +26,7 @@ from . import numpy_stream
 from ._native import CemConfig, f64, ptr, upload_scenes
 from .basis import PolynomialBasis, TrajectoryCoeffs, eval_trajectory
 from .batch_qp import NumericalFailure, QPSolutionBatch, TrackingWeights, build_qp_structure
-from .behavior import BehaviorParams, ParamLayout, WarmStartSource
+from .behavior import BehaviorParams, DeviceWarmStart, ParamLayout, WarmStartSource
 from .constraints import PlanningScene
 from .projection import ProjectionBatchResult, ProjectionConfig, ProjectionOperator, require_device_order
 
@@ -296,8 +296,11 @@ def solve_bilevel(scene: PlanningScene, solver: LowerLevelSolver, config: BiLeve
     solver.projector._ensure_scene(scene)
     pcfg = solver.projector.config
     state0 = rng.bit_generator.state
-    warm = f64(warm_start.draw(B)) if warm_start is not None else None
-    n_draw = N - (1 if warm is not None else 0)
+    # device-resident rows (CVAE decoder, same context) go to the cycle in place
+    warm_dev = warm_start.device_rows(solver.context, B) if isinstance(warm_start, DeviceWarmStart) else None
+    warm = f64(warm_start.draw(B)) if warm_start is not None and warm_dev is None else None
+    warm_arg = ctypes.c_void_p(warm_dev) if warm_dev is not None else ptr(warm)
+    n_draw = N - (1 if warm_start is not None else 0)
     bi = np.zeros(1, dtype=np.int64)
     bp = np.zeros(dim)
     bx = np.zeros(2 * solver.basis.num_coeffs)
@@ -322,7 +325,7 @@ def solve_bilevel(scene: PlanningScene, solver: LowerLevelSolver, config: BiLeve
         cfg.pcg64_state = st_words.ctypes.data
         cfg.pcg64_positions = pos.ctypes.data
         try:
-            solver.context.call("bd_cem_cycle", 1, ctypes.byref(cfg), mean0, cov0, None, ptr(warm), ptr(bi), ptr(bp),
+            solver.context.call("bd_cem_cycle", 1, ctypes.byref(cfg), mean0, cov0, None, warm_arg, ptr(bi), ptr(bp),
                                 ptr(bx), ptr(bc), ptr(br), ptr(ba), ptr(st), ptr(fm), ptr(fc), ptr(done))
         except RuntimeError as e:
             if "numpy normal stream" not in str(e):
@@ -331,7 +334,7 @@ def solve_bilevel(scene: PlanningScene, solver: LowerLevelSolver, config: BiLeve
         else:
             k = int(done[0])
             attempted = N if k >= N else (1 if k <= 0 else k + 1)
-            consumed = attempted - (1 if warm is not None else 0)
+            consumed = attempted - (1 if warm_start is not None else 0)
             if consumed > 0:
                 # PCG64.advance drops a buffered 32-bit half; standard_normal never touches it
                 buf = rng.bit_generator.state
@@ -345,13 +348,13 @@ def solve_bilevel(scene: PlanningScene, solver: LowerLevelSolver, config: BiLeve
     # Iteration 1 is launched as soon as its draws exist; the remaining N-1 batches of the caller's
     # Generator are drawn while the GPU runs it (the stream is the same sequence as one
     # standard_normal((N, B, dim)) call), then iterations 2..N follow in a second call.
-    z1 = None if warm is not None else rng.standard_normal((1, B, dim))
+    z1 = None if warm_start is not None else rng.standard_normal((1, B, dim))
     if N == 1:
-        solver.context.call("bd_cem_cycle", 1, ctypes.byref(cfg_range(0, 1)), mean0, cov0, ptr(z1), ptr(warm),
+        solver.context.call("bd_cem_cycle", 1, ctypes.byref(cfg_range(0, 1)), mean0, cov0, ptr(z1), warm_arg,
                             ptr(bi), ptr(bp), ptr(bx), ptr(bc), ptr(br), ptr(ba), ptr(st), ptr(fm), ptr(fc),
                             ptr(done))
     else:
-        solver.context.call("bd_cem_cycle", 1, ctypes.byref(cfg_range(0, 1)), mean0, cov0, ptr(z1), ptr(warm),
+        solver.context.call("bd_cem_cycle", 1, ctypes.byref(cfg_range(0, 1)), mean0, cov0, ptr(z1), warm_arg,
                             None, None, None, None, None, None, None, None, None, None)
         z = rng.standard_normal((N - 1, B, dim))
         solver.context.call("bd_cem_cycle", 1, ctypes.byref(cfg_range(1, N)), mean0, cov0, ptr(z), None,
@@ -359,7 +362,7 @@ def solve_bilevel(scene: PlanningScene, solver: LowerLevelSolver, config: BiLeve
                             ptr(done))
     k = int(done[0])
     attempted = N if k >= N else (1 if k <= 0 else k + 1)
-    consumed = attempted - (1 if warm is not None else 0)
+    consumed = attempted - (1 if warm_start is not None else 0)
     if consumed != n_draw:   # leave the caller's generator exactly where the reference would
         rng.bit_generator.state = state0
         if consumed > 0:

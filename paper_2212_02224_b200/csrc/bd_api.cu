@@ -134,6 +134,7 @@ struct bd_ctx {
     std::vector<DevBuf*> cvae_w, cvae_b, cvae_w16;
     DevBuf cvae_h0, cvae_h1, cvae_obs, cvae_z, cvae_a0, cvae_a1;
     DevBuf cvae_ready;          // fused decoder's arrival counters (persist across launches)
+    DevBuf cvae_warm;           // bd_cvae_warm_start's rows (valid until its next call)
     int cvae_tc = 1;            // option "cvae_tensor_cores": bf16 tcgen05 hidden layers (1) or fp32 SIMT (0)
     int cvae_fused = 1;         // option "cvae_fused": the whole decoder in one persistent launch (1) or per layer (0)
     bool err_sticky = false;    // option "sticky_errors": entry points accumulate into the error word
@@ -1967,19 +1968,11 @@ bool make_map_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t c
 }
 }  // namespace
 
-int bd_cvae_decode(bd_ctx* ctx, int count, const float* obs, const float* z, double* params) {
-    NvtxRange nvtx_("bd_cvae_decode");
-    if (!ctx || count < 1 || !obs || !z || !params) return BD_ERR_VALUE;
-    if (ctx->cvae_w.empty()) return fail(ctx, BD_ERR_STATE, "CVAE weights not set");
-    begin_call(ctx);
-    int rc;
+// The decoder's launches for `count` samples (inputs and the count x out_dim output on the device).
+static int cvae_decode_dev(bd_ctx* ctx, int count, const float* dobs, const float* dz, double* dout) {
     const auto& d = ctx->cvae_dims;
     const int L = (int)ctx->cvae_w.size();
     const int zdim = d[0] - CVAE_OBS;
-    if (zdim < 1) return fail(ctx, BD_ERR_VALUE, "first layer must take 55 observation + latent inputs");
-    const float *dobs, *dz;
-    if ((rc = stage_in(ctx, obs, (size_t)CVAE_OBS, &dobs))) return rc;
-    if ((rc = stage_in(ctx, z, (size_t)count * zdim, &dz))) return rc;
     int widest = 0;
     for (int l = 1; l <= L; ++l) widest = widest > d[l] ? widest : d[l];
     bool tc_ok = ctx->cvae_tc && L >= 3 && tensor_map_encoder() != nullptr;
@@ -2011,9 +2004,6 @@ int bd_cvae_decode(bd_ctx* ctx, int count, const float* obs, const float* z, dou
                 ctx->fz_ctr_mblocks = mblocks;
             }
             ++ctx->fz_epoch;
-            double* dout;
-            DevBuf& ws = ctx->stage[7];
-            if ((rc = stage_out(ctx, params, (size_t)count * d[L], ws, &dout))) return rc;
             FusedArgs fa{};
             FusedMaps fm{};
             fa.count = count; fa.nh = nh; fa.zdim = zdim;
@@ -2052,7 +2042,7 @@ int bd_cvae_decode(bd_ctx* ctx, int count, const float* obs, const float* z, dou
                                                         FZ_SMEM, ctx->stream);
             if (e != cudaSuccess) return fail(ctx, BD_ERR_CUDA, "fused CVAE launch: %s", cudaGetErrorString(e));
             ctx->launches++;
-            return finish_call(ctx, false, 0);
+            return 0;
         }
     }
     if (tc_ok) {
@@ -2060,9 +2050,6 @@ int bd_cvae_decode(bd_ctx* ctx, int count, const float* obs, const float* z, dou
         CU(ctx->cvae_a0.ensure((size_t)mpad * widest * 2));
         CU(ctx->cvae_a1.ensure((size_t)mpad * widest * 2));
         CU(cudaMemsetAsync(ctx->cvae_a0.p, 0, (size_t)mpad * widest * 2, ctx->stream));
-        double* dout;
-        DevBuf& ws = ctx->stage[7];
-        if ((rc = stage_out(ctx, params, (size_t)count * d[L], ws, &dout))) return rc;
         auto* cur = ctx->cvae_a0.as<__nv_bfloat16>();
         auto* nxt = ctx->cvae_a1.as<__nv_bfloat16>();
         cvae_first_layer_bf16<<<dim3((d[1] + 127) / 128, (count + 31) / 32), dim3(128), 0, ctx->stream>>>(
@@ -2086,13 +2073,10 @@ int bd_cvae_decode(bd_ctx* ctx, int count, const float* obs, const float* z, dou
                                                                        ctx->cvae_w[L - 1]->as<float>(),
                                                                        ctx->cvae_b[L - 1]->as<float>(), dout);
         ctx->launches++;
-        return finish_call(ctx, false, 0);
+        return 0;
     }
     CU(ctx->cvae_h0.ensure((size_t)count * widest * 4));
     CU(ctx->cvae_h1.ensure((size_t)count * widest * 4));
-    double* dout;
-    DevBuf& ws = ctx->stage[7];
-    if ((rc = stage_out(ctx, params, (size_t)count * d[L], ws, &dout))) return rc;
     // layer 0: scene part W[:, :55] obs is shared by every sample
     cvae_first_layer<<<dim3((d[1] + 127) / 128, (count + 31) / 32), dim3(128), 0, ctx->stream>>>(
         count, d[1], zdim, ctx->cvae_w[0]->as<float>(), ctx->cvae_b[0]->as<float>(), dobs, dz,
@@ -2113,6 +2097,72 @@ int bd_cvae_decode(bd_ctx* ctx, int count, const float* obs, const float* z, dou
     cvae_to_double<<<(unsigned)(((size_t)count * d[L] + 255) / 256), 256, 0, ctx->stream>>>(cur, dout,
                                                                                            (size_t)count * d[L]);
     ctx->launches++;
+    return 0;
+}
+
+static int cvae_stage_inputs(bd_ctx* ctx, int count, const float* obs, const float* z, const float** dobs,
+                             const float** dz) {
+    if (ctx->cvae_w.empty()) return fail(ctx, BD_ERR_STATE, "CVAE weights not set");
+    const int zdim = ctx->cvae_dims[0] - CVAE_OBS;
+    if (zdim < 1) return fail(ctx, BD_ERR_VALUE, "first layer must take 55 observation + latent inputs");
+    int rc;
+    if ((rc = stage_in(ctx, obs, (size_t)CVAE_OBS, dobs))) return rc;
+    return stage_in(ctx, z, (size_t)count * zdim, dz);
+}
+
+int bd_cvae_decode(bd_ctx* ctx, int count, const float* obs, const float* z, double* params) {
+    NvtxRange nvtx_("bd_cvae_decode");
+    if (!ctx || count < 1 || !obs || !z || !params) return BD_ERR_VALUE;
+    begin_call(ctx);
+    int rc;
+    const float *dobs, *dz;
+    if ((rc = cvae_stage_inputs(ctx, count, obs, z, &dobs, &dz))) return rc;
+    double* dout;
+    if ((rc = stage_out(ctx, params, (size_t)count * ctx->cvae_dims.back(), ctx->stage[7], &dout))) return rc;
+    if ((rc = cvae_decode_dev(ctx, count, dobs, dz, dout))) return rc;
+    return finish_call(ctx, false, 0);
+}
+
+// p = decode * scale + shift, rounded like the host's two float64 steps (no fused multiply-add).
+__global__ void rows_affine_kernel(int count, int dim, double* rows, const double* scale, const double* shift) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long long)count * dim) return;
+    const int c = (int)(i % dim);
+    double v = rows[i];
+    if (scale) v = __dmul_rn(v, scale[c]);
+    if (shift) v = __dadd_rn(v, shift[c]);
+    rows[i] = v;
+}
+
+int bd_cvae_warm_start(bd_ctx* ctx, int count, const float* obs, const float* z, const double* scale,
+                       const double* shift, double* params, const double** rows_dev) {
+    NvtxRange nvtx_("bd_cvae_warm_start");
+    if (!ctx || count < 1 || !obs || !z || !rows_dev) return BD_ERR_VALUE;
+    begin_call(ctx);
+    int rc;
+    const float *dobs, *dz;
+    if ((rc = cvae_stage_inputs(ctx, count, obs, z, &dobs, &dz))) return rc;
+    const int dim = ctx->cvae_dims.back();
+    const double *dsc = nullptr, *dsh = nullptr;
+    if ((rc = stage_in(ctx, scale, (size_t)dim, &dsc))) return rc;
+    if ((rc = stage_in(ctx, shift, (size_t)dim, &dsh))) return rc;
+    CU(ctx->cvae_warm.ensure((size_t)count * dim * 8));
+    double* rows = ctx->cvae_warm.as<double>();
+    if ((rc = cvae_decode_dev(ctx, count, dobs, dz, rows))) return rc;
+    if (dsc || dsh) {
+        rows_affine_kernel<<<(unsigned)(((size_t)count * dim + 255) / 256), 256, 0, ctx->stream>>>(count, dim, rows,
+                                                                                                  dsc, dsh);
+        ctx->launches++;
+    }
+    if (params) {
+        if (is_device_ptr(params)) {
+            CU(cudaMemcpyAsync(params, rows, (size_t)count * dim * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+        } else {
+            ctx->pending.push_back({params, rows, (size_t)count * dim * 8});
+            ctx->host_out = true;
+        }
+    }
+    *rows_dev = rows;
     return finish_call(ctx, false, 0);
 }
 

@@ -18,7 +18,7 @@ import ctypes
 import numpy as np
 
 from ._native import Context
-from .behavior import ParamLayout, WarmStartSource
+from .behavior import DeviceWarmStart, ParamLayout, WarmStartSource
 
 __all__ = ["CVAEDecoder", "fold_batchnorm", "OBS_DIM", "LATENT_DIM", "HIDDEN"]
 
@@ -87,10 +87,34 @@ class CVAEDecoder:
     def warm_start(self, obs: np.ndarray, count: int, layout: ParamLayout, rng: np.random.Generator,
                    scale: np.ndarray | None = None, shift: np.ndarray | None = None) -> WarmStartSource:
         """Decode `count` samples (z ~ N(0, I)) into the reference's warm-start interface.
-        `scale`/`shift` map the decoder output to set-point units (y [m], v [m/s])."""
-        p = self.decode(obs, rng.standard_normal((count, self.latent_dim)))
-        if scale is not None:
-            p = p * np.asarray(scale)
-        if shift is not None:
-            p = p + np.asarray(shift)
-        return WarmStartSource(p, layout)
+        `scale`/`shift` map the decoder output to set-point units (y [m], v [m/s]):
+        rows = decode * scale + shift.  The rows stay on the device (`bd_cvae_warm_start`) and
+        `solve_bilevel` on the same context feeds them to the cycle in place; `samples` / `draw`
+        build the host copy on first use."""
+        if layout.dim != self.out_dim:
+            raise ValueError(f"decoder rows have {self.out_dim} columns, the layout {layout.dim}")
+        obs32 = np.ascontiguousarray(np.asarray(obs, dtype=np.float32).reshape(-1))
+        if obs32.shape != (OBS_DIM,):
+            raise ValueError(f"need obs ({OBS_DIM},)")
+        z = rng.standard_normal((count, self.latent_dim))
+        z32 = np.ascontiguousarray(z, dtype=np.float32)
+        sc = None if scale is None else np.ascontiguousarray(np.broadcast_to(np.asarray(scale, dtype=np.float64),
+                                                                             (self.out_dim,)))
+        sh = None if shift is None else np.ascontiguousarray(np.broadcast_to(np.asarray(shift, dtype=np.float64),
+                                                                             (self.out_dim,)))
+        rows = ctypes.c_void_p()
+        self.ctx.call("bd_cvae_warm_start", count, obs32.ctypes.data, z32.ctypes.data,
+                      None if sc is None else sc.ctypes.data, None if sh is None else sh.ctypes.data, None,
+                      ctypes.addressof(rows))
+        gen = getattr(self.ctx, "_warm_gen", 0) + 1
+        self.ctx._warm_gen = gen
+
+        def materialize():
+            p = self.decode(obs32, z32)
+            if sc is not None:
+                p = p * sc
+            if sh is not None:
+                p = p + sh
+            return p
+
+        return DeviceWarmStart(self.ctx, rows.value, count, layout, gen, materialize)

@@ -109,3 +109,75 @@ def test_config3_cvae_warm_start_then_cem():
                            np.random.default_rng(6), warm_start=ws)
     assert len(one.diagnostics) == 1 and 0 <= one.best.index < 1000
     np.testing.assert_array_equal(one.best.params.to_vector(), ws.samples[one.best.index])
+
+
+def _c3_setup(seed=2):
+    import paper_2212_02224_b200 as bd
+    from paper_2212_02224_b200.cvae import CVAEDecoder
+    from paper_2212_02224_b200.fleet import initial_distribution
+    from paper_2212_02224_b200.scenes import highway_scene
+    basis = bd.build_basis(10, 100, 5.0, "bernstein")
+    solver = bd.LowerLevelSolver(basis, bd.TrackingWeights(), bd.ParamLayout(4), bd.ProjectionConfig(1.0, 100, 1e-3), 10)
+    scene = highway_scene(seed)
+    mean, cov = initial_distribution(scene)
+    dec = CVAEDecoder.synthetic(3, context=solver.context)
+    return bd, solver, scene, mean, cov, dec
+
+
+def _same_result(a, b):
+    assert a.best.index == b.best.index and a.degraded == b.degraded
+    np.testing.assert_array_equal(a.best.coeffs.stacked(), b.best.coeffs.stacked())
+    np.testing.assert_array_equal(a.distribution.mean, b.distribution.mean)
+    np.testing.assert_array_equal(a.distribution.cov, b.distribution.cov)
+    assert [d.cov_trace for d in a.diagnostics] == [d.cov_trace for d in b.diagnostics]
+
+
+def test_device_warm_start_rows_and_cycle_match_host_rows():
+    """bd_cvae_warm_start keeps the rows on the device and solve_bilevel feeds them to the cycle in
+    place: the rows equal decode * scale + shift computed on the host (float64, two roundings),
+    the generator advances by the same count x 2 normals, and the cycle is bit-identical to the
+    one fed the host copy through the reference's WarmStartSource."""
+    from paper_2212_02224_b200.behavior import DeviceWarmStart, WarmStartSource
+    bd, solver, scene, mean, cov, dec = _c3_setup()
+    obs = np.linspace(-1.0, 1.0, 55)
+    scale = np.array([1.5, 1.5, 1.5, 1.5, 2.0, 2.0, 2.0, 2.0])
+    shift = mean - 0.3
+    r1, r2 = np.random.default_rng(11), np.random.default_rng(11)
+    ws = dec.warm_start(obs, 1000, solver.layout, r1, scale=scale, shift=shift)
+    assert isinstance(ws, DeviceWarmStart) and ws.device_rows(solver.context, 1000) is not None
+    z = r2.standard_normal((1000, 2))
+    assert r1.bit_generator.state == r2.bit_generator.state
+    want = dec.decode(obs, z) * scale + shift
+    np.testing.assert_array_equal(ws.samples, want)
+    cfg = bd.BiLevelConfig(1000, 150, 100, 4, 0.7, 0.9, 1.0, mean, cov)
+    ga, gb = np.random.default_rng(6), np.random.default_rng(6)
+    ws2 = dec.warm_start(obs, 1000, solver.layout, np.random.default_rng(11), scale=scale, shift=shift)
+    a = bd.solve_bilevel(scene, solver, cfg, ga, warm_start=ws2)
+    b = bd.solve_bilevel(scene, solver, cfg, gb, warm_start=WarmStartSource(want, solver.layout))
+    _same_result(a, b)
+    assert ga.bit_generator.state == gb.bit_generator.state
+
+
+def test_device_warm_start_stale_or_short_rows_use_the_host_copy():
+    """A later decode overwrites the context's device rows: the earlier source then goes through
+    its host copy (same results); a batch larger than the rows repeats them cyclically (host)."""
+    from paper_2212_02224_b200.behavior import WarmStartSource
+    bd, solver, scene, mean, cov, dec = _c3_setup(4)
+    obs = np.zeros(55)
+    shift = mean.copy()
+    old = dec.warm_start(obs, 1000, solver.layout, np.random.default_rng(1), shift=shift)
+    dec.warm_start(obs, 1000, solver.layout, np.random.default_rng(2), shift=shift)
+    assert old.device_rows(solver.context, 1000) is None
+    cfg = bd.BiLevelConfig(1000, 150, 100, 2, 0.7, 0.9, 1.0, mean, cov)
+    a = bd.solve_bilevel(scene, solver, cfg, np.random.default_rng(3), warm_start=old)
+    b = bd.solve_bilevel(scene, solver, cfg, np.random.default_rng(3), warm_start=WarmStartSource(old.samples,
+                                                                                                  solver.layout))
+    _same_result(a, b)
+    short = dec.warm_start(obs, 600, solver.layout, np.random.default_rng(4), shift=shift)
+    assert short.device_rows(solver.context, 1000) is None
+    c = bd.solve_bilevel(scene, solver, cfg, np.random.default_rng(3), warm_start=short)
+    d = bd.solve_bilevel(scene, solver, cfg, np.random.default_rng(3),
+                         warm_start=WarmStartSource(short.samples, solver.layout))
+    _same_result(c, d)
+    with pytest.raises(ValueError):
+        dec.warm_start(obs, 10, bd.ParamLayout(3), np.random.default_rng(0))

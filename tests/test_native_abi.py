@@ -36,7 +36,7 @@ def test_library_exports_every_declared_symbol(lib):
 
 
 def test_abi_version(lib):
-    assert lib.bd_abi_version() == 3
+    assert lib.bd_abi_version() == 4
 
 
 def test_struct_layouts():
