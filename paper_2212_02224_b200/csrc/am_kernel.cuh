@@ -182,6 +182,39 @@ __device__ __forceinline__ void group_reduce_scatter(float (&v)[NV], int lane) {
     }
 }
 
+// The same reduce-scatter for one-warp groups with NREAL live values (the rest zero padding):
+// the sums go through packed FADD2 two slots at a time, and in the first stage a pair whose
+// upper slot is padding needs only the lower lanes' result (the upper lanes end up owning padding
+// values, which nothing reads), so it skips the two selects.  Sums identical to
+// group_reduce_scatter<32>.
+template <int NREAL>
+__device__ __forceinline__ void reduce_scatter32(float (&v)[32], int lane) {
+    static_assert(NREAL > 16 && NREAL <= 32 && NREAL % 2 == 0, "live values: 17-32, even");
+    constexpr unsigned FULL = 0xffffffffu;
+#pragma unroll
+    for (int o = 16; o >= 2; o >>= 1) {
+        const bool hi = (lane & o) != 0;
+#pragma unroll
+        for (int k = 0; k < o; k += 2) {
+            float2 keep, recv;
+            if (o == 16 && k + 16 >= NREAL) {
+                keep = make_float2(v[k], v[k + 1]);
+                recv = make_float2(__shfl_xor_sync(FULL, v[k], 16), __shfl_xor_sync(FULL, v[k + 1], 16));
+            } else {
+                keep = make_float2(hi ? v[k | o] : v[k], hi ? v[(k + 1) | o] : v[k + 1]);
+                const float s0 = hi ? v[k] : v[k | o], s1 = hi ? v[k + 1] : v[(k + 1) | o];
+                recv = make_float2(__shfl_xor_sync(FULL, s0, o), __shfl_xor_sync(FULL, s1, o));
+            }
+            const float2 r = fadd2(keep, recv);
+            v[k] = r.x;
+            v[k + 1] = r.y;
+        }
+    }
+    const bool hi = (lane & 1) != 0;
+    const float keep = hi ? v[1] : v[0], send = hi ? v[0] : v[1];
+    v[0] = keep + __shfl_xor_sync(FULL, send, 1);
+}
+
 // One sweep over this lane's timesteps at the current coefficients cxy[k] = (c_x[k], c_y[k]):
 // forward evaluation, polar split + coupled clips, back-projection of the residuals
 // (v[2k] = g_x[k], v[2k+1] = g_y[k]), the direct residual (v[22]) and the upper cost (v[23]).
@@ -911,7 +944,10 @@ __device__ __forceinline__ void am_samples(const AmArgs& a, int scene, int blk, 
     float* xbuf = reinterpret_cast<float*>(smem + lay.scr + (size_t)slot * AmSmem::SCR_BYTES + 672);
     const float* hsm = reinterpret_cast<const float*>(smem + lay.hlp) + slot * HELP * AmSmem::HSTR + lane;
     auto reduce = [&]() {
-        group_reduce_scatter<RP>(v, lane);
+        if constexpr (HELPED && NV == 32)
+            reduce_scatter32<NX + 2>(v, lane);
+        else
+            group_reduce_scatter<RP>(v, lane);
         if (PAIR) {                                   // second warp -> first warp partial sums
             if ((threadIdx.x & 32) && lane < NX + 2) xbuf[lane] = v[0];
             pair_sync();
