@@ -167,55 +167,64 @@ __global__ void __launch_bounds__(128, 1) cvae_fused_kernel(const __grid_constan
         const int zd = a.zdim;
         for (int t = blockIdx.x; t < mblocks * nb; t += gridDim.x) {
             const int m = t / nb, n = t % nb;
-            // the block's latent rows, staged once (coalesced) instead of a dependent load per row
+            // every global load of the tile is issued before any is used (one L2 round trip): the
+            // block's latent rows, the observation terms of its 64 outputs (two threads per output,
+            // 28 / 27 terms each) and the latent weights
+            const int cl = threadIdx.x & 63, half = threadIdx.x >> 6;
+            const int c = n * FZ_BN + cl;
+            const float* wr = a.W0 + (size_t)c * K;
+            constexpr int OT = (CVAE_OBS + 1) / 2;
+            float wv[OT], ov[OT];
+#pragma unroll
+            for (int j = 0; j < OT; ++j) {
+                const int k = half + 2 * j;
+                wv[j] = k < CVAE_OBS ? __ldg(wr + k) : 0.f;
+                ov[j] = k < CVAE_OBS ? __ldg(a.obs + k) : 0.f;
+            }
             for (int i = threadIdx.x; i < FZ_BM * zd; i += blockDim.x) {
                 const int r = m * FZ_BM + i / zd;
                 zs[i] = r < count ? a.z[(size_t)m * FZ_BM * zd + i] : 0.f;
             }
-            // observation part of each of the tile's 64 outputs: two threads per output split the
-            // 55 terms (independent loads, short chains), then the latent weights to shared memory
-            FZ_STAMP();
-            const int cl = threadIdx.x & 63, half = threadIdx.x >> 6;
-            const int c = n * FZ_BN + cl;
-            const float* wr = a.W0 + (size_t)c * K;
-            float sp = 0.f;
-#pragma unroll 7
-            for (int k = half; k < CVAE_OBS; k += 2) sp = fmaf(__ldg(wr + k), __ldg(a.obs + k), sp);
             for (int i = threadIdx.x; i < FZ_BN * zd; i += blockDim.x)
                 w0z[i] = __ldg(a.W0 + (size_t)(n * FZ_BN + i / zd) * K + CVAE_OBS + i % zd);
+            FZ_STAMP();
+            float sp = 0.f;
+#pragma unroll
+            for (int j = 0; j < OT; ++j) sp = fmaf(wv[j], ov[j], sp);
             float* sps = zs + FZ_BM * FZ_MAXZ / 2;                        // [2][64] halves, then [64] sums
             sps[half * FZ_BN + cl] = sp;
             __syncthreads();
             if (threadIdx.x < FZ_BN) sps[2 * FZ_BN + cl] = a.bias[0][c] + (sps[cl] + sps[FZ_BN + cl]);
             __syncthreads();
             FZ_STAMP();
-            // thread = row: the tile's 64 outputs of one sample, written as eight 16-byte stores
-            const int rl = threadIdx.x, r = m * FZ_BM + rl;
-            float zr[FZ_MAXZ / 2];
+            // eight threads per row, each one 16-byte chunk (8 outputs) of the row's 128-byte
+            // segment: a warp stores four whole segments per instruction (coalesced)
+            const int q = threadIdx.x & 7;
+#pragma unroll 2
+            for (int rl = threadIdx.x >> 3; rl < FZ_BM; rl += 128 / 8) {
+                const int r = m * FZ_BM + rl;
+                float zr[FZ_MAXZ / 2];
 #pragma unroll
-            for (int k = 0; k < FZ_MAXZ / 2; ++k) zr[k] = k < zd ? zs[rl * zd + k] : 0.f;
-            if (r < count) {
-                uint4* dst = reinterpret_cast<uint4*>(a.act[0] + (size_t)r * N + n * FZ_BN);
+                for (int k = 0; k < FZ_MAXZ / 2; ++k) zr[k] = k < zd ? zs[rl * zd + k] : 0.f;
+                uint32_t pk[4];
 #pragma unroll
-                for (int q = 0; q < FZ_BN / 8; ++q) {
-                    uint32_t pk[4];
+                for (int j = 0; j < 4; ++j) {
+                    float v2[2];
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        float v2[2];
+                    for (int e = 0; e < 2; ++e) {
+                        const int cc = q * 8 + 2 * j + e;
+                        float acc = sps[2 * FZ_BN + cc];
 #pragma unroll
-                        for (int e = 0; e < 2; ++e) {
-                            const int cc = q * 8 + 2 * j + e;
-                            float acc = sps[2 * FZ_BN + cc];
-#pragma unroll
-                            for (int k = 0; k < FZ_MAXZ / 2; ++k)
-                                if (k < zd) acc = fmaf(w0z[cc * zd + k], zr[k], acc);
-                            v2[e] = fmaxf(acc, 0.f);
-                        }
-                        const __nv_bfloat162 hv = __floats2bfloat162_rn(v2[0], v2[1]);
-                        pk[j] = *reinterpret_cast<const uint32_t*>(&hv);
+                        for (int k = 0; k < FZ_MAXZ / 2; ++k)
+                            if (k < zd) acc = fmaf(w0z[cc * zd + k], zr[k], acc);
+                        v2[e] = fmaxf(acc, 0.f);
                     }
-                    dst[q] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                    const __nv_bfloat162 hv = __floats2bfloat162_rn(v2[0], v2[1]);
+                    pk[j] = *reinterpret_cast<const uint32_t*>(&hv);
                 }
+                if (r < count)
+                    reinterpret_cast<uint4*>(a.act[0] + (size_t)r * N + n * FZ_BN)[q] =
+                        make_uint4(pk[0], pk[1], pk[2], pk[3]);
             }
             FZ_STAMP();
             fz_arrive(a.ready + m);
