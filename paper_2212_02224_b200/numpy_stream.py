@@ -93,12 +93,12 @@ def ziggurat_tables():
     return None
 
 
-def pcg64_state_words(bitgen) -> np.ndarray | None:
-    """[state lo, state hi, inc lo, inc hi] of a PCG64 bit generator with no buffered 32-bit
-    draw, else None."""
+def pcg64_state_words(bitgen, state: dict | None = None) -> np.ndarray | None:
+    """[state lo, state hi, inc lo, inc hi] of a PCG64 bit generator (its `state` dict may be
+    passed in when the caller already holds it), else None."""
     if type(bitgen) is not np.random.PCG64:
         return None
-    st = bitgen.state
+    st = bitgen.state if state is None else state
     s, inc = int(st["state"]["state"]), int(st["state"]["inc"])
     m = (1 << 64) - 1
     return np.array([s & m, s >> 64, inc & m, inc >> 64], dtype=np.uint64)
