@@ -123,9 +123,10 @@ constexpr int SORT_MIN_PAIRS = BD_SORT_MIN_PAIRS;   // >= 16 obstacles: sorted-w
 
 // Shared-memory carve-up, identical on host and device.
 struct AmSmem {
-    size_t w, obs, k, kb, a, curv, scr, dap, kap, kix, itm, hlp, total;
+    size_t w, obs, k, kb, a, curv, scr, dap, kap, kix, itm, hlp, red, total;
     // help > 0: the remainder warp's per-(sample, timestep) partial sums (am_helper), HSTR floats each
     static constexpr int HSTR = 28;
+    static constexpr int RSTR = 28;     // row stride of the column-reduction buffer (conflict-free STS.128)
     __host__ __device__ AmSmem(int m, int n_obs, int neq, int n_curv, int s_cta, int threads, int P, bool curv_on,
                                int max_iters, int help = 0) {
         const int J = (m + P - 1) / P;
@@ -144,6 +145,8 @@ struct AmSmem {
         // the CTA's per-iteration residual maxima (float bits), flushed to the global table once
         itm = o;  o = align_up(o + (size_t)max_iters * 4, 16);
         hlp = o;  o = align_up(o + (help > 0 ? (size_t)32 * HSTR * 4 : 0), 16);   // one slot per helper lane
+        // help > 0: each sample warp's 32 x 24 partial sums for the shared-memory column reduction
+        red = o;  o = align_up(o + (help > 0 ? (size_t)s_cta * 32 * RSTR * 4 : 0), 16);
         total = o;
     }
     // per-sample scratch: u (24 doubles) | c32 (24 floats) | lambda-state l (24 doubles) | first-step
@@ -180,39 +183,6 @@ __device__ __forceinline__ void group_reduce_scatter(float (&v)[NV], int lane) {
             v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
         }
     }
-}
-
-// The same reduce-scatter for one-warp groups with NREAL live values (the rest zero padding):
-// the sums go through packed FADD2 two slots at a time, and in the first stage a pair whose
-// upper slot is padding needs only the lower lanes' result (the upper lanes end up owning padding
-// values, which nothing reads), so it skips the two selects.  Sums identical to
-// group_reduce_scatter<32>.
-template <int NREAL>
-__device__ __forceinline__ void reduce_scatter32(float (&v)[32], int lane) {
-    static_assert(NREAL > 16 && NREAL <= 32 && NREAL % 2 == 0, "live values: 17-32, even");
-    constexpr unsigned FULL = 0xffffffffu;
-#pragma unroll
-    for (int o = 16; o >= 2; o >>= 1) {
-        const bool hi = (lane & o) != 0;
-#pragma unroll
-        for (int k = 0; k < o; k += 2) {
-            float2 keep, recv;
-            if (o == 16 && k + 16 >= NREAL) {
-                keep = make_float2(v[k], v[k + 1]);
-                recv = make_float2(__shfl_xor_sync(FULL, v[k], 16), __shfl_xor_sync(FULL, v[k + 1], 16));
-            } else {
-                keep = make_float2(hi ? v[k | o] : v[k], hi ? v[(k + 1) | o] : v[k + 1]);
-                const float s0 = hi ? v[k] : v[k | o], s1 = hi ? v[k + 1] : v[(k + 1) | o];
-                recv = make_float2(__shfl_xor_sync(FULL, s0, o), __shfl_xor_sync(FULL, s1, o));
-            }
-            const float2 r = fadd2(keep, recv);
-            v[k] = r.x;
-            v[k + 1] = r.y;
-        }
-    }
-    const bool hi = (lane & 1) != 0;
-    const float keep = hi ? v[1] : v[0], send = hi ? v[0] : v[1];
-    v[0] = keep + __shfl_xor_sync(FULL, send, 1);
 }
 
 // One sweep over this lane's timesteps at the current coefficients cxy[k] = (c_x[k], c_y[k]):
@@ -943,11 +913,30 @@ __device__ __forceinline__ void am_samples(const AmArgs& a, int scene, int blk, 
     float v[NV];
     float* xbuf = reinterpret_cast<float*>(smem + lay.scr + (size_t)slot * AmSmem::SCR_BYTES + 672);
     const float* hsm = reinterpret_cast<const float*>(smem + lay.hlp) + slot * HELP * AmSmem::HSTR + lane;
+    float* rbuf = reinterpret_cast<float*>(smem + lay.red) + (size_t)slot * 32 * AmSmem::RSTR;
     auto reduce = [&]() {
-        if constexpr (HELPED && NV == 32)
-            reduce_scatter32<NX + 2>(v, lane);
-        else
+        if constexpr (HELPED && NV == 32) {
+            // column sums through shared memory: every lane stores its 24 partials as a row, lane j
+            // adds column j over the 32 rows (independent loads, a 5-level add tree) -- a shorter
+            // dependency chain than the 5-stage shuffle reduce-scatter, which held ~20 % of the
+            // warps' stall samples (profiles/r02/am_kernel_lat32_help_v2)
+            float4* rw = reinterpret_cast<float4*>(rbuf + lane * AmSmem::RSTR);
+#pragma unroll
+            for (int q = 0; q < (NX + 2) / 4; ++q) rw[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            __syncwarp();
+            const int col = lane < NX + 2 ? lane : 0;
+            float t[32];
+#pragma unroll
+            for (int l = 0; l < 32; ++l) t[l] = rbuf[l * AmSmem::RSTR + col];
+#pragma unroll
+            for (int h = 16; h >= 1; h >>= 1)
+#pragma unroll
+                for (int l = 0; l < h; ++l) t[l] += t[l + h];
+            v[0] = t[0];
+            __syncwarp();
+        } else {
             group_reduce_scatter<RP>(v, lane);
+        }
         if (PAIR) {                                   // second warp -> first warp partial sums
             if ((threadIdx.x & 32) && lane < NX + 2) xbuf[lane] = v[0];
             pair_sync();
