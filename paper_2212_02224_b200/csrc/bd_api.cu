@@ -1955,6 +1955,21 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 }
 
 // 2-D bf16 row-major [rows x cols] tensor map with a box_rows x 64-col box and 128-byte swizzle.
+// [K block][row][64] view of a row-major rows x cols bf16 matrix (cols a multiple of 64): a box of
+// kg K blocks x box_rows rows lands as kg consecutive 128-byte-swizzled K-major tiles.
+bool make_map_bf16_kblocks(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
+                           uint32_t kg) {
+    auto enc = tensor_map_encoder();
+    if (!enc) return false;
+    const cuuint64_t dims[3] = {64, rows, cols / 64};
+    const cuuint64_t strides[2] = {cols * 2, 128};
+    const cuuint32_t box[3] = {64, box_rows, kg};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool make_map_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows = TC_BM) {
     auto enc = tensor_map_encoder();
     if (!enc) return false;
@@ -1979,7 +1994,7 @@ static int cvae_decode_dev(bd_ctx* ctx, int count, const float* dobs, const floa
     for (int l = 1; l < L - 1 && tc_ok; ++l) tc_ok = d[l] % TC_BK == 0 && d[l + 1] % TC_BN == 0;
     // the whole decoder as one persistent cooperative kernel (csrc/cvae_fused.cuh)
     bool fused_ok = tc_ok && ctx->cvae_fused && L - 2 <= FZ_MAXH && d[L] <= FZ_MAXOUT && zdim <= FZ_MAXZ / 2;
-    for (int l = 1; l < L && fused_ok; ++l) fused_ok = d[l] % FZ_BN == 0 && d[l] % FZ_BK == 0;
+    for (int l = 1; l < L && fused_ok; ++l) fused_ok = d[l] % FZ_BN == 0 && d[l] % (FZ_BK * FZ_KG) == 0;
     if (fused_ok) {
         int sms = 148, coop = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
@@ -2026,9 +2041,10 @@ static int cvae_decode_dev(bd_ctx* ctx, int count, const float* dobs, const floa
                 ctx->fz_count = -1;
                 for (int h = 0; h < nh; ++h) {
                     const int l = h + 1;
-                    if (!make_map_bf16(&ctx->fz_maps.a[h], fa.act[l - 1], (uint64_t)count, (uint64_t)d[l], FZ_BM) ||
-                        !make_map_bf16(&ctx->fz_maps.b[h], ctx->cvae_w16[l]->p, (uint64_t)d[l + 1], (uint64_t)d[l],
-                                       FZ_BN))
+                    if (!make_map_bf16_kblocks(&ctx->fz_maps.a[h], fa.act[l - 1], (uint64_t)count, (uint64_t)d[l],
+                                               FZ_BM, FZ_KG) ||
+                        !make_map_bf16_kblocks(&ctx->fz_maps.b[h], ctx->cvae_w16[l]->p, (uint64_t)d[l + 1],
+                                               (uint64_t)d[l], FZ_BN, FZ_KG))
                         return fail(ctx, BD_ERR_CUDA, "cuTensorMapEncodeTiled failed");
                 }
                 ctx->fz_count = count;

@@ -25,11 +25,20 @@
 
 namespace bd {
 
-constexpr int FZ_BM = 128, FZ_BN = 64, FZ_BK = 64, FZ_STAGES = 6;
+// A ring stage holds FZ_KG 64-wide K blocks, each operand loaded by ONE 3-D tensor copy
+// ([K block][row][64]): the per-SM ingest of bulk copies grows with the bytes per copy (8 / 16 /
+// 24 / >= 32 KB: 32 / 62 / 91 / ~120 GB/s, tools/probes/l2_ingest.cu), and the tiles are
+// ingest-bound.  Kernel time at 1000 samples (ncu, warm L2): FZ_KG 1 (6 stages of 24 KB) 50.5 us,
+// 2 (4 x 48 KB) 46.1 us, 4 (2 x 96 KB) 44.8 us
+#ifndef FZ_KG_DEF
+#define FZ_KG_DEF 4
+#endif
+constexpr int FZ_KG = FZ_KG_DEF;
+constexpr int FZ_BM = 128, FZ_BN = 64, FZ_BK = 64, FZ_STAGES = FZ_KG == 1 ? 6 : (FZ_KG == 2 ? 4 : 2);
 constexpr int FZ_MAXH = 6;                            // hidden tensor-core layers supported
 constexpr int FZ_MAXOUT = 16;                         // last-layer outputs
-constexpr int FZ_A_BYTES = FZ_BM * FZ_BK * 2;         // 16 KB
-constexpr int FZ_B_BYTES = FZ_BN * FZ_BK * 2;         // 8 KB
+constexpr int FZ_A_BYTES = FZ_KG * FZ_BM * FZ_BK * 2;         // 16 KB per K block
+constexpr int FZ_B_BYTES = FZ_KG * FZ_BN * FZ_BK * 2;         // 8 KB per K block
 constexpr int FZ_MAXZ = 16;                           // latent dimension
 constexpr int FZ_SMEM = FZ_STAGES * (FZ_A_BYTES + FZ_B_BYTES) + 1024 /*align*/ + 256 /*barriers*/ +
                         FZ_MAXOUT * FZ_BN * 4 /*last-layer weight slice*/ + FZ_BM * FZ_MAXZ * 4 /*latent rows*/ +
@@ -63,10 +72,12 @@ __device__ __forceinline__ void fence_proxy_async_global() {
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-__device__ __forceinline__ void tma_load_2d_fz(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+// 3-D box [FZ_KG K blocks][rows][64] at (K block kb, row y): FZ_KG consecutive 128-byte-swizzled
+// K-major tiles in shared memory, the layout FZ_KG 2-D copies would produce
+__device__ __forceinline__ void tma_load_3d_fz(void* dst, const CUtensorMap* map, int y, int kb, uint64_t* bar) {
     asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-        ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+        ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(y), "r"(kb), "r"(smem_u32(bar))
         : "memory");
 }
 
@@ -236,7 +247,7 @@ __global__ void __launch_bounds__(128, 1) cvae_fused_kernel(const __grid_constan
     uint32_t gk = 0, tiles = 0;                  // ring position / done-barrier parity, across tiles
     for (int h = 0; h < a.nh; ++h) {
         const int l = h + 1;                      // Linear layer index
-        const int K = a.dims[l], N = a.dims[l + 1], nb = N / FZ_BN, kblocks = K / FZ_BK;
+        const int K = a.dims[l], N = a.dims[l + 1], nb = N / FZ_BN, kblocks = K / (FZ_BK * FZ_KG);
         const int nb_prev = a.dims[l] / FZ_BN;
         const bool last_hidden = (h == a.nh - 1);
         for (int t = blockIdx.x; t < mblocks * nb; t += gridDim.x) {
@@ -252,24 +263,27 @@ __global__ void __launch_bounds__(128, 1) cvae_fused_kernel(const __grid_constan
                     const uint32_t g = gk + kb, s = g % FZ_STAGES;
                     if (g >= FZ_STAGES) mbar_wait_fz(empty + s, ((g / FZ_STAGES) + 1) & 1);
                     mbar_expect_tx(full + s, FZ_A_BYTES + FZ_B_BYTES);
-                    tma_load_2d_fz(tiles_a + s * FZ_A_BYTES, &maps.a[h], kb * FZ_BK, m * FZ_BM, full + s);
-                    tma_load_2d_fz(tiles_b + s * FZ_B_BYTES, &maps.b[h], kb * FZ_BK, n * FZ_BN, full + s);
+                    tma_load_3d_fz(tiles_a + s * FZ_A_BYTES, &maps.a[h], m * FZ_BM, kb * FZ_KG, full + s);
+                    tma_load_3d_fz(tiles_b + s * FZ_B_BYTES, &maps.b[h], n * FZ_BN, kb * FZ_KG, full + s);
                 }
             } else if (warp == 1 && lane == 0) {
-                // ---- MMA issuer: 4 x (128 x 64 x 16) per 64-wide K block
+                // ---- MMA issuer: 4 x (128 x 64 x 16) per 64-wide K block, FZ_KG blocks per stage
                 for (int kb = 0; kb < kblocks; ++kb) {
                     const uint32_t g = gk + kb, s = g % FZ_STAGES;
                     mbar_wait_fz(full + s, (g / FZ_STAGES) & 1);
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                    const uint64_t da = umma_desc_sw128(smem_u32(tiles_a + s * FZ_A_BYTES));
-                    const uint64_t db = umma_desc_sw128(smem_u32(tiles_b + s * FZ_B_BYTES));
 #pragma unroll
-                    for (int k = 0; k < FZ_BK / 16; ++k) {
+                    for (int k = 0; k < FZ_KG * FZ_BK / 16; ++k) {
+                        const int u = k / (FZ_BK / 16), kk = k % (FZ_BK / 16);   // K block of the stage, step in it
+                        const uint64_t da =
+                            umma_desc_sw128(smem_u32(tiles_a + s * FZ_A_BYTES + u * (FZ_A_BYTES / FZ_KG)));
+                        const uint64_t db =
+                            umma_desc_sw128(smem_u32(tiles_b + s * FZ_B_BYTES + u * (FZ_B_BYTES / FZ_KG)));
                         const uint32_t acc = (kb | k) != 0;
                         asm volatile(
                             "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
                             "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
-                            "l"(da + (uint64_t)(k * 2)), "l"(db + (uint64_t)(k * 2)), "r"(FZ_IDESC), "r"(acc));
+                            "l"(da + (uint64_t)(kk * 2)), "l"(db + (uint64_t)(kk * 2)), "r"(FZ_IDESC), "r"(acc));
                     }
                     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                                      smem_u32(empty + s))
