@@ -211,6 +211,39 @@ __global__ void __launch_bounds__(128, 1) cvae_fused_kernel(const __grid_constan
             // eight threads per row, each one 16-byte chunk (8 outputs) of the row's 128-byte
             // segment: a warp stores four whole segments per instruction (coalesced)
             const int q = threadIdx.x & 7;
+            if (zd <= 2) {
+                // the paper's latent size: this thread's 8 outputs' observation sums and latent
+                // weights stay in registers across its rows (same arithmetic order as below)
+                float bo[8], wa[8], wb[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const int cc = q * 8 + e;
+                    bo[e] = sps[2 * FZ_BN + cc];
+                    wa[e] = w0z[cc * zd];
+                    wb[e] = zd > 1 ? w0z[cc * zd + 1] : 0.f;
+                }
+#pragma unroll 4
+                for (int rl = threadIdx.x >> 3; rl < FZ_BM; rl += 128 / 8) {
+                    const int r = m * FZ_BM + rl;
+                    const float z0 = zs[rl * zd], z1 = zd > 1 ? zs[rl * zd + 1] : 0.f;
+                    uint32_t pk[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        float v2[2];
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            float acc = fmaf(wa[2 * j + e], z0, bo[2 * j + e]);
+                            if (zd > 1) acc = fmaf(wb[2 * j + e], z1, acc);
+                            v2[e] = fmaxf(acc, 0.f);
+                        }
+                        const __nv_bfloat162 hv = __floats2bfloat162_rn(v2[0], v2[1]);
+                        pk[j] = *reinterpret_cast<const uint32_t*>(&hv);
+                    }
+                    if (r < count)
+                        reinterpret_cast<uint4*>(a.act[0] + (size_t)r * N + n * FZ_BN)[q] =
+                            make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                }
+            } else
 #pragma unroll 2
             for (int rl = threadIdx.x >> 3; rl < FZ_BM; rl += 128 / 8) {
                 const int r = m * FZ_BM + rl;
