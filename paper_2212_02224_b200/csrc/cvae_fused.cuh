@@ -371,11 +371,26 @@ __global__ void __launch_bounds__(128, 1) cvae_fused_kernel(const __grid_constan
                             }
                     }
                 }
-                if (!last_hidden && row < count) {
-                    uint4* dst = reinterpret_cast<uint4*>(a.act[l] + (size_t)row * N + n * FZ_BN + c0);
+                if (!last_hidden) {
+                    // stage the row's 16-byte chunks in the (idle) ring, XOR-swizzled by row, so the
+                    // warp can store whole 128-byte row segments below
+                    uint4* st = reinterpret_cast<uint4*>(tiles_a) + (size_t)(warp * 32 + lane) * 8;
 #pragma unroll
                     for (int q = 0; q < 4; ++q)
-                        dst[q] = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+                        st[((c0 >> 3) + q) ^ (lane & 7)] =
+                            make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+                }
+            }
+            if (!last_hidden) {
+                // the warp's 32 rows x 128 bytes: lane l stores chunk l % 8 of row 4 i + l / 8
+                __syncwarp();
+                const uint4* st = reinterpret_cast<const uint4*>(tiles_a) + (size_t)warp * 32 * 8;
+                const int ch = lane & 7;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int rr = 4 * i + (lane >> 3), grow = m * FZ_BM + warp * 32 + rr;
+                    if (grow < count)
+                        reinterpret_cast<uint4*>(a.act[l] + (size_t)grow * N + n * FZ_BN)[ch] = st[rr * 8 + (ch ^ (rr & 7))];
                 }
             }
             if (last_hidden && row < count)
