@@ -401,11 +401,19 @@ __global__ void __launch_bounds__(128, 1) cvae_fused_kernel(const __grid_constan
             const unsigned prev = fz_arrive(a.ready + (size_t)l * mblocks + m);
             if (last_hidden && prev == a.epoch * (unsigned)nb - 1 && row < count) {
                 // this tile completed the row block: sum the nb partials in column-block order + bias
-                for (int o = 0; o < nout; ++o) {
-                    float s = 0.f;
-                    for (int q = 0; q < nb; ++q) s += __ldcg(a.partial + ((size_t)q * count + row) * nout + o);
-                    a.out[(size_t)row * nout + o] = (double)(s + a.bias[a.nh + 1][o]);
+                // (loads of all outputs first: one L2 round trip per column block, not per output)
+                float acc[FZ_MAXOUT];
+#pragma unroll
+                for (int o = 0; o < FZ_MAXOUT; ++o) acc[o] = 0.f;
+                for (int q = 0; q < nb; ++q) {
+                    const float* pp = a.partial + ((size_t)q * count + row) * nout;
+                    float pv[FZ_MAXOUT];
+#pragma unroll
+                    for (int o = 0; o < FZ_MAXOUT; ++o) pv[o] = o < nout ? __ldcg(pp + o) : 0.f;
+#pragma unroll
+                    for (int o = 0; o < FZ_MAXOUT; ++o) acc[o] += pv[o];
                 }
+                for (int o = 0; o < nout; ++o) a.out[(size_t)row * nout + o] = (double)(acc[o] + a.bias[a.nh + 1][o]);
             }
         }
     }
