@@ -113,14 +113,15 @@ __device__ __forceinline__ void fz_wait(const unsigned* ctr, unsigned need) {
 
 // Publish this CTA's tile: every thread fences its generic stores to the async proxy, then one
 // release increment.  Returns the counter value before the increment (all threads).
-__device__ __forceinline__ unsigned fz_arrive(unsigned* ctr) {
+// acquire: the caller reads other CTAs' data if it was the last to arrive (fence after the add).
+__device__ __forceinline__ unsigned fz_arrive(unsigned* ctr, bool acquire = true) {
     __shared__ unsigned s_old;
     fence_proxy_async_global();
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
         s_old = atomicAdd(ctr, 1u);
-        __threadfence();
+        if (acquire) __threadfence();
     }
     __syncthreads();
     return s_old;
@@ -271,7 +272,7 @@ __global__ void __launch_bounds__(128, 1) cvae_fused_kernel(const __grid_constan
                         make_uint4(pk[0], pk[1], pk[2], pk[3]);
             }
             FZ_STAMP();
-            fz_arrive(a.ready + m);
+            fz_arrive(a.ready + m, false);
         }
     }
     FZ_STAMP();
@@ -398,7 +399,7 @@ __global__ void __launch_bounds__(128, 1) cvae_fused_kernel(const __grid_constan
                 for (int o = 0; o < FZ_MAXOUT; ++o)
                     if (o < nout) a.partial[((size_t)n * count + row) * nout + o] = pout[o];
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            const unsigned prev = fz_arrive(a.ready + (size_t)l * mblocks + m);
+            const unsigned prev = fz_arrive(a.ready + (size_t)l * mblocks + m, last_hidden);
             if (last_hidden && prev == a.epoch * (unsigned)nb - 1 && row < count) {
                 // this tile completed the row block: sum the nb partials in column-block order + bias
                 // (loads of all outputs first: one L2 round trip per column block, not per output)
