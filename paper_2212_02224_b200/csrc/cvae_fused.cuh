@@ -101,11 +101,14 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
     return v;
 }
 
+#ifndef FZ_POLL_NS
+#define FZ_POLL_NS 16   // A/B (ncu warm, median): 64 ns 40.0 us, 16 ns 39.7 us, 0 ns 39.7 us
+#endif
 // Block until `need` tiles of a row block arrived (thread 0 polls; bounded, then gives up).
 __device__ __forceinline__ void fz_wait(const unsigned* ctr, unsigned need) {
     if (threadIdx.x == 0) {
         long long spins = 0;
-        while (ld_acquire_u32(ctr) < need && ++spins < (1ll << 27)) __nanosleep(64);
+        while (ld_acquire_u32(ctr) < need && ++spins < (1ll << 27)) __nanosleep(FZ_POLL_NS);
         fence_proxy_async_global();
     }
     __syncthreads();
