@@ -154,3 +154,26 @@ def test_persistent_teacher_forced_config2_against_reference():
         assert ok, f"iteration {it}: constraint-elite swaps outside the tie band: {diff}"
         assert res.best.index == int(g["elite_idx"][it][0]), "best index"
     assert _persistent_count(solver.context) - n0 == int(N), "the persistent kernel did not run"
+
+
+@pytest.mark.parametrize("persist", [1, 0])
+def test_remainder_warp_matches_plain_latency_instance(persist):
+    """B = 1000 (7 samples per SM): the latency instance with the remainder warp (timesteps 96-99 of
+    every sample on an eighth warp, named-barrier handshake, shared-memory column sums) against the
+    plain one-warp instance (option remainder_warp = 0), in the persistent kernel and in the launch
+    chain: the same best sample and set-points, coefficients and statistics within fp32 rounding of
+    the two summation orders."""
+    import paper_2212_02224_b200 as bd
+    from paper_2212_02224_b200.fleet import FleetPlanner
+    from paper_2212_02224_b200.scenes import highway_scene
+    basis = bd.build_basis(10, 100, 5.0, "bernstein")
+    cfg = bd.BiLevelConfig(1000, 150, 100, 4, 0.7, 0.9, 1.0)
+    fp = FleetPlanner(basis, bd.TrackingWeights(), bd.ParamLayout(4), bd.ProjectionConfig(1.0, 100, 1e-3), 10, cfg)
+    fp.context.set_option("persistent_cycle", persist)
+    sc = [highway_scene(7)]
+    a = fp.plan(sc, seed=11)
+    fp.context.set_option("remainder_warp", 0)
+    b = fp.plan(sc, seed=11)
+    fp.context.set_option("remainder_warp", 1)
+    _close(a, b)
+    np.testing.assert_array_equal(a.iterations_done, b.iterations_done)
