@@ -14,6 +14,7 @@ set +e
 BD_LIB_PATH=$lib python -m pytest -s -m gpu -q -p no:cacheprovider \
   tests/test_gpu_parity.py tests/test_gpu_cem.py tests/test_gpu_fleet.py tests/test_gpu_shapes.py \
   tests/test_gpu_random_parity.py tests/test_gpu_worlds.py tests/test_gpu_sim.py tests/test_gpu_cvae.py \
+  tests/test_gpu_persistent.py tests/test_gpu_numpy_stream.py tests/test_gpu_spec_bilevel.py \
   > "$out/pytest_checks.log" 2>&1
 rc=$?
 fired=$(grep -c "BD_CHECK failed" "$out/pytest_checks.log")
