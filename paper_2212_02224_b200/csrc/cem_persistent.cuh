@@ -2,7 +2,7 @@
 //
 // Replaces the per-iteration launch chain of bd_cem_cycle -- sample + stage 1, AM pass, replay
 // guard, rank count, rank + refit -- for solve_bilevel's loop (pkg/bilevel.py:249-292) when the
-// batch fills every SM with one CTA of 7-8 one-warp samples (B ~ 900-1200).  All CTAs are
+// batch fills every SM with one CTA of 5-8 one-warp samples (B ~ 600-1200).  All CTAs are
 // co-resident (cooperative launch), so the batch-global steps are grid barriers instead of kernel
 // boundaries, and the serial work of each barrier is done by a dedicated control CTA:
 //
