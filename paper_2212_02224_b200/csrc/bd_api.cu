@@ -496,7 +496,7 @@ int dispatch_am(bd_ctx* ctx, AmArgs a, int P, int threads, bool replay_pass, int
             default: return fail(ctx, BD_ERR_VALUE, "unsupported CTA size %d", threads);
         }
     }
-    // single-scene latency shape, one-warp samples: one CTA of 7-8 samples + the remainder warp per
+    // single-scene latency shape, one-warp samples: one CTA of 5-7 samples + the remainder warp per
     // SM (timesteps 96-99 of every sample, am_helper), <= 255 registers
     if (P == 32 && !curv && a.m == 100 && a.n_obs == 10 && lat_helped(ctx, (long long)a.B * ctx->S)) {
         switch (threads) {
@@ -554,8 +554,9 @@ int pick_lanes(bd_ctx* ctx, const AmArgs& a) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
     // BASELINE latency shape with 7-8 samples per SM: one-warp samples in the 255-register
-    // phase-split instance (A/B on B200, ms per AM launch, one-warp vs two-warp: B = 1000 0.230 vs
-    // 0.242, B = 1100 0.234 vs 0.246; at 5-6 per SM the two-warp mapping wins: B = 700 0.222 vs 0.196)
+    // instance (round-1 A/B on B200, ms per AM launch, one-warp vs two-warp: B = 1000 0.230 vs
+    // 0.242, B = 1100 0.234 vs 0.246; at 5-6 per SM the two-warp mapping won, B = 700 0.222 vs
+    // 0.196, until the remainder warp)
     if (!ctx->opt_lat_off && a.n_curv == 0 && a.m == 100 && a.n_obs == 10) {
         const long long per_sm = ((long long)total + sms - 1) / sms;
         if (per_sm >= 7 && per_sm <= 8) return 32;
