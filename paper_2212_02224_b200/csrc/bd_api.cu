@@ -561,8 +561,10 @@ int pick_lanes(bd_ctx* ctx, const AmArgs& a) {
         const long long per_sm = ((long long)total + sms - 1) / sms;
         if (per_sm >= 7 && per_sm <= 8) return 32;
         // with the remainder warp the one-warp instance also beats the two-warp one at 5-6 per SM
-        // (ms per AM launch: B = 740 0.167 vs 0.184, B = 888 0.174 vs 0.188; without it 0.202 / 0.208)
-        if (per_sm >= 5 && lat_helped(ctx, (long long)total)) return 32;
+        // (ms per AM launch: B = 740 0.167 vs 0.184, B = 888 0.174 vs 0.188; without it 0.202 / 0.208);
+        // single-scene cycles only, so a fleet keeps the lane mapping its scenes get when planned
+        // one at a time at these sizes (tests/test_gpu_fleet.py: results independent of batching)
+        if (per_sm >= 5 && ctx->S == 1 && lat_helped(ctx, (long long)total)) return 32;
     }
     const int cands[4] = {8, 16, 32, 64};
     const double overhead[4] = {0.5, 0.7, 0.9, 1.0};
