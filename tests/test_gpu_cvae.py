@@ -181,3 +181,30 @@ def test_device_warm_start_stale_or_short_rows_use_the_host_copy():
     _same_result(c, d)
     with pytest.raises(ValueError):
         dec.warm_start(obs, 10, bd.ParamLayout(3), np.random.default_rng(0))
+
+
+def test_device_warm_start_abi_copy_and_trace_path():
+    """bd_cvae_warm_start with a host `params` buffer copies the same rows the device keeps; the
+    stepped solve_bilevel (trace_hook) draws a DeviceWarmStart through its host view and matches
+    the reference-typed WarmStartSource."""
+    import ctypes
+    from paper_2212_02224_b200.behavior import WarmStartSource
+    bd, solver, scene, mean, cov, dec = _c3_setup(5)
+    obs = np.linspace(0.0, 2.0, 55).astype(np.float32)
+    z = np.random.default_rng(3).standard_normal((300, 2)).astype(np.float32)
+    shift = np.ascontiguousarray(mean, dtype=np.float64)
+    host = np.empty((300, 8))
+    rows = ctypes.c_void_p()
+    dec.ctx.call("bd_cvae_warm_start", 300, obs.ctypes.data, z.ctypes.data, None, shift.ctypes.data, host,
+                 ctypes.addressof(rows))
+    assert rows.value
+    np.testing.assert_array_equal(host, dec.decode(obs, z) + shift)
+    ws = dec.warm_start(obs, 1000, solver.layout, np.random.default_rng(8), shift=shift)
+    cfg = bd.BiLevelConfig(1000, 150, 100, 2, 0.7, 0.9, 1.0, mean, cov)
+    seen = []
+    a = bd.solve_bilevel(scene, solver, cfg, np.random.default_rng(2), warm_start=ws,
+                         trace_hook=lambda *args: seen.append(1))
+    b = bd.solve_bilevel(scene, solver, cfg, np.random.default_rng(2),
+                         warm_start=WarmStartSource(ws.samples, solver.layout), trace_hook=lambda *args: None)
+    assert seen
+    _same_result(a, b)
