@@ -23,7 +23,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import numpy_stream
-from ._native import CemConfig, f64, ptr, upload_scenes
+from ._native import CemConfig, f64, ptr
 from .basis import PolynomialBasis, TrajectoryCoeffs, eval_trajectory
 from .batch_qp import NumericalFailure, QPSolutionBatch, TrackingWeights, build_qp_structure
 from .behavior import BehaviorParams, DeviceWarmStart, ParamLayout, WarmStartSource
