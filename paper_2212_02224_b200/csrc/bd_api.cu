@@ -65,6 +65,12 @@ struct bd_ctx {
     int device = 0;
     cudaStream_t own = nullptr;
     cudaStream_t stream = nullptr;
+    // side stream of the device numpy stream: its kernel depends only on the host's generator
+    // state, so it runs beside whatever the main stream still has in flight (e.g. the CVAE decode
+    // of a config-3 warm start); nn_free orders it after the previous cycle's use of its buffers
+    cudaStream_t side = nullptr;
+    cudaEvent_t nn_ready = nullptr, nn_free = nullptr;
+    bool nn_free_valid = false;
     std::string err;
     int64_t launches = 0;
     int64_t persistent_cycles = 0;   // bd_cem_cycle calls run as the persistent kernel
@@ -729,6 +735,9 @@ void bd_destroy(bd_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     if (ctx->own) cudaStreamDestroy(ctx->own);
+    if (ctx->side) cudaStreamDestroy(ctx->side);
+    if (ctx->nn_ready) cudaEventDestroy(ctx->nn_ready);
+    if (ctx->nn_free) cudaEventDestroy(ctx->nn_free);
     delete ctx;
 }
 
@@ -1667,10 +1676,20 @@ int bd_cem_cycle(bd_ctx* ctx, int S, const bd_cem_config* cfg, const double* ini
         CU(ctx->nn_z.ensure((size_t)(it1 - it0) * tot * dim * 8));
         CU(ctx->nn_pos.ensure((size_t)(nblk + 1) * 8));
         if (nblk > 0) {
-            if ((rc = launch_numpy_normals(ctx, cfg->pcg64_state, (long long)nblk * tot * dim, (long long)tot * dim,
-                                           ctx->nn_z.as<double>() + (size_t)first * tot * dim,
-                                           ctx->nn_pos.as<long long>())))
-                return rc;
+            if (!ctx->side) {
+                CU(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+                CU(cudaEventCreateWithFlags(&ctx->nn_ready, cudaEventDisableTiming));
+                CU(cudaEventCreateWithFlags(&ctx->nn_free, cudaEventDisableTiming));
+            }
+            if (ctx->nn_free_valid) CU(cudaStreamWaitEvent(ctx->side, ctx->nn_free, 0));
+            cudaStream_t main_stream = ctx->stream;
+            ctx->stream = ctx->side;
+            rc = launch_numpy_normals(ctx, cfg->pcg64_state, (long long)nblk * tot * dim, (long long)tot * dim,
+                                      ctx->nn_z.as<double>() + (size_t)first * tot * dim, ctx->nn_pos.as<long long>());
+            ctx->stream = main_stream;
+            if (rc) return rc;
+            CU(cudaEventRecord(ctx->nn_ready, ctx->side));
+            CU(cudaStreamWaitEvent(ctx->stream, ctx->nn_ready, 0));
         } else {
             CU(cudaMemsetAsync(ctx->nn_pos.p, 0, 8, ctx->stream));
         }
@@ -1782,6 +1801,10 @@ int bd_cem_cycle(bd_ctx* ctx, int S, const bd_cem_config* cfg, const double* ini
                 ctx->host_out = true;
             }
         }
+    if (ctx->side) {                    // the numpy-stream buffers are free once this call's work is
+        CU(cudaEventRecord(ctx->nn_free, ctx->stream));
+        ctx->nn_free_valid = true;
+    }
     return finish_call(ctx, false, 0);
 }
 
