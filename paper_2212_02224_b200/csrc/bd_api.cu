@@ -1669,6 +1669,7 @@ int bd_cem_cycle(bd_ctx* ctx, int S, const bd_cem_config* cfg, const double* ini
     if ((rc = stage_in(ctx, init_cov, (size_t)S * dim * dim, &dc0))) return rc;
     if ((rc = stage_in(ctx, z, z ? (size_t)(it1 - it0) * tot * dim : 0, &dz))) return rc;
     if ((rc = stage_in(ctx, warm, warm ? tot * dim : 0, &dwarm))) return rc;
+    bool join_nn = false;
     if (!z && cfg->pcg64_state) {
         // numpy stream mode: the caller's Generator(PCG64) normals of every drawing iteration of the
         // range, generated on the device (the first iteration of a warm-started cycle draws none)
@@ -1688,21 +1689,21 @@ int bd_cem_cycle(bd_ctx* ctx, int S, const bd_cem_config* cfg, const double* ini
                                       ctx->nn_z.as<double>() + (size_t)first * tot * dim, ctx->nn_pos.as<long long>());
             ctx->stream = main_stream;
             if (rc) return rc;
-            CU(cudaEventRecord(ctx->nn_ready, ctx->side));
-            CU(cudaStreamWaitEvent(ctx->stream, ctx->nn_ready, 0));
+            join_nn = true;                // the main stream joins after cem_init (below)
         } else {
             CU(cudaMemsetAsync(ctx->nn_pos.p, 0, 8, ctx->stream));
         }
         dz = ctx->nn_z.as<double>();
         if (cfg->pcg64_positions) {
-            if (is_device_ptr(cfg->pcg64_positions)) {
+            if (is_device_ptr(cfg->pcg64_positions)) {   // after the normals kernel on its stream
                 CU(cudaMemcpyAsync(cfg->pcg64_positions, ctx->nn_pos.p, (size_t)(nblk + 1) * 8, cudaMemcpyDeviceToDevice,
-                                   ctx->stream));
+                                   join_nn ? ctx->side : ctx->stream));
             } else {
                 ctx->pending.push_back({cfg->pcg64_positions, ctx->nn_pos.p, (size_t)(nblk + 1) * 8});
                 ctx->host_out = true;
             }
         }
+        if (join_nn) CU(cudaEventRecord(ctx->nn_ready, ctx->side));
     }
     CU(ctx->c_mean.ensure((size_t)S * dim * 8));
     CU(ctx->c_cov.ensure((size_t)S * dim * dim * 8));
@@ -1738,6 +1739,7 @@ int bd_cem_cycle(bd_ctx* ctx, int S, const bd_cem_config* cfg, const double* ini
         cem_init_kernel<<<S, 64, 0, ctx->stream>>>(s, dm0, dc0);
         ctx->launches++;
     }
+    if (join_nn) CU(cudaStreamWaitEvent(ctx->stream, ctx->nn_ready, 0));   // the normals are ready
     CU(ctx->w_order.ensure(tot * 4));
     const size_t rsmem = rank_refit_smem(cfg->n_cons, cfg->n_elite, dim);
     raise_smem(rank_refit_kernel, rsmem);
