@@ -461,9 +461,9 @@ int launch_am_t(bd_ctx* ctx, AmArgs a, int threads, bool replay_pass, int* occ =
     return 0;
 }
 
-// The one-warp latency instance runs with a remainder warp at 5-7 samples per SM unless the option
-// turns it off (8 samples + the remainder warp = 3 warps on one SM sub-partition: <= 168 registers,
-// which spills).
+// The one-warp latency instance runs with a remainder warp at 5-8 samples per SM unless the option
+// turns it off (8 samples + the remainder warp put 3 warps on one SM sub-partition: <= 168
+// registers, still faster: 0.200 against 0.217 ms per AM launch at B = 1100).
 static int samples_per_sm(const bd_ctx* ctx, long long samples) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
@@ -471,7 +471,7 @@ static int samples_per_sm(const bd_ctx* ctx, long long samples) {
 }
 static bool lat_helped(const bd_ctx* ctx, long long samples) {
     const int per_sm = samples_per_sm(ctx, samples);
-    return !ctx->opt_help_off && !ctx->opt_spc && per_sm >= 5 && per_sm <= 7;
+    return !ctx->opt_help_off && !ctx->opt_spc && per_sm >= 5 && per_sm <= 8;
 }
 
 int dispatch_am(bd_ctx* ctx, AmArgs a, int P, int threads, bool replay_pass, int* occ) {
@@ -502,13 +502,14 @@ int dispatch_am(bd_ctx* ctx, AmArgs a, int P, int threads, bool replay_pass, int
             default: return fail(ctx, BD_ERR_VALUE, "unsupported CTA size %d", threads);
         }
     }
-    // single-scene latency shape, one-warp samples: one CTA of 5-7 samples + the remainder warp per
-    // SM (timesteps 96-99 of every sample, am_helper), <= 255 registers
+    // single-scene latency shape, one-warp samples: one CTA of 5-8 samples + the remainder warp per
+    // SM (timesteps 96-99 of every sample, am_helper), <= 255 registers (<= 168 at 8 + 1 warps)
     if (P == 32 && !curv && a.m == 100 && a.n_obs == 10 && lat_helped(ctx, (long long)a.B * ctx->S)) {
         switch (threads) {
             case 192: return launch_am_t<32, false, 100, 5, 192, true, 4>(ctx, a, threads, replay_pass, occ);
             case 224: return launch_am_t<32, false, 100, 5, 224, true, 4>(ctx, a, threads, replay_pass, occ);
             case 256: return launch_am_t<32, false, 100, 5, 256, true, 4>(ctx, a, threads, replay_pass, occ);
+            case 288: return launch_am_t<32, false, 100, 5, 288, true, 4>(ctx, a, threads, replay_pass, occ);
             default: return fail(ctx, BD_ERR_VALUE, "unsupported CTA size %d", threads);
         }
     }
@@ -594,7 +595,7 @@ int launch_am(bd_ctx* ctx, AmArgs a, bool replay_pass) {
     const int P = pick_lanes(ctx, a);
     const int threads = default_threads(ctx, P, a);
     // > 256 threads only for the latency-shape instances (dispatch_am: P = 64, m = 100, 10 obstacles)
-    const bool big_ok = P == 64 && a.n_curv == 0 && a.m == 100 && a.n_obs == 10;
+    const bool big_ok = (P == 64 || (P == 32 && threads == 288)) && a.n_curv == 0 && a.m == 100 && a.n_obs == 10;
     if (threads % 32 || threads > 512 || threads < 32 || (threads > 256 && !big_ok))
         return fail(ctx, BD_ERR_VALUE, "bad samples_per_cta (more than 256 threads only for the 10-obstacle "
                     "m=100 two-warp mapping)");
@@ -1605,7 +1606,8 @@ static int try_cem_persistent(bd_ctx* ctx, const bd_cem_config* cfg, const CemSt
     };
     if (help)
         e = spc == 5 ? launch(cem_persistent_kernel<192, 4>)
-                     : (spc == 6 ? launch(cem_persistent_kernel<224, 4>) : launch(cem_persistent_kernel<256, 4>));
+                     : spc == 6 ? launch(cem_persistent_kernel<224, 4>)
+                                : spc == 7 ? launch(cem_persistent_kernel<256, 4>) : launch(cem_persistent_kernel<288, 4>);
     else
         e = spc == 7 ? launch(cem_persistent_kernel<224, 0>) : launch(cem_persistent_kernel<256, 0>);
     if (e == cudaErrorCooperativeLaunchTooLarge) {   // not co-resident on this device: launch chain instead

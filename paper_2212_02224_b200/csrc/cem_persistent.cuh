@@ -7,7 +7,7 @@
 // boundaries, and the serial work of each barrier is done by a dedicated control CTA:
 //
 //   per CEM iteration (worker CTAs: one CTA of 5-8 one-warp samples per SM, + the remainder warp at
-//   5-7; one control CTA)
+//   5-8; one control CTA)
 //     S   every warp: draw its set-point (p = mu + z L^T, pkg/bilevel.py:51-57) and solve its
 //         stage-1 QP (pkg/batch_qp.py:209-280), constants staged in shared memory once per launch
 //     A   every warp: the AM projection of its sample (am_samples, the latency instance of K2)
