@@ -80,7 +80,7 @@ int bd_synchronize(bd_ctx* ctx);
 /* Knobs: "lanes_per_sample" (0=auto, 4/8/16/32/64), "samples_per_cta" (0=auto), "timing" (0/1),
  * "latency_instance" (1=auto / 0=never pick the up-to-255-register one-warp AM instance for 5-8
  * samples per SM), "remainder_warp" (1=auto / 0=never add the remainder warp to that instance at
- * 4-8 samples per SM), "persistent_cycle" (1=auto / 0=never run a single-scene bd_cem_cycle as
+ * 3-8 samples per SM), "persistent_cycle" (1=auto / 0=never run a single-scene bd_cem_cycle as
  * the persistent cooperative kernel), "cvae_tensor_cores" (1/0), "cvae_fused" (1/0: the decoder
  * as one cooperative kernel), "sticky_errors" (1/0). */
 int bd_set_option(bd_ctx* ctx, const char* key, int value);

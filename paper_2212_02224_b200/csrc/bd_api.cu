@@ -461,7 +461,7 @@ int launch_am_t(bd_ctx* ctx, AmArgs a, int threads, bool replay_pass, int* occ =
     return 0;
 }
 
-// The one-warp latency instance runs with a remainder warp at 4-8 samples per SM unless the option
+// The one-warp latency instance runs with a remainder warp at 3-8 samples per SM unless the option
 // turns it off (8 samples + the remainder warp put 3 warps on one SM sub-partition: <= 168
 // registers, still faster: 0.200 against 0.217 ms per AM launch at B = 1100).
 static int samples_per_sm(const bd_ctx* ctx, long long samples) {
@@ -469,9 +469,13 @@ static int samples_per_sm(const bd_ctx* ctx, long long samples) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
     return (int)((samples + sms - 1) / sms);
 }
+#ifndef BD_HELP_MIN
+#define BD_HELP_MIN 3   // 2 per SM is faster too (B = 290: 0.133 vs 0.142 ms) but moves the B <= 296 cases
+                         // the batching-independence tests pin onto another lane mapping
+#endif
 static bool lat_helped(const bd_ctx* ctx, long long samples) {
     const int per_sm = samples_per_sm(ctx, samples);
-    return !ctx->opt_help_off && !ctx->opt_spc && per_sm >= 4 && per_sm <= 8;
+    return !ctx->opt_help_off && !ctx->opt_spc && per_sm >= BD_HELP_MIN && per_sm <= 8;
 }
 
 int dispatch_am(bd_ctx* ctx, AmArgs a, int P, int threads, bool replay_pass, int* occ) {
@@ -502,10 +506,11 @@ int dispatch_am(bd_ctx* ctx, AmArgs a, int P, int threads, bool replay_pass, int
             default: return fail(ctx, BD_ERR_VALUE, "unsupported CTA size %d", threads);
         }
     }
-    // single-scene latency shape, one-warp samples: one CTA of 4-8 samples + the remainder warp per
+    // single-scene latency shape, one-warp samples: one CTA of 3-8 samples + the remainder warp per
     // SM (timesteps 96-99 of every sample, am_helper), <= 255 registers (<= 168 at 8 + 1 warps)
     if (P == 32 && !curv && a.m == 100 && a.n_obs == 10 && lat_helped(ctx, (long long)a.B * ctx->S)) {
         switch (threads) {
+            case 128: return launch_am_t<32, false, 100, 5, 128, true, 4>(ctx, a, threads, replay_pass, occ);
             case 160: return launch_am_t<32, false, 100, 5, 160, true, 4>(ctx, a, threads, replay_pass, occ);
             case 192: return launch_am_t<32, false, 100, 5, 192, true, 4>(ctx, a, threads, replay_pass, occ);
             case 224: return launch_am_t<32, false, 100, 5, 224, true, 4>(ctx, a, threads, replay_pass, occ);
@@ -546,7 +551,8 @@ int default_threads(bd_ctx* ctx, int P, const AmArgs& a) {
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
         const long long per_sm = ((long long)a.B * ctx->S + sms - 1) / sms;
         if (per_sm >= 5 && per_sm <= 8) threads = P * (int)per_sm;
-        else if (P == 32 && per_sm == 4 && lat_helped(ctx, (long long)a.B * ctx->S)) threads = 32 * 4;
+        else if (P == 32 && per_sm >= BD_HELP_MIN && per_sm < 5 && lat_helped(ctx, (long long)a.B * ctx->S))
+            threads = 32 * (int)per_sm;
         if (P == 32 && lat_helped(ctx, (long long)a.B * ctx->S)) threads += 32;   // + the remainder warp
     }
     return threads;
@@ -569,12 +575,12 @@ int pick_lanes(bd_ctx* ctx, const AmArgs& a) {
     if (!ctx->opt_lat_off && a.n_curv == 0 && a.m == 100 && a.n_obs == 10) {
         const long long per_sm = ((long long)total + sms - 1) / sms;
         if (per_sm >= 7 && per_sm <= 8) return 32;
-        // with the remainder warp the one-warp instance also beats the two-warp one at 4-6 per SM
-        // (ms per AM launch: B = 590 0.145 vs 0.167, B = 740 0.167 vs 0.184, B = 888 0.174 vs 0.188;
-        // without it 0.202 / 0.208 at 5 / 6);
+        // with the remainder warp the one-warp instance also beats the two-warp one at 3-6 per SM
+        // (ms per AM launch: B = 440 0.135 vs 0.168, B = 590 0.145 vs 0.167,
+        // B = 740 0.167 vs 0.184, B = 888 0.174 vs 0.188; without it 0.202 / 0.208 at 5 / 6);
         // single-scene cycles only, so a fleet keeps the lane mapping its scenes get when planned
         // one at a time at these sizes (tests/test_gpu_fleet.py: results independent of batching)
-        if (per_sm >= 4 && ctx->S == 1 && lat_helped(ctx, (long long)total)) return 32;
+        if (per_sm >= BD_HELP_MIN && ctx->S == 1 && lat_helped(ctx, (long long)total)) return 32;
     }
     const int cands[4] = {8, 16, 32, 64};
     const double overhead[4] = {0.5, 0.7, 0.9, 1.0};
@@ -1545,7 +1551,7 @@ static int launch_numpy_normals(bd_ctx* ctx, const uint64_t* st4, long long coun
 }
 
 // Single-scene CEM cycle as one cooperative persistent kernel (csrc/cem_persistent.cuh) when the
-// batch maps to one CTA of 4-8 one-warp samples per SM (4-6 only with the remainder warp) on the
+// batch maps to one CTA of 3-8 one-warp samples per SM (3-6 only with the remainder warp) on the
 // BASELINE latency shape; returns 1
 // when the shape does not apply (the caller runs the per-iteration launch chain instead).
 static int try_cem_persistent(bd_ctx* ctx, const bd_cem_config* cfg, const CemState& s, const S1Args& s1, bool s1def,
@@ -1559,7 +1565,7 @@ static int try_cem_persistent(bd_ctx* ctx, const bd_cem_config* cfg, const CemSt
     cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->device);
     const int B = cfg->batch;
     const int spc = (B + sms - 1) / sms;
-    if (!coop || spc < 4 || spc > 8 || (spc < 7 && !lat_helped(ctx, B))) return 1;
+    if (!coop || spc < BD_HELP_MIN || spc > 8 || (spc < 7 && !lat_helped(ctx, B))) return 1;
     const bool help = lat_helped(ctx, B);                           // + the remainder warp per worker
     const int grid = (B + spc - 1) / spc + 1, threads = 32 * (spc + (help ? 1 : 0));   // workers + control
     if (grid > sms) return 1;
@@ -1608,7 +1614,8 @@ static int try_cem_persistent(bd_ctx* ctx, const bd_cem_config* cfg, const CemSt
         return cudaLaunchCooperativeKernel((const void*)kernel, dim3(grid), dim3(threads), args, smem, ctx->stream);
     };
     if (help)
-        e = spc == 4 ? launch(cem_persistent_kernel<160, 4>)
+        e = spc == 3 ? launch(cem_persistent_kernel<128, 4>)
+            : spc == 4 ? launch(cem_persistent_kernel<160, 4>)
             : spc == 5 ? launch(cem_persistent_kernel<192, 4>)
                      : spc == 6 ? launch(cem_persistent_kernel<224, 4>)
                                 : spc == 7 ? launch(cem_persistent_kernel<256, 4>) : launch(cem_persistent_kernel<288, 4>);

@@ -2,12 +2,12 @@
 //
 // Replaces the per-iteration launch chain of bd_cem_cycle -- sample + stage 1, AM pass, replay
 // guard, rank count, rank + refit -- for solve_bilevel's loop (pkg/bilevel.py:249-292) when the
-// batch fills every SM with one CTA of 4-8 one-warp samples (B ~ 450-1200).  All CTAs are
+// batch fills every SM with one CTA of 3-8 one-warp samples (B ~ 300-1200).  All CTAs are
 // co-resident (cooperative launch), so the batch-global steps are grid barriers instead of kernel
 // boundaries, and the serial work of each barrier is done by a dedicated control CTA:
 //
-//   per CEM iteration (worker CTAs: one CTA of 4-8 one-warp samples per SM, + the remainder warp at
-//   4-8; one control CTA)
+//   per CEM iteration (worker CTAs: one CTA of 3-8 one-warp samples per SM, + the remainder warp at
+//   3-8; one control CTA)
 //     S   every warp: draw its set-point (p = mu + z L^T, pkg/bilevel.py:51-57) and solve its
 //         stage-1 QP (pkg/batch_qp.py:209-280), constants staged in shared memory once per launch
 //     A   every warp: the AM projection of its sample (am_samples, the latency instance of K2)

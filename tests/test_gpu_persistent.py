@@ -54,8 +54,8 @@ def _fleet_pair(B, tol=1e-3, seed=3):
     return a, b, used
 
 
-# B = 580 / 730 / 870 / 1000 / 1100: 4 / 5 / 6 / 7 / 8 samples + the remainder warp per SM
-@pytest.mark.parametrize("B", [580, 730, 870, 1000, 1100])
+# B = 430 / 580 / 730 / 870 / 1000 / 1100: 3-8 samples + the remainder warp per SM
+@pytest.mark.parametrize("B", [430, 580, 730, 870, 1000, 1100])
 def test_persistent_cycle_equals_launch_chain_device_rng(B):
     a, b, used = _fleet_pair(B)
     assert used == 1, "the persistent kernel did not run"
@@ -157,9 +157,9 @@ def test_persistent_teacher_forced_config2_against_reference():
     assert _persistent_count(solver.context) - n0 == int(N), "the persistent kernel did not run"
 
 
-@pytest.mark.parametrize("persist,B", [(1, 1000), (0, 1000), (1, 580), (1, 730), (0, 870), (1, 1100)])
+@pytest.mark.parametrize("persist,B", [(1, 1000), (0, 1000), (1, 430), (1, 580), (1, 730), (0, 870), (1, 1100)])
 def test_remainder_warp_matches_plain_latency_instance(persist, B):
-    """4-8 samples per SM: the latency instance with the remainder warp (the last MT mod 32 = 4
+    """3-8 samples per SM: the latency instance with the remainder warp (the last MT mod 32 = 4
     timesteps of every sample on an extra warp, named-barrier handshake, shared-memory column
     sums) against the plain one-warp instance (option remainder_warp = 0), in the persistent kernel
     and in the launch chain.  One CEM iteration: the same best sample and set-points, coefficients
